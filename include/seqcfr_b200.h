@@ -1,0 +1,203 @@
+/*
+ * seqcfr_b200.h — C-ABI of the B200-native sequence-form CFR hot path.
+ *
+ * Drop-in boundary for the reference package `seqcfr` (read-only at
+ * /root/reference/pkg/src/seqcfr).  The reference has no native FFI of its
+ * own: its hot path is Python driving numba loops through the `Backend`
+ * object.  The entry points below replace, at the solver level (SURVEY.md
+ * §8(b) boundary 2):
+ *
+ *   scfr_compile            GameBundle.__init__           pkg/solvers.py:314-323
+ *                           (DecisionProcess._extract     pkg/decision_process.py:76-242,
+ *                            build_payoff_matrix          pkg/operators.py:164-180,
+ *                            CsrMatrix.from_coo/transposed pkg/kernels.py:95-127)
+ *   scfr_create             RegretState x2 allocation     pkg/solvers.py:97-127, :404-405
+ *   scfr_step               the `while True: _step(...)`  pkg/solvers.py:351-372, :424-434
+ *   scfr_read_average       RegretState.average_strategy  pkg/solvers.py:129-134
+ *   scfr_read_current       the x1, x2 returned by _step  pkg/solvers.py:372
+ *   scfr_exploitability     metrics.exploitability        pkg/metrics.py:59-75
+ *                           (+ oracle.scalar_best_response pkg/oracle.py:186-221)
+ *   scfr_status             FloatingPointError checks     pkg/solvers.py:154-155, :188-189
+ *
+ * Conventions
+ *   - Every function returns an int status: 0 on success, a negative
+ *     SCFR_E* code on failure; scfr_last_error() gives the message of the
+ *     calling thread's most recent failure.  SCFR_EINVAL maps to the
+ *     reference's ValueError, SCFR_EGAME to GameValidationError and
+ *     SCFR_ENONFINITE to FloatingPointError.
+ *   - Arrays use the reference's dtypes (int64 indices, float64 values) and
+ *     index layout (DecisionProcess ids, Σ-indexed sequence vectors with
+ *     slot 0 = the empty sequence), so a reference maintainer can pass its
+ *     numpy arrays' buffers straight through.
+ *   - The caller keeps ownership of every input pointer; the library copies.
+ *   - Handles are independent; one host thread drives a handle at a time.
+ *   - No CPU fallback: without a usable sm_100 device, scfr_create fails with
+ *     SCFR_ECUDA.
+ */
+#ifndef SEQCFR_B200_H
+#define SEQCFR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCFR_ABI_VERSION 1
+
+#define SCFR_OK 0
+#define SCFR_EINVAL (-1)     /* bad argument / dimension mismatch (ValueError) */
+#define SCFR_EGAME (-2)      /* invalid game, e.g. perfect recall (GameValidationError) */
+#define SCFR_ENONFINITE (-3) /* non-finite regrets or utilities (FloatingPointError) */
+#define SCFR_ECUDA (-4)      /* CUDA runtime failure / no device */
+#define SCFR_ENOMEM (-5)
+#define SCFR_ENCCL (-6)
+
+/* Variants (pkg/solvers.py:35) and update modes (pkg/solvers.py:38-44). */
+#define SCFR_CFR 0
+#define SCFR_CFR_PLUS 1
+#define SCFR_DCFR 2
+#define SCFR_PCFR 3
+#define SCFR_PCFR_PLUS 4
+#define SCFR_MODE_SIM 0
+#define SCFR_MODE_ALT 1
+
+/* Node kinds of the input game (pkg/games.py:23-25). */
+#define SCFR_NODE_CHANCE 0
+#define SCFR_NODE_DECISION 1
+#define SCFR_NODE_TERMINAL 2
+
+/* Engines (scfr_config.engine). */
+#define SCFR_ENGINE_AUTO 0
+#define SCFR_ENGINE_LEVELS 1     /* one kernel per DP level, captured in a CUDA graph */
+#define SCFR_ENGINE_PERSISTENT 2 /* whole iterations inside one cooperative kernel */
+
+const char* scfr_last_error(void);
+int scfr_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Tree compiler (host).  Input: the reference Game flattened to columns
+ * (paper_2605_14277_b200.games.FlatGame).  Output: both players' decision
+ * processes, bit-identical to DecisionProcess, plus U and Uᵀ bit-identical
+ * to build_payoff_matrix(...) and CsrMatrix.transposed().
+ * ---------------------------------------------------------------------- */
+typedef struct scfr_game {
+    int64_t num_nodes;
+    const int8_t* kind;       /* SCFR_NODE_* */
+    const int64_t* parent;    /* -1 at the root (node 0) */
+    const int64_t* child_ptr; /* [num_nodes+1] */
+    const int64_t* child_idx; /* children in GameNode.children order */
+    const int8_t* player;     /* 1/2 at decision nodes */
+    const int64_t* infoset;   /* interned infoset label id at decision nodes, -1 elsewhere */
+    const double* prob;       /* chance-edge probability, NaN when absent */
+    const double* payoff;     /* payoff to player 1 at terminals, NaN elsewhere */
+} scfr_game;
+
+/* One player's tree-form sequential decision process, in the reference
+ * DecisionProcess layout (pkg/decision_process.py:48-65). */
+typedef struct scfr_tfsdp {
+    int64_t num_nodes, num_decisions, num_seqs, height, degree;
+    const int8_t* kind;            /* [num_nodes] 0 decision / 1 observation / 2 end */
+    const int64_t* depth;          /* [num_nodes] */
+    const int64_t* parent;         /* [num_nodes] */
+    const int64_t* node_seq;       /* [num_nodes] */
+    const int64_t* seq_node;       /* [num_seqs] */
+    const int64_t* dp_node;        /* [num_decisions] */
+    const int64_t* dp_first_seq;   /* [num_decisions] */
+    const int64_t* dp_num_actions; /* [num_decisions] */
+    const int64_t* dp_parent_seq;  /* [num_decisions] */
+    const int64_t* level_starts;   /* [height+2] */
+    const int64_t* game_seq;       /* [game num_nodes] (compiler output only) */
+    const int64_t* dp_infoset;     /* [num_decisions] infoset id (compiler output only) */
+    const int64_t* dp_game_node;   /* [num_decisions] first game node of the infoset */
+} scfr_tfsdp;
+
+/* CSR over float64 (pkg/kernels.py:33-49). */
+typedef struct scfr_csr {
+    int64_t rows, cols, nnz;
+    const int64_t* indptr;  /* [rows+1] */
+    const int64_t* indices; /* [nnz] */
+    const double* data;     /* [nnz] */
+} scfr_csr;
+
+typedef struct scfr_compiled scfr_compiled;
+
+int scfr_compile(const scfr_game* game, scfr_compiled** out);
+/* Views stay valid until scfr_compiled_free. player is 1 or 2. */
+int scfr_compiled_tfsdp(const scfr_compiled* c, int player, scfr_tfsdp* out);
+int scfr_compiled_payoff(const scfr_compiled* c, int transposed, scfr_csr* out);
+void scfr_compiled_free(scfr_compiled* c);
+
+/* Native generators for the large fixtures, emitting
+ * the same trees as paper_2605_14277_b200.games.liars_dice / goofspiel. */
+typedef struct scfr_flat_game {
+    scfr_game game;
+    int64_t num_infosets;
+} scfr_flat_game;
+int scfr_generate_liars_dice(int faces, scfr_flat_game** out);
+int scfr_generate_goofspiel(int cards, scfr_flat_game** out);
+void scfr_flat_game_free(scfr_flat_game* g);
+
+/* ------------------------------------------------------------------------
+ * Solver (device).
+ * ---------------------------------------------------------------------- */
+typedef struct scfr_config {
+    int32_t variant; /* SCFR_CFR .. SCFR_PCFR_PLUS */
+    int32_t mode;    /* SCFR_MODE_SIM / SCFR_MODE_ALT */
+    double alpha, beta, gamma;
+    int32_t batch;   /* independent solves sharing the structure (>= 1) */
+    /* Per-solve DCFR/averaging parameters, [batch] each, or NULL to use the
+     * scalars above for every solve. */
+    const double* batch_alpha;
+    const double* batch_beta;
+    const double* batch_gamma;
+    int32_t engine;  /* SCFR_ENGINE_* */
+    int32_t reserved[7];
+} scfr_config;
+
+typedef struct scfr_handle scfr_handle;
+
+/* Copies the structure to `device` and allocates the state of `batch`
+ * solves, each initialised like RegretState (t=1, zero regrets, uniform
+ * behaviour, zero averages). */
+int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                const scfr_csr* UT, const scfr_config* cfg, int device,
+                scfr_handle** out);
+/* Runs n full iterations (_step semantics incl. t++ for both players) on the
+ * handle's stream; asynchronous. */
+int scfr_step(scfr_handle* h, int64_t n_iter);
+int scfr_synchronize(scfr_handle* h);
+/* Completed iterations (the reference's RegretState.t - 1). */
+int scfr_iterations(const scfr_handle* h, int64_t* out);
+/* Normalised average strategy avg_accum / avg_weight over Σ (player 1/2). */
+int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out);
+/* The sequence-form strategy emitted by the last iteration (x1/x2 of _step). */
+int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out);
+#define SCFR_STATE_REGRETS 0  /* [num_seqs-1]  RegretState.regrets   */
+#define SCFR_STATE_BEHAVIOR 1 /* [num_seqs-1]  RegretState.behavior  */
+#define SCFR_STATE_ACCUM 2    /* [num_seqs]    RegretState.avg_accum */
+#define SCFR_STATE_UTILITY 3  /* [num_seqs]    u of the last iteration (the next prediction) */
+int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* host_out);
+int scfr_avg_weight(const scfr_handle* h, int player, int solve, double* out);
+/* NashConv/2 of the average (which=0) or last emitted (which=1) profile,
+ * computed on the device; br1/br2 may be NULL. */
+int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl,
+                        double* br1, double* br2);
+/* Player-1 expected value x1ᵀ U x2 of the average profile (metrics.expected_value). */
+int scfr_expected_value(scfr_handle* h, int solve, double* out);
+/* Non-finite flag raised by any kernel since creation (FloatingPointError). */
+int scfr_status(scfr_handle* h, int* nonfinite);
+/* Device bytes held by the handle (structure + state). */
+int scfr_device_bytes(const scfr_handle* h, int64_t* out);
+/* Number of kernel launches issued by scfr_step so far (graph nodes count
+ * individually). */
+int scfr_launch_count(const scfr_handle* h, int64_t* out);
+/* Kernel-only device time of the last scfr_step in ms (CUDA events on the
+ * handle's stream), and the summed duration of the payoff-SpMV kernels. */
+int scfr_last_step_ms(scfr_handle* h, double* total_ms);
+int scfr_destroy(scfr_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEQCFR_B200_H */
