@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark: CFR iterations/sec on the largest single-GPU config.
+
+Workload (default): Goofspiel-5 (bids revealed, random prize order, win/loss;
+8 530 656 game nodes, |Σ| = 2 666 026 per player, nnz(U) = 1 728 000), PCFR+
+alternating, gamma = 2, fp64 — BASELINE.json configs[3] on one GPU.  A step is
+one full CFR iteration (reference ``_step``, pkg/solvers.py:351-372).  The
+working set (~1 GB/iteration) is far above the 126 MB L2, so no L2 flush is
+needed between iterations.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload ...]
+
+N > 1 (torchrun, one rank per GPU): every rank runs an independent replica of
+the solve (no collective on the data path; weak scaling), value = all ranks'
+iterations / max-over-ranks device time.
+
+``--impl reference`` times the reference algorithm's CPU implementation on the
+host cores: the C oracle (a port of the reference's per-iteration path,
+oracle/seqcfr_oracle.c, pinned bit-exact to the reference by tests/) with all
+host threads; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (description, builder, variant)
+    "goofspiel5": ("goofspiel-5 pcfr+ alt (bids revealed, random prize order, win/loss)", "goof", "pcfr+"),
+    "liars_dice": ("liars-dice 1x1x6 dcfr(1.5,0,2) alt", "liars", "dcfr"),
+    "leduc": ("leduc cfr+ alt", "leduc", "cfr+"),
+    "kuhn": ("kuhn cfr sim", "kuhn", "cfr"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_bundle(kind: str):
+    from paper_2605_14277_b200 import GameBundle, flat_goofspiel, flat_liars_dice, kuhn_poker, leduc_poker
+    if kind == "goof":
+        return GameBundle(flat_goofspiel(5))
+    if kind == "liars":
+        return GameBundle(flat_liars_dice(6))
+    if kind == "leduc":
+        return GameBundle(leduc_poker())
+    return GameBundle(kuhn_poker())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+        self.window = None
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append((time.time(), out.split(", ")))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self, t0: float, t1: float) -> dict:
+        rows = [s for (t, s) in self.samples if t0 <= t <= t1] or [s for (_, s) in self.samples]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: float | None,
+                    threads: int):
+    """The oracle port on the host cores: iterations/sec over a bounded sample."""
+    from oracle.oracle import OracleSolver
+    o = OracleSolver(bundle, variant, threads=threads)
+    if warmup:
+        o.step(warmup)
+    if budget_s is not None:
+        t0 = time.perf_counter()
+        o.step(1)
+        one = time.perf_counter() - t0
+        steps = max(1, min(steps, int(budget_s / max(one, 1e-9))))
+    t0 = time.perf_counter()
+    o.step(steps)
+    dt = time.perf_counter() - t0
+    return steps / dt, steps, dt
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    desc, kind, variant = WORKLOADS[args.workload]
+    bundle = make_bundle(kind)
+    threads = os.cpu_count() or 1
+    rate, steps, dt = cpu_oracle_rate(bundle, variant, args.steps, args.warmup, None, threads)
+    line = {
+        "impl": "reference", "metric": "cfr_iterations_per_sec", "value": rate,
+        "unit": "iterations/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated game tree)",
+        "config": {"workload": desc, "variant": variant, "parallelism": "host threads"},
+        "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} {args.workload} iterations after {args.warmup} warm-up "
+                                   f"(oracle/seqcfr_oracle.c, bit-exact port of the reference path)"},
+        "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local
+    from paper_2605_14277_b200 import Solver, SolverConfig, native
+
+    desc, kind, variant = WORKLOADS[args.workload]
+    bundle = make_bundle(kind)
+    cfg = SolverConfig(variant)
+    h2d0, d2h0 = native.transfer_bytes()
+
+    # --- end-to-end through the public API: upload (create) + K iterations +
+    # read back both average strategies; wall clock, host buffers.
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    s = Solver(bundle, cfg, device=device)
+    s.step(args.steps)
+    avg = (s.average(1), s.average(2))
+    e2e_s = time.perf_counter() - t0
+    h2d1, d2h1 = native.transfer_bytes()
+    del avg
+    s.close()
+
+    # --- device-timed region
+    s = Solver(bundle, cfg, device=device)
+    s.step(args.warmup)
+    s.synchronize()
+    sampler = ClockSampler(device)
+    sampler.start()
+    soak_end = time.time() + args.soak
+    while time.time() < soak_end:  # keep the GPU loaded while the clock sampler warms up
+        s.step(max(1, args.warmup))
+        s.synchronize()
+    launches0 = s.launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    tw0 = time.time()
+    s.step(args.steps)
+    s.synchronize()
+    tw1 = time.time()
+    ms = s.last_step_ms()
+    launches = s.launch_count() - launches0
+    sampler.stop()
+    clocks = sampler.summary(tw0 - args.soak, tw1)
+    ms_max = ms
+    e2e_max = e2e_s
+    if dist:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max, e2e_max = float(t[0]), float(t[1])
+
+    # --- per-kernel roofline (CUDA events around every launch, same stream)
+    prof = s.profile(args.profile_iters)
+    peak, peak_kind = _peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+    step_bytes = sum(v["bytes"] for v in prof.values()) / args.profile_iters
+    prof_ms = sum(v["ms"] for v in prof.values()) / args.profile_iters
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as fh:
+                tj = json.load(fh)
+            if args.workload in tj and dname in tj[args.workload]:
+                traffic = tj[args.workload][dname]
+        except Exception:
+            traffic = None
+
+    value = ws * args.steps / (ms_max / 1e3)
+    line = {
+        "metric": "cfr_iterations_per_sec", "value": value, "unit": "iterations/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated game tree)",
+        "config": {"workload": desc, "variant": variant, "mode": cfg.mode, "gamma": cfg.gamma,
+                   "seqs_per_player": [p.num_seqs for p in bundle.procs],
+                   "nnz_U": bundle.payoff.nnz, "parallelism": f"replicas x{ws}" if ws > 1 else "1 gpu",
+                   "l2": "working set > L2 (no flush needed)",
+                   "engine": "levels+cuda-graph"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": {"value": ws * args.steps / e2e_max, "unit": "iterations/s",
+                "h2d_bytes_per_step": (h2d1 - h2d0) / args.steps,
+                "d2h_bytes_per_step": (d2h1 - d2h0) / args.steps,
+                "includes": "scfr_create upload + K iterations + average-strategy readback, wall clock"},
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "step": {"algorithmic_bytes": step_bytes, "profiled_ms": prof_ms,
+                              "achieved_gbs": step_bytes / (prof_ms / 1e3) / 1e9,
+                              "frac": step_bytes / (prof_ms / 1e3) / 1e9 / peak},
+                     "kernels": {k: {"launches": v["launches"] // args.profile_iters,
+                                     "ms": v["ms"] / args.profile_iters,
+                                     "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
+                                 for k, v in prof.items()}},
+    }
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, steps, dt = cpu_oracle_rate(bundle, variant, 50, 1, args.cpu_budget, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"{steps} {args.workload} iterations after 1 warm-up, "
+                                          f"{dt:.1f}s (oracle/seqcfr_oracle.c)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="goofspiel5")
+    ap.add_argument("--profile-iters", type=int, default=3)
+    ap.add_argument("--soak", type=float, default=1.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -185,6 +185,12 @@ int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl,
                         double* br1, double* br2);
 /* Player-1 expected value x1ᵀ U x2 of the average profile (metrics.expected_value). */
 int scfr_expected_value(scfr_handle* h, int solve, double* out);
+/* Best-response values of both players against an arbitrary host profile
+ * (x1 over Σ1, x2 over Σ2): metrics.best_response_values, pkg/metrics.py:59-68. */
+int scfr_best_response_values(scfr_handle* h, const double* x1, const double* x2, double* br1,
+                              double* br2);
+/* x1ᵀ (U x2) for an arbitrary host profile (metrics.expected_value, pkg/metrics.py:50-56). */
+int scfr_expected_value_of(scfr_handle* h, const double* x1, const double* x2, double* out);
 /* Non-finite flag raised by any kernel since creation (FloatingPointError). */
 int scfr_status(scfr_handle* h, int* nonfinite);
 /* Device bytes held by the handle (structure + state). */
@@ -195,6 +201,20 @@ int scfr_launch_count(const scfr_handle* h, int64_t* out);
 /* Kernel-only device time of the last scfr_step in ms (CUDA events on the
  * handle's stream), and the summed duration of the payoff-SpMV kernels. */
 int scfr_last_step_ms(scfr_handle* h, double* total_ms);
+/* Runs n iterations (real ones: state advances) without the graph, timing
+ * every kernel launch with CUDA events on the handle's stream; aggregates
+ * per kernel kind (td_avg, td, cur, obs_rm, obs, pred, spmv, tick): launch
+ * count, summed device ms and algorithmic HBM bytes. */
+typedef struct scfr_kernel_stat {
+    char name[16];
+    int64_t launches;
+    double ms;
+    double bytes;
+} scfr_kernel_stat;
+int scfr_profile_step(scfr_handle* h, int64_t n_iter, scfr_kernel_stat* out, int cap, int* count);
+/* Process-wide bytes copied host->device and device->host by this library
+ * (structure uploads, state reads); used for the end-to-end accounting. */
+int scfr_transfer_bytes(int64_t* h2d, int64_t* d2h);
 int scfr_destroy(scfr_handle* h);
 
 #ifdef __cplusplus

@@ -1,0 +1,366 @@
+// Tree compiler: flattened game -> per-player TFSDP arrays + payoff CSR.
+//
+// Output is bit-identical to the reference's compile step
+// (GameBundle.__init__, pkg/solvers.py:314-323):
+//   * DecisionProcess._extract        pkg/decision_process.py:76-242
+//   * build_payoff_matrix             pkg/operators.py:164-180
+//   * CsrMatrix.from_coo / transposed pkg/kernels.py:95-127
+//   * Game.chance_reach               pkg/games.py:93-103
+// The numbering rules (BFS over the game for infoset discovery, BFS over the
+// process tree for node / sequence / decision-point ids) are what makes every
+// depth a contiguous id range; the kernels rely on that.
+//
+// Everything is linear-time array code (no per-node heap objects), so
+// Goofspiel-5 (8.5 M game nodes) compiles in about a second instead of the
+// reference's minutes.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace scfr {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+struct Tfsdp {
+    int64_t num_nodes = 0, num_decisions = 0, num_seqs = 0, height = 0, degree = 0;
+    std::vector<int8_t> kind;
+    std::vector<int64_t> depth, parent, node_seq, seq_node;
+    std::vector<int64_t> dp_node, dp_first_seq, dp_num_actions, dp_parent_seq;
+    std::vector<int64_t> level_starts, game_seq, dp_infoset, dp_game_node;
+};
+
+struct Csr {
+    int64_t rows = 0, cols = 0;
+    std::vector<int64_t> indptr, indices;
+    std::vector<double> data;
+};
+
+}  // namespace scfr
+
+struct scfr_compiled {
+    scfr::Tfsdp proc[2];
+    scfr::Csr U, UT;
+};
+
+namespace scfr {
+
+static const int8_t K_DEC = 0, K_OBS = 1, K_END = 2;
+
+static void check_game(const scfr_game* g) {
+    if (!g || g->num_nodes <= 0) fail(SCFR_EGAME, "empty game");
+    if (!g->kind || !g->parent || !g->child_ptr || !g->child_idx || !g->player ||
+        !g->infoset || !g->prob || !g->payoff)
+        fail(SCFR_EINVAL, "scfr_game has a NULL array");
+    const int64_t n = g->num_nodes;
+    if (g->child_ptr[0] != 0) fail(SCFR_EINVAL, "child_ptr[0] must be 0");
+    for (int64_t i = 0; i < n; ++i) {
+        if (g->child_ptr[i + 1] < g->child_ptr[i]) fail(SCFR_EINVAL, "child_ptr must be non-decreasing");
+        if (g->kind[i] < 0 || g->kind[i] > 2) fail(SCFR_EGAME, "node %lld: unknown kind", (long long)i);
+        if (i && (g->parent[i] < 0 || g->parent[i] >= n)) fail(SCFR_EGAME, "node %lld: invalid parent id", (long long)i);
+    }
+    const int64_t m = g->child_ptr[n];
+    for (int64_t k = 0; k < m; ++k)
+        if (g->child_idx[k] <= 0 || g->child_idx[k] >= n) fail(SCFR_EGAME, "child id out of range");
+}
+
+// DecisionProcess._extract for one player (pkg/decision_process.py:76-242).
+static void extract(const scfr_game* g, int player, Tfsdp& P) {
+    const int64_t n = g->num_nodes;
+    const int64_t* cp = g->child_ptr;
+    const int64_t* ci = g->child_idx;
+
+    int64_t max_inf = -1;
+    for (int64_t i = 0; i < n; ++i)
+        if (g->kind[i] == SCFR_NODE_DECISION) {
+            if (g->infoset[i] < 0) fail(SCFR_EGAME, "node %lld: decision node needs an infoset", (long long)i);
+            max_inf = std::max(max_inf, g->infoset[i]);
+        }
+    std::vector<int32_t> pid_of(max_inf + 1, -1);
+
+    // --- game walk: provisional infoset ids (pid) in BFS discovery order and
+    // the player's last provisional sequence key per game node (0 = empty).
+    std::vector<int64_t> order;
+    order.reserve(n);
+    order.push_back(0);
+    std::vector<int64_t> prov(n, 0);
+    std::vector<int64_t> first_key, parent_key, nact, first_node;
+    std::vector<int64_t> pair_key, pair_pid;  // children_of_key as (key, pid) in discovery order
+    int64_t next_key = 1;
+    for (size_t h = 0; h < order.size(); ++h) {
+        const int64_t v = order[h];
+        const bool mine = g->kind[v] == SCFR_NODE_DECISION && g->player[v] == player;
+        int64_t pid = -1;
+        if (mine) {
+            const int64_t key = prov[v];
+            pid = pid_of[g->infoset[v]];
+            if (pid < 0) {
+                pid = (int64_t)first_key.size();
+                pid_of[g->infoset[v]] = (int32_t)pid;
+                first_key.push_back(next_key);
+                parent_key.push_back(key);
+                nact.push_back(cp[v + 1] - cp[v]);
+                first_node.push_back(v);
+                next_key += cp[v + 1] - cp[v];
+                pair_key.push_back(key);
+                pair_pid.push_back(pid);
+            } else if (parent_key[pid] != key) {
+                fail(SCFR_EGAME, "node %lld: perfect recall violated in infoset %lld", (long long)v,
+                     (long long)g->infoset[v]);
+            }
+        }
+        for (int64_t k = cp[v]; k < cp[v + 1]; ++k) {
+            const int64_t c = ci[k];
+            prov[c] = mine ? first_key[pid] + (k - cp[v]) : prov[v];
+            order.push_back(c);
+            if ((int64_t)order.size() > n) fail(SCFR_EGAME, "not a tree: node has two parents");
+        }
+    }
+    if ((int64_t)order.size() != n) fail(SCFR_EGAME, "not a tree: node unreachable from root");
+
+    // children_of_key as CSR over keys, stable in discovery order.
+    const int64_t n_pid = (int64_t)first_key.size();
+    std::vector<int64_t> kptr(next_key + 1, 0), kpid(n_pid);
+    for (int64_t i = 0; i < n_pid; ++i) kptr[pair_key[i] + 1]++;
+    for (int64_t k = 0; k < next_key; ++k) kptr[k + 1] += kptr[k];
+    {
+        std::vector<int64_t> fill(kptr.begin(), kptr.end() - 1);
+        for (int64_t i = 0; i < n_pid; ++i) kpid[fill[pair_key[i]]++] = pair_pid[i];
+    }
+
+    // --- breadth-first assembly of the process tree.
+    int64_t num_seqs = 1;
+    for (int64_t p = 0; p < n_pid; ++p) num_seqs += nact[p];
+    P.seq_node.assign(num_seqs, -1);
+    P.dp_node.assign(n_pid, 0);
+    P.dp_first_seq.assign(n_pid, 0);
+    P.dp_num_actions.assign(n_pid, 0);
+    P.dp_parent_seq.assign(n_pid, 0);
+    P.dp_infoset.assign(n_pid, 0);
+    P.dp_game_node.assign(n_pid, 0);
+    std::vector<int64_t> j_of_pid(n_pid, -1);
+    P.kind.clear();
+    P.depth.clear();
+    P.parent.clear();
+    P.node_seq.clear();
+
+    struct Item {
+        int64_t a, par, d, b;  // seq item: (seq, par, d, key); dp item: (pid, par, d, parent_seq)
+        bool is_seq;
+    };
+    std::vector<Item> q;
+    q.reserve(num_seqs + n_pid + 1);
+    int64_t next_j = 0, next_seq = 1;
+
+    auto new_node = [&](int8_t k, int64_t par, int64_t d, int64_t seq) {
+        const int64_t nid = (int64_t)P.kind.size();
+        P.kind.push_back(k);
+        P.parent.push_back(par);
+        P.depth.push_back(d);
+        P.node_seq.push_back(seq);
+        if (seq >= 0) P.seq_node[seq] = nid;
+        return nid;
+    };
+    auto open_decision = [&](int64_t pid, int64_t par, int64_t d, int64_t parent_seq, int64_t seq) {
+        const int64_t nid = new_node(K_DEC, par, d, seq);
+        const int64_t j = next_j++;
+        j_of_pid[pid] = j;
+        P.dp_node[j] = nid;
+        P.dp_first_seq[j] = next_seq;
+        P.dp_num_actions[j] = nact[pid];
+        P.dp_parent_seq[j] = parent_seq;
+        P.dp_infoset[j] = g->infoset[first_node[pid]];
+        P.dp_game_node[j] = first_node[pid];
+        for (int64_t a = 0; a < nact[pid]; ++a)
+            q.push_back({next_seq + a, nid, d + 1, first_key[pid] + a, true});
+        next_seq += nact[pid];
+    };
+
+    q.push_back({0, -1, 0, 0, true});
+    for (size_t h = 0; h < q.size(); ++h) {
+        const Item it = q[h];
+        if (it.is_seq) {
+            const int64_t lo = it.b < next_key ? kptr[it.b] : 0;
+            const int64_t hi = it.b < next_key ? kptr[it.b + 1] : 0;
+            if (hi == lo) {
+                new_node(K_END, it.par, it.d, it.a);
+            } else if (hi - lo == 1) {
+                open_decision(kpid[lo], it.par, it.d, it.a, it.a);
+            } else {
+                const int64_t nid = new_node(K_OBS, it.par, it.d, it.a);
+                for (int64_t k = lo; k < hi; ++k) q.push_back({kpid[k], nid, it.d + 1, it.a, false});
+            }
+        } else {
+            open_decision(it.a, it.par, it.d, it.b, -1);
+        }
+    }
+
+    P.num_nodes = (int64_t)P.kind.size();
+    P.num_decisions = n_pid;
+    P.num_seqs = num_seqs;
+    P.height = 0;
+    for (int64_t d : P.depth) P.height = std::max(P.height, d);
+    {
+        std::vector<int64_t> cnt(P.num_nodes, 0);
+        for (int64_t i = 1; i < P.num_nodes; ++i) cnt[P.parent[i]]++;
+        P.degree = P.num_nodes > 1 ? *std::max_element(cnt.begin(), cnt.end()) : 0;
+    }
+    // level_starts = searchsorted(depth, arange(height+2)) (depth is sorted).
+    P.level_starts.assign(P.height + 2, 0);
+    for (int64_t d = 0; d <= P.height + 1; ++d)
+        P.level_starts[d] = std::lower_bound(P.depth.begin(), P.depth.end(), d) - P.depth.begin();
+    // game_seq = final_of_key[prov]
+    std::vector<int64_t> final_of_key(next_key, 0);
+    for (int64_t pid = 0; pid < n_pid; ++pid) {
+        const int64_t j = j_of_pid[pid];
+        for (int64_t a = 0; a < nact[pid]; ++a) final_of_key[first_key[pid] + a] = P.dp_first_seq[j] + a;
+    }
+    P.game_seq.resize(n);
+    for (int64_t v = 0; v < n; ++v) P.game_seq[v] = final_of_key[prov[v]];
+}
+
+// build_payoff_matrix + CsrMatrix.from_coo + transposed.
+static void payoff(const scfr_game* g, const Tfsdp& P1, const Tfsdp& P2, Csr& U, Csr& UT) {
+    const int64_t n = g->num_nodes;
+    // chance_reach in node-id order (pkg/games.py:93-103).
+    std::vector<double> reach(n, 1.0);
+    for (int64_t i = 1; i < n; ++i) {
+        double p = reach[g->parent[i]];
+        if (!std::isnan(g->prob[i])) p = p * g->prob[i];
+        reach[i] = p;
+    }
+    std::vector<int64_t> r, c;
+    std::vector<double> v;
+    for (int64_t z = 0; z < n; ++z)
+        if (g->kind[z] == SCFR_NODE_TERMINAL) {
+            r.push_back(P1.game_seq[z]);
+            c.push_back(P2.game_seq[z]);
+            v.push_back(g->payoff[z] * reach[z]);
+        }
+    const int64_t m = (int64_t)r.size();
+    const int64_t R = P1.num_seqs, C = P2.num_seqs;
+    // Stable lexsort by (row, col): LSD counting sorts, col then row.
+    std::vector<int64_t> idx(m), tmp(m);
+    {
+        std::vector<int64_t> cnt(C + 1, 0);
+        for (int64_t k = 0; k < m; ++k) cnt[c[k] + 1]++;
+        for (int64_t k = 0; k < C; ++k) cnt[k + 1] += cnt[k];
+        for (int64_t k = 0; k < m; ++k) tmp[cnt[c[k]]++] = k;
+        std::vector<int64_t> cr(R + 1, 0);
+        for (int64_t k = 0; k < m; ++k) cr[r[k] + 1]++;
+        for (int64_t k = 0; k < R; ++k) cr[k + 1] += cr[k];
+        for (int64_t k = 0; k < m; ++k) idx[cr[r[tmp[k]]]++] = tmp[k];
+    }
+    // Sum duplicate cells sequentially from 0.0 (np.bincount with weights).
+    U.rows = R;
+    U.cols = C;
+    U.indptr.assign(R + 1, 0);
+    U.indices.clear();
+    U.data.clear();
+    for (int64_t k = 0; k < m;) {
+        const int64_t rr = r[idx[k]], cc = c[idx[k]];
+        double acc = 0.0;
+        while (k < m && r[idx[k]] == rr && c[idx[k]] == cc) acc = acc + v[idx[k++]];
+        U.indices.push_back(cc);
+        U.data.push_back(acc);
+        U.indptr[rr + 1]++;
+    }
+    for (int64_t k = 0; k < R; ++k) U.indptr[k + 1] += U.indptr[k];
+    // Stable transpose (argsort of column indices, kind="stable").
+    const int64_t nnz = (int64_t)U.data.size();
+    UT.rows = C;
+    UT.cols = R;
+    UT.indptr.assign(C + 1, 0);
+    UT.indices.assign(nnz, 0);
+    UT.data.assign(nnz, 0.0);
+    for (int64_t k = 0; k < nnz; ++k) UT.indptr[U.indices[k] + 1]++;
+    for (int64_t k = 0; k < C; ++k) UT.indptr[k + 1] += UT.indptr[k];
+    std::vector<int64_t> fill(UT.indptr.begin(), UT.indptr.end() - 1);
+    for (int64_t row = 0; row < R; ++row)
+        for (int64_t k = U.indptr[row]; k < U.indptr[row + 1]; ++k) {
+            const int64_t dst = fill[U.indices[k]]++;
+            UT.indices[dst] = row;
+            UT.data[dst] = U.data[k];
+        }
+}
+
+static void fill_view(const Tfsdp& P, scfr_tfsdp* o) {
+    o->num_nodes = P.num_nodes;
+    o->num_decisions = P.num_decisions;
+    o->num_seqs = P.num_seqs;
+    o->height = P.height;
+    o->degree = P.degree;
+    o->kind = P.kind.data();
+    o->depth = P.depth.data();
+    o->parent = P.parent.data();
+    o->node_seq = P.node_seq.data();
+    o->seq_node = P.seq_node.data();
+    o->dp_node = P.dp_node.data();
+    o->dp_first_seq = P.dp_first_seq.data();
+    o->dp_num_actions = P.dp_num_actions.data();
+    o->dp_parent_seq = P.dp_parent_seq.data();
+    o->level_starts = P.level_starts.data();
+    o->game_seq = P.game_seq.data();
+    o->dp_infoset = P.dp_infoset.data();
+    o->dp_game_node = P.dp_game_node.data();
+}
+
+}  // namespace scfr
+
+using namespace scfr;
+
+extern "C" {
+
+const char* scfr_last_error(void) { return g_last_error.c_str(); }
+int scfr_abi_version(void) { return SCFR_ABI_VERSION; }
+
+int scfr_compile(const scfr_game* game, scfr_compiled** out) {
+    return guarded([&] {
+        if (!out) fail(SCFR_EINVAL, "out is NULL");
+        check_game(game);
+        auto* c = new scfr_compiled();
+        try {
+            extract(game, 1, c->proc[0]);
+            extract(game, 2, c->proc[1]);
+            payoff(game, c->proc[0], c->proc[1], c->U, c->UT);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int scfr_compiled_tfsdp(const scfr_compiled* c, int player, scfr_tfsdp* out) {
+    return guarded([&] {
+        if (!c || !out || (player != 1 && player != 2)) fail(SCFR_EINVAL, "bad arguments");
+        fill_view(c->proc[player - 1], out);
+    });
+}
+
+int scfr_compiled_payoff(const scfr_compiled* c, int transposed, scfr_csr* out) {
+    return guarded([&] {
+        if (!c || !out) fail(SCFR_EINVAL, "bad arguments");
+        const Csr& m = transposed ? c->UT : c->U;
+        out->rows = m.rows;
+        out->cols = m.cols;
+        out->nnz = (int64_t)m.data.size();
+        out->indptr = m.indptr.data();
+        out->indices = m.indices.data();
+        out->data = m.data.data();
+    });
+}
+
+void scfr_compiled_free(scfr_compiled* c) { delete c; }
+
+}  // extern "C"

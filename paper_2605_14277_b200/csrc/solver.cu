@@ -1,0 +1,926 @@
+// Device runtime behind the C-ABI: structure upload, per-iteration kernel
+// schedule captured as a CUDA graph, on-device best response.
+//
+// One iteration is the reference _step (pkg/solvers.py:351-372):
+//   sim:  next1, next2, u1 = U x2, u2 = -Uᵀ x1, observe1(u1), observe2(u2)
+//   alt:  next1, next2, u1 = U x2, observe1(u1), x1' = current1(),
+//         u2 = -Uᵀ x1', observe2(u2)
+// mapped onto fused per-level kernels (kernels.cuh):
+//   next    = [PRED levels deep→shallow, if predictive] + TD levels (+avg)
+//   observe = OBS levels deep→shallow (+ RM into b for non-predictive)
+//   current = CUR levels (predictive) / TD levels without avg (otherwise:
+//             b was already regret-matched by OBS)
+// Per-iteration scalars (t^gamma, DCFR factors) come from host-computed
+// schedules indexed by a device-side iteration counter, so one captured
+// graph serves every iteration.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "persistent.cuh"
+
+namespace scfr {
+
+#define CUDA_OK(expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            ::scfr::fail(SCFR_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));      \
+    } while (0)
+
+constexpr int TPB = 128;
+
+// Process-wide host<->device byte counters (scfr_transfer_bytes).
+static std::atomic<int64_t> g_h2d{0}, g_d2h{0};
+static void count_copy(size_t n, cudaMemcpyKind k) {
+    if (k == cudaMemcpyHostToDevice) g_h2d += (int64_t)n;
+    else if (k == cudaMemcpyDeviceToHost) g_d2h += (int64_t)n;
+}
+static cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t s) {
+    count_copy(n, k);
+    return cudaMemcpyAsync(dst, src, n, k, s);
+}
+static cudaError_t copy_sync(void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+    count_copy(n, k);
+    return cudaMemcpy(dst, src, n, k);
+}
+
+enum KernelKind : int { KK_TD_AVG = 0, KK_TD, KK_CUR, KK_OBS_RM, KK_OBS, KK_PRED, KK_SPMV, KK_TICK, KK_COUNT };
+static const char* kKernelNames[KK_COUNT] = {"td_avg", "td", "cur", "obs_rm", "obs", "pred", "spmv", "tick"};
+struct KernelRecord {
+    int kind;
+    double bytes;
+    cudaEvent_t e0, e1;
+};
+
+// ---------------------------------------------------------------------------
+// Level kernels (blockIdx.y = solve within the batch).
+
+__global__ void k_td(DevTree T, int lo, int hi, int S, const double* __restrict__ b,
+                     double* __restrict__ x, double* __restrict__ avg,
+                     const double* __restrict__ wsched, int cap, const long long* __restrict__ tdev) {
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    const size_t o = (size_t)blockIdx.y * S;
+    double w = 0.0;
+    double* a = nullptr;
+    if (avg) {
+        w = wsched[(size_t)blockIdx.y * cap + *tdev];
+        a = avg + o;
+        // the reference axpy also covers the empty sequence (x[0] = 1)
+        if (j == 0) a[0] = dadd(dmul(w, __ldcg(x + o)), __ldcg(a));
+    }
+    td_dp(T, j, b + o, x + o, a, w);
+}
+
+// avg[0] update for a player without decision points (no TD levels).
+__global__ void k_avg0(int S, const double* __restrict__ x, double* __restrict__ avg,
+                       const double* __restrict__ wsched, int cap, const long long* __restrict__ tdev) {
+    const size_t o = (size_t)blockIdx.x * S;
+    const double w = wsched[(size_t)blockIdx.x * cap + *tdev];
+    avg[o] = dadd(dmul(w, x[o]), avg[o]);
+}
+
+__global__ void k_cur(DevTree T, int lo, int hi, int S, const double* __restrict__ r,
+                      double* __restrict__ x) {
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    const size_t o = (size_t)blockIdx.y * S;
+    cur_dp(T, j, r + o, x + o);
+}
+
+__global__ void k_obs(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ u,
+                      double* __restrict__ r, double* __restrict__ b, double* __restrict__ V,
+                      int post, const double* __restrict__ pfs, const double* __restrict__ nfs,
+                      int cap, const long long* __restrict__ tdev, int do_rm, int* nonfinite) {
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    const size_t o = (size_t)blockIdx.y * S;
+    double pf = 1.0, nf = 1.0;
+    if (post == POST_DCFR) {
+        const size_t k = (size_t)blockIdx.y * cap + *tdev;
+        pf = pfs[k];
+        nf = nfs[k];
+    }
+    obs_dp(T, j, u + o, r + o, b + o, V + (size_t)blockIdx.y * J, post, pf, nf, do_rm != 0,
+           nonfinite);
+}
+
+__global__ void k_pred(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ m,
+                       const double* __restrict__ r, double* __restrict__ b,
+                       double* __restrict__ V, int plus) {
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    const size_t o = (size_t)blockIdx.y * S;
+    pred_dp(T, j, m + o, r + o, b + o, V + (size_t)blockIdx.y * J, plus != 0);
+}
+
+__global__ void k_br(DevTree T, int lo, int hi, const double* __restrict__ g,
+                     double* __restrict__ W) {
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    br_dp(T, j, g, W);
+}
+
+// br = g[0] + value of the root (the empty sequence's child sum).
+__global__ void k_br_root(DevTree T, const double* __restrict__ g, const double* __restrict__ W,
+                          double* out) {
+    *out = dadd(g[0], child_sum(T.child[0], W));
+}
+
+__global__ void k_spmv(int rows, const int* __restrict__ indptr, const int* __restrict__ indices,
+                       const double* __restrict__ data, const double* __restrict__ x, int sx,
+                       double* __restrict__ out, int so, int negate, int* nonfinite) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= rows) return;
+    double acc = spmv_row(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
+    if (negate) acc = dmul(-1.0, acc);
+    if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);
+    out[(size_t)blockIdx.y * so + row] = acc;
+}
+
+__global__ void k_normalize(const double* __restrict__ a, double w, double* __restrict__ out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ddiv(a[i], w);
+}
+
+__global__ void k_tick(long long* tdev) { *tdev += 1; }
+
+// ---------------------------------------------------------------------------
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CUDA_OK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    ~DevBuf() { free(); }
+};
+
+struct Player {
+    int S = 0, J = 0;
+    std::vector<int> lvl;  // DP level starts (by process-tree depth), size L+1
+    std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
+    std::vector<double> uniform;  // host copy of the uniform behaviour (slot 0 = 0)
+    DevBuf<int> seq_ptr, dp_parent;
+    DevBuf<int2> child;
+    DevBuf<double> r, b, x, xpost, avg, u, V;   // batched [B][...]
+    DevBuf<double> g, W, xbar;                   // best-response scratch, one solve
+    DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
+    int levels() const { return (int)lvl.size() - 1; }
+};
+
+struct DevCsr {
+    int rows = 0, cols = 0, nnz = 0;
+    DevBuf<int> indptr, indices;
+    DevBuf<double> data;
+};
+
+}  // namespace scfr
+
+struct scfr_handle {
+    int device = 0;
+    int B = 1;
+    int variant = 0, mode = 0;
+    int engine = SCFR_ENGINE_LEVELS;
+    std::vector<double> alpha, beta, gamma;
+    scfr::Player P[2];
+    scfr::DevCsr U, UT;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // schedules [B][cap]
+    int cap = 0;
+    std::vector<double> w_host;  // [B][cap]
+    scfr::DevBuf<double> wsched, pfsched, nfsched;
+    scfr::DevBuf<long long> tdev;
+    scfr::DevBuf<int> nonfinite;
+    scfr::DevBuf<double> brout;
+    int64_t t = 0;                 // completed iterations
+    std::vector<double> avg_weight;  // [B]
+    cudaGraphExec_t exec = nullptr;
+    int64_t nodes_per_iter = 0;
+    int64_t launches = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued by the API
+    bool use_graph = true;
+    bool timed = false;
+    scfr::PersistentPlan plan;
+    ~scfr_handle() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace scfr {
+
+static bool predictive(int v) { return v == SCFR_PCFR || v == SCFR_PCFR_PLUS; }
+static int post_of(int v) {
+    if (v == SCFR_CFR_PLUS || v == SCFR_PCFR_PLUS) return POST_PLUS;
+    if (v == SCFR_DCFR) return POST_DCFR;
+    return POST_NONE;
+}
+
+// float(t) ** e with the reference's semantics (pkg/solvers.py:82-94, :172):
+// both go through libm pow(); an infinite power gives DCFR factor 1.
+static double tpow(int64_t t, double e) { return std::pow((double)t, e); }
+static double dfactor(int64_t t, double e) {
+    const double p = tpow(t, e);
+    if (std::isinf(p)) return 1.0;
+    return p / (p + 1.0);
+}
+
+static int grid_for(int n) { return std::max(1, (n + TPB - 1) / TPB); }
+
+static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s) {
+    if (!p || p->num_seqs < 1 || p->num_decisions < 0 || p->num_nodes < 1)
+        fail(SCFR_EINVAL, "bad tfsdp sizes");
+    if (p->num_seqs >= (1ll << 31) / 2) fail(SCFR_EINVAL, "tfsdp too large for int32 indexing");
+    if (!p->depth || !p->dp_node || !p->dp_first_seq || !p->dp_num_actions || !p->dp_parent_seq)
+        fail(SCFR_EINVAL, "tfsdp has a NULL array");
+    const int S = (int)p->num_seqs, J = (int)p->num_decisions;
+    P.S = S;
+    P.J = J;
+    std::vector<int> seq_ptr(J + 1), dp_parent(J);
+    std::vector<int2> child(S, make_int2(0, 0));
+    P.uniform.assign(S, 0.0);
+    int64_t next = 1;
+    int64_t prev_depth = -1;
+    P.lvl.clear();
+    for (int j = 0; j < J; ++j) {
+        if (p->dp_first_seq[j] != next) fail(SCFR_EINVAL, "dp_first_seq is not contiguous in j");
+        const int64_t n = p->dp_num_actions[j];
+        if (n < 1) fail(SCFR_EINVAL, "decision point without actions");
+        seq_ptr[j] = (int)next;
+        for (int64_t a = 0; a < n; ++a) P.uniform[next + a] = 1.0 / (double)n;
+        next += n;
+        const int64_t ps = p->dp_parent_seq[j];
+        if (ps < 0 || ps >= S) fail(SCFR_EINVAL, "dp_parent_seq out of range");
+        dp_parent[j] = (int)ps;
+        int2& c = child[ps];
+        if (c.y == 0) c.x = j;
+        else if (c.x + c.y != j) fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
+        c.y++;
+        const int64_t node = p->dp_node[j];
+        if (node < 0 || node >= p->num_nodes) fail(SCFR_EINVAL, "dp_node out of range");
+        const int64_t d = p->depth[node];
+        if (d < prev_depth) fail(SCFR_EINVAL, "decision points are not ordered by depth");
+        if (d != prev_depth) P.lvl.push_back(j);
+        prev_depth = d;
+    }
+    P.lvl.push_back(J);
+    if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
+    seq_ptr[J] = S;
+    P.lvl_ns.clear();
+    P.lvl_nj.clear();
+    P.lvl_nc.clear();
+    for (size_t l = 0; l + 1 < P.lvl.size(); ++l) {
+        const int j0 = P.lvl[l], j1 = P.lvl[l + 1];
+        const int s0 = seq_ptr[j0], s1 = j1 < J ? seq_ptr[j1] : (int)next;
+        double nc = 0;
+        for (int s = s0; s < s1; ++s) nc += child[s].y;
+        P.lvl_ns.push_back(s1 - s0);
+        P.lvl_nj.push_back(j1 - j0);
+        P.lvl_nc.push_back(nc);
+    }
+    // parent sequences precede their decision point's level
+    for (int j = 0; j < J; ++j)
+        if (dp_parent[j] >= seq_ptr[j]) fail(SCFR_EINVAL, "parent sequence after its decision point");
+
+    P.seq_ptr.alloc(J + 1);
+    P.dp_parent.alloc(std::max(J, 1));
+    P.child.alloc(S);
+    CUDA_OK(copy_async(P.seq_ptr.p, seq_ptr.data(), (J + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (J) CUDA_OK(copy_async(P.dp_parent.p, dp_parent.data(), J * sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_OK(copy_async(P.child.p, child.data(), S * sizeof(int2), cudaMemcpyHostToDevice, s));
+
+    const size_t SB = (size_t)S * B, JB = (size_t)std::max(J, 1) * B;
+    P.r.alloc(SB);
+    P.b.alloc(SB);
+    P.x.alloc(SB);
+    P.xpost.alloc(SB);
+    P.avg.alloc(SB);
+    P.u.alloc(SB);
+    P.V.alloc(JB);
+    P.g.alloc(S);
+    P.W.alloc(std::max(J, 1));
+    P.xbar.alloc(S);
+    for (auto* buf : {&P.r, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
+    // b = uniform; x[0] = xpost[0] = 1 (the empty sequence's mass).
+    std::vector<double> init((size_t)S * B);
+    for (int k = 0; k < B; ++k) std::copy(P.uniform.begin(), P.uniform.end(), init.begin() + (size_t)k * S);
+    CUDA_OK(copy_async(P.b.p, init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    std::vector<double> ones((size_t)S * B, 0.0);
+    for (int k = 0; k < B; ++k) ones[(size_t)k * S] = 1.0;
+    // set slot 0 of every solve to 1.0 via a strided copy
+    CUDA_OK(cudaMemcpy2DAsync(P.x.p, S * sizeof(double), ones.data(), S * sizeof(double),
+                              sizeof(double), B, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpy2DAsync(P.xpost.p, S * sizeof(double), ones.data(), S * sizeof(double),
+                              sizeof(double), B, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s) {
+    if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
+    if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
+    if (m->indptr[0] != 0 || m->indptr[m->rows] != m->nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
+    D.rows = (int)m->rows;
+    D.cols = (int)m->cols;
+    D.nnz = (int)m->nnz;
+    std::vector<int> ip(m->rows + 1), ix(m->nnz);
+    for (int64_t i = 0; i <= m->rows; ++i) ip[i] = (int)m->indptr[i];
+    for (int64_t k = 0; k < m->nnz; ++k) {
+        if (m->indices[k] < 0 || m->indices[k] >= m->cols) fail(SCFR_EINVAL, "column index out of range");
+        ix[k] = (int)m->indices[k];
+    }
+    D.indptr.alloc(m->rows + 1);
+    D.indices.alloc(std::max<int64_t>(m->nnz, 1));
+    D.data.alloc(std::max<int64_t>(m->nnz, 1));
+    CUDA_OK(copy_async(D.indptr.p, ip.data(), ip.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (m->nnz) {
+        CUDA_OK(copy_async(D.indices.p, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+        CUDA_OK(copy_async(D.data.p, m->data, m->nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+// --- per-iteration launch sequence --------------------------------------
+
+// Algorithmic (compulsory) HBM bytes of one launch, fp64 values / int32
+// indices, every array touched once (DESIGN.md §4 has the derivation).
+struct LevelBytes {
+    static double obs(const Player& P, int l, bool rm) {
+        const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
+        // u, b read; r RMW; child {lo,cnt}; [b write]; seq_ptr, V write; child V reads
+        return (8 + 8 + 16 + 8 + (rm ? 8 : 0)) * ns + 12 * nj + 8 * nc;
+    }
+    static double pred(const Player& P, int l) {
+        const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
+        return (8 + 8 + 8 + 8 + 8) * ns + 12 * nj + 8 * nc;  // m, b, r read; b write; child
+    }
+    static double td(const Player& P, int l, bool avg) {
+        const double ns = P.lvl_ns[l], nj = P.lvl_nj[l];
+        // b read, x write, [avg RMW]; seq_ptr, dp_parent, parent x
+        return (16 + (avg ? 16 : 0)) * ns + 16 * nj;
+    }
+    static double cur(const Player& P, int l) {
+        return 16.0 * P.lvl_ns[l] + 16.0 * P.lvl_nj[l];  // r read, x write; structure
+    }
+    static double spmv(const DevCsr& M) {
+        return 4.0 * (M.rows + 1) + 12.0 * M.nnz + 8.0 * M.cols + 8.0 * M.rows;
+    }
+};
+
+struct Launcher {
+    scfr_handle* h;
+    int64_t count = 0;
+    std::vector<KernelRecord>* prof = nullptr;  // per-launch events when profiling
+
+    template <class F>
+    void launch(int kind, double bytes, F&& f) {
+        if (prof) {
+            KernelRecord r;
+            r.kind = kind;
+            r.bytes = bytes * h->B;
+            CUDA_OK(cudaEventCreate(&r.e0));
+            CUDA_OK(cudaEventCreate(&r.e1));
+            CUDA_OK(cudaEventRecord(r.e0, h->stream));
+            f();
+            CUDA_OK(cudaEventRecord(r.e1, h->stream));
+            prof->push_back(r);
+        } else {
+            f();
+        }
+        ++count;
+    }
+
+    void spmv(const DevCsr& M, const double* x, int sx, double* out, int so, bool neg) {
+        launch(KK_SPMV, LevelBytes::spmv(M), [&] {
+            dim3 grid(grid_for(M.rows), h->B);
+            k_spmv<<<grid, TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p, M.data.p, x, sx,
+                                                out, so, neg ? 1 : 0, h->nonfinite.p);
+        });
+    }
+    void td(Player& P, const double* b, double* x, bool avg) {
+        if (avg && P.J == 0) {
+            launch(KK_TD_AVG, 16.0, [&] {
+                k_avg0<<<h->B, 1, 0, h->stream>>>(P.S, x, P.avg.p, h->wsched.p, h->cap, h->tdev.p);
+            });
+        }
+        for (int l = 0; l < P.levels(); ++l) {
+            const int lo = P.lvl[l], hi = P.lvl[l + 1];
+            launch(avg ? KK_TD_AVG : KK_TD, LevelBytes::td(P, l, avg), [&] {
+                dim3 grid(grid_for(hi - lo), h->B);
+                k_td<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, b, x,
+                                                  avg ? P.avg.p : nullptr, h->wsched.p, h->cap,
+                                                  h->tdev.p);
+            });
+        }
+    }
+    void cur(Player& P) {
+        for (int l = 0; l < P.levels(); ++l) {
+            const int lo = P.lvl[l], hi = P.lvl[l + 1];
+            launch(KK_CUR, LevelBytes::cur(P, l), [&] {
+                dim3 grid(grid_for(hi - lo), h->B);
+                k_cur<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, P.r.p, P.xpost.p);
+            });
+        }
+    }
+    void pred(Player& P, bool plus) {
+        for (int l = P.levels() - 1; l >= 0; --l) {
+            const int lo = P.lvl[l], hi = P.lvl[l + 1];
+            launch(KK_PRED, LevelBytes::pred(P, l), [&] {
+                dim3 grid(grid_for(hi - lo), h->B);
+                k_pred<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
+                                                    P.r.p, P.b.p, P.V.p, plus ? 1 : 0);
+            });
+        }
+    }
+    void obs(Player& P, int post, bool rm) {
+        for (int l = P.levels() - 1; l >= 0; --l) {
+            const int lo = P.lvl[l], hi = P.lvl[l + 1];
+            launch(rm ? KK_OBS_RM : KK_OBS, LevelBytes::obs(P, l, rm), [&] {
+                dim3 grid(grid_for(hi - lo), h->B);
+                k_obs<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
+                                                   P.r.p, P.b.p, P.V.p, post, h->pfsched.p,
+                                                   h->nfsched.p, h->cap, h->tdev.p, rm ? 1 : 0,
+                                                   h->nonfinite.p);
+            });
+        }
+    }
+
+    void iteration() {
+        Player& A = h->P[0];
+        Player& Bp = h->P[1];
+        const bool pr = predictive(h->variant);
+        const int post = post_of(h->variant);
+        const bool plus = h->variant == SCFR_PCFR_PLUS;
+        // next_strategy for both players
+        for (Player* P : {&A, &Bp}) {
+            if (pr) pred(*P, plus);
+            td(*P, P->b.p, P->x.p, true);
+        }
+        // u1 = U x2 ; sim: u2 = -Uᵀ x1
+        spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);
+        if (h->mode == SCFR_MODE_SIM) {
+            spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);
+            obs(A, post, !pr);
+        } else {
+            obs(A, post, !pr);
+            if (pr) cur(A);
+            else td(A, A.b.p, A.xpost.p, false);
+            spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);
+        }
+        obs(Bp, post, !pr);
+        launch(KK_TICK, 0.0, [&] { k_tick<<<1, 1, 0, h->stream>>>(h->tdev.p); });
+    }
+};
+
+static void ensure_schedule(scfr_handle* h, int64_t upto) {
+    if (upto <= h->cap) return;
+    int64_t cap = std::max<int64_t>(4096, h->cap);
+    while (cap < upto) cap *= 2;
+    if (cap >= (1ll << 31)) fail(SCFR_EINVAL, "iteration count too large");
+    const int B = h->B;
+    std::vector<double> w((size_t)B * cap), pf((size_t)B * cap), nf((size_t)B * cap);
+    for (int k = 0; k < B; ++k)
+        for (int64_t i = 0; i < cap; ++i) {
+            const int64_t t = i + 1;  // reference RegretState.t during iteration i+1
+            w[(size_t)k * cap + i] = tpow(t, h->gamma[k]);
+            pf[(size_t)k * cap + i] = dfactor(t, h->alpha[k]);
+            nf[(size_t)k * cap + i] = dfactor(t, h->beta[k]);
+        }
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    h->wsched.alloc(w.size());
+    h->pfsched.alloc(pf.size());
+    h->nfsched.alloc(nf.size());
+    CUDA_OK(copy_sync(h->wsched.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OK(copy_sync(h->pfsched.p, pf.data(), pf.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OK(copy_sync(h->nfsched.p, nf.data(), nf.size() * sizeof(double), cudaMemcpyHostToDevice));
+    h->w_host.swap(w);
+    h->cap = (int)cap;
+    if (h->exec) {
+        cudaGraphExecDestroy(h->exec);
+        h->exec = nullptr;
+    }
+}
+
+static void build_graph(scfr_handle* h) {
+    cudaGraph_t graph;
+    Launcher L{h};
+    CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    L.iteration();
+    CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
+    CUDA_OK(cudaGraphInstantiate(&h->exec, graph, 0));
+    cudaGraphDestroy(graph);
+    h->nodes_per_iter = L.count;
+}
+
+static void set_device(const scfr_handle* h) { CUDA_OK(cudaSetDevice(h->device)); }
+
+static void check_player(const scfr_handle* h, int player, int solve) {
+    if (!h) fail(SCFR_EINVAL, "handle is NULL");
+    if (player != 1 && player != 2) fail(SCFR_EINVAL, "player must be 1 or 2");
+    if (solve < 0 || solve >= h->B) fail(SCFR_EINVAL, "solve index out of range");
+}
+
+// Best response of `player` against the opponent's strategy x_opp (one solve).
+static double best_response(scfr_handle* h, int player, const double* x_opp) {
+    Player& P = h->P[player - 1];
+    const DevCsr& M = player == 1 ? h->U : h->UT;
+    Player& O = h->P[2 - player];
+    (void)O;
+    k_spmv<<<dim3(grid_for(M.rows), 1), TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p, M.data.p,
+                                                            x_opp, 0, P.g.p, 0, player == 2 ? 1 : 0,
+                                                            nullptr);
+    for (int l = P.levels() - 1; l >= 0; --l) {
+        const int lo = P.lvl[l], hi = P.lvl[l + 1];
+        k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
+    }
+    k_br_root<<<1, 1, 0, h->stream>>>(P.tree(), P.g.p, P.W.p, h->brout.p + (player - 1));
+    CUDA_OK(cudaGetLastError());
+    double v = 0.0;
+    CUDA_OK(copy_async(&v, h->brout.p + (player - 1), sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return v;
+}
+
+// Device pointer to the solve's profile component: normalised average
+// (written into xbar) or the last emitted strategy.
+static const double* profile(scfr_handle* h, int player, int solve, int which) {
+    Player& P = h->P[player - 1];
+    const size_t o = (size_t)solve * P.S;
+    if (which == 1) return P.x.p + o;
+    if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
+    k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(P.avg.p + o, h->avg_weight[solve], P.xbar.p, P.S);
+    CUDA_OK(cudaGetLastError());
+    return P.xbar.p;
+}
+
+static int choose_engine(scfr_handle*) { return SCFR_ENGINE_LEVELS; }
+static void prepare_persistent(scfr_handle*) {
+    fail(SCFR_EINVAL, "persistent engine not available in this build");
+}
+static int64_t launch_persistent(scfr_handle*, int64_t) {
+    fail(SCFR_EINVAL, "persistent engine not available in this build");
+}
+
+}  // namespace scfr
+
+using namespace scfr;
+
+extern "C" {
+
+int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, const scfr_csr* UT,
+                const scfr_config* cfg, int device, scfr_handle** out) {
+    return guarded([&] {
+        if (!out || !cfg) fail(SCFR_EINVAL, "NULL argument");
+        if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
+        if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
+        if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) fail(SCFR_ECUDA, "no CUDA device available: %s", cudaGetErrorString(e));
+        if (device < 0 || device >= ndev) fail(SCFR_EINVAL, "device index out of range");
+        CUDA_OK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CUDA_OK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) fail(SCFR_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+        std::unique_ptr<scfr_handle> h(new scfr_handle());
+        h->device = device;
+        h->B = cfg->batch;
+        h->variant = cfg->variant;
+        h->mode = cfg->mode;
+        h->engine = cfg->engine;
+        h->alpha.resize(h->B);
+        h->beta.resize(h->B);
+        h->gamma.resize(h->B);
+        for (int k = 0; k < h->B; ++k) {
+            h->alpha[k] = cfg->batch_alpha ? cfg->batch_alpha[k] : cfg->alpha;
+            h->beta[k] = cfg->batch_beta ? cfg->batch_beta[k] : cfg->beta;
+            h->gamma[k] = cfg->batch_gamma ? cfg->batch_gamma[k] : cfg->gamma;
+            if (!std::isfinite(h->alpha[k]) || !std::isfinite(h->beta[k])) fail(SCFR_EINVAL, "alpha and beta must be finite");
+            if (!(h->gamma[k] >= 0)) fail(SCFR_EINVAL, "gamma must be >= 0");
+        }
+        if (p1->num_seqs != U->rows || p2->num_seqs != U->cols || UT->rows != U->cols ||
+            UT->cols != U->rows || UT->nnz != U->nnz)
+            fail(SCFR_EINVAL, "dimension mismatch between the payoff matrix and the decision processes");
+        CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreate(&h->ev0));
+        CUDA_OK(cudaEventCreate(&h->ev1));
+        upload_player(p1, h->P[0], h->B, h->stream);
+        upload_player(p2, h->P[1], h->B, h->stream);
+        upload_csr(U, h->U, h->stream);
+        upload_csr(UT, h->UT, h->stream);
+        h->tdev.alloc(1);
+        h->tdev.zero(h->stream);
+        h->nonfinite.alloc(1);
+        h->nonfinite.zero(h->stream);
+        h->brout.alloc(2);
+        h->avg_weight.assign(h->B, 0.0);
+        const char* ng = std::getenv("SCFR_NO_GRAPH");
+        h->use_graph = !(ng && ng[0] == '1');
+        if (h->engine == SCFR_ENGINE_AUTO) h->engine = choose_engine(h.get());
+        if (h->engine == SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        *out = h.release();
+    });
+}
+
+int scfr_step(scfr_handle* h, int64_t n) {
+    return guarded([&] {
+        if (!h) fail(SCFR_EINVAL, "handle is NULL");
+        if (n < 0) fail(SCFR_EINVAL, "n_iter must be >= 0");
+        if (n == 0) return;
+        set_device(h);
+        ensure_schedule(h, h->t + n);
+        for (int k = 0; k < h->B; ++k)
+            for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
+        CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+        if (h->engine == SCFR_ENGINE_PERSISTENT) {
+            h->launches += launch_persistent(h, n);
+        } else if (h->use_graph) {
+            if (!h->exec) build_graph(h);
+            for (int64_t i = 0; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->exec, h->stream));
+            h->launches += n * h->nodes_per_iter;
+        } else {
+            Launcher L{h};
+            for (int64_t i = 0; i < n; ++i) L.iteration();
+            CUDA_OK(cudaGetLastError());
+            h->launches += L.count;
+        }
+        CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+        h->timed = true;
+        h->t += n;
+    });
+}
+
+int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap, int* count) {
+    return guarded([&] {
+        if (!h || !out || !count || cap < KK_COUNT) fail(SCFR_EINVAL, "bad arguments");
+        if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
+        set_device(h);
+        ensure_schedule(h, h->t + n);
+        for (int k = 0; k < h->B; ++k)
+            for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
+        std::vector<KernelRecord> recs;
+        Launcher L{h};
+        L.prof = &recs;
+        CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+        for (int64_t i = 0; i < n; ++i) L.iteration();
+        CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        h->timed = true;
+        h->t += n;
+        h->launches += L.count;
+        for (int k = 0; k < KK_COUNT; ++k) {
+            std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[k]);
+            out[k].launches = 0;
+            out[k].ms = 0.0;
+            out[k].bytes = 0.0;
+        }
+        for (auto& r : recs) {
+            float ms = 0.f;
+            CUDA_OK(cudaEventElapsedTime(&ms, r.e0, r.e1));
+            out[r.kind].launches++;
+            out[r.kind].ms += ms;
+            out[r.kind].bytes += r.bytes;
+            cudaEventDestroy(r.e0);
+            cudaEventDestroy(r.e1);
+        }
+        *count = KK_COUNT;
+    });
+}
+
+int scfr_synchronize(scfr_handle* h) {
+    return guarded([&] {
+        if (!h) fail(SCFR_EINVAL, "handle is NULL");
+        set_device(h);
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int scfr_iterations(const scfr_handle* h, int64_t* out) {
+    return guarded([&] {
+        if (!h || !out) fail(SCFR_EINVAL, "NULL argument");
+        *out = h->t;
+    });
+}
+
+int scfr_avg_weight(const scfr_handle* h, int player, int solve, double* out) {
+    return guarded([&] {
+        check_player(h, player, solve);
+        if (!out) fail(SCFR_EINVAL, "NULL argument");
+        *out = h->avg_weight[solve];
+    });
+}
+
+int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* host_out) {
+    return guarded([&] {
+        check_player(h, player, solve);
+        if (!host_out) fail(SCFR_EINVAL, "NULL argument");
+        set_device(h);
+        Player& P = h->P[player - 1];
+        const size_t o = (size_t)solve * P.S;
+        const double* src = nullptr;
+        size_t off = 0, cnt = P.S;
+        switch (which) {
+            case SCFR_STATE_REGRETS: src = P.r.p; off = 1; cnt = P.S - 1; break;
+            case SCFR_STATE_BEHAVIOR:
+                // non-predictive OBS regret-matches ahead of time; expose the
+                // behaviour the reference holds (the one used last iteration)
+                src = P.b.p; off = 1; cnt = P.S - 1; break;
+            case SCFR_STATE_ACCUM: src = P.avg.p; break;
+            case SCFR_STATE_UTILITY: src = P.u.p; break;
+            default: fail(SCFR_EINVAL, "unknown state selector");
+        }
+        if (cnt) CUDA_OK(copy_async(host_out, src + o + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
+    return guarded([&] {
+        check_player(h, player, solve);
+        if (!host_out) fail(SCFR_EINVAL, "NULL argument");
+        if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
+        set_device(h);
+        Player& P = h->P[player - 1];
+        CUDA_OK(copy_async(host_out, P.avg.p + (size_t)solve * P.S, P.S * sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        const double w = h->avg_weight[solve];
+        for (int i = 0; i < P.S; ++i) host_out[i] = host_out[i] / w;
+    });
+}
+
+int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
+    return guarded([&] {
+        check_player(h, player, solve);
+        if (!host_out) fail(SCFR_EINVAL, "NULL argument");
+        if (h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
+        set_device(h);
+        Player& P = h->P[player - 1];
+        CUDA_OK(copy_async(host_out, P.x.p + (size_t)solve * P.S, P.S * sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl, double* br1, double* br2) {
+    return guarded([&] {
+        check_player(h, 1, solve);
+        if (which != 0 && which != 1) fail(SCFR_EINVAL, "which must be 0 (average) or 1 (current)");
+        if (which == 1 && h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
+        set_device(h);
+        // br1 against x2, then br2 against x1 (pkg/metrics.py:59-68); xbar
+        // buffers are per player so both profiles can be live at once.
+        const double* x2 = profile(h, 2, solve, which);
+        const double b1 = best_response(h, 1, x2);
+        const double* x1 = profile(h, 1, solve, which);
+        const double b2 = best_response(h, 2, x1);
+        if (br1) *br1 = b1;
+        if (br2) *br2 = b2;
+        if (expl) *expl = (b1 + b2) / 2.0;
+    });
+}
+
+int scfr_expected_value(scfr_handle* h, int solve, double* out) {
+    return guarded([&] {
+        check_player(h, 1, solve);
+        if (!out) fail(SCFR_EINVAL, "NULL argument");
+        set_device(h);
+        const double* x2 = profile(h, 2, solve, 0);
+        Player& A = h->P[0];
+        k_spmv<<<dim3(grid_for(h->U.rows), 1), TPB, 0, h->stream>>>(h->U.rows, h->U.indptr.p, h->U.indices.p,
+                                                                   h->U.data.p, x2, 0, A.g.p, 0, 0, nullptr);
+        profile(h, 1, solve, 0);
+        std::vector<double> g(A.S), x(A.S);
+        CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(copy_async(x.data(), A.xbar.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        double acc = 0.0;  // Backend.dot: sequential (pkg/kernels.py:278-283)
+        for (int i = 0; i < A.S; ++i) acc = acc + x[i] * g[i];
+        *out = acc;
+    });
+}
+
+int scfr_best_response_values(scfr_handle* h, const double* x1, const double* x2, double* br1,
+                              double* br2) {
+    return guarded([&] {
+        if (!h || !x1 || !x2) fail(SCFR_EINVAL, "NULL argument");
+        set_device(h);
+        Player& A = h->P[0];
+        Player& Bp = h->P[1];
+        CUDA_OK(copy_async(A.xbar.p, x1, A.S * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(copy_async(Bp.xbar.p, x2, Bp.S * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        const double b1 = best_response(h, 1, Bp.xbar.p);
+        const double b2 = best_response(h, 2, A.xbar.p);
+        if (br1) *br1 = b1;
+        if (br2) *br2 = b2;
+    });
+}
+
+int scfr_expected_value_of(scfr_handle* h, const double* x1, const double* x2, double* out) {
+    return guarded([&] {
+        if (!h || !x1 || !x2 || !out) fail(SCFR_EINVAL, "NULL argument");
+        set_device(h);
+        Player& A = h->P[0];
+        Player& Bp = h->P[1];
+        CUDA_OK(copy_async(Bp.xbar.p, x2, Bp.S * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        k_spmv<<<dim3(grid_for(h->U.rows), 1), TPB, 0, h->stream>>>(h->U.rows, h->U.indptr.p, h->U.indices.p,
+                                                                   h->U.data.p, Bp.xbar.p, 0, A.g.p, 0, 0, nullptr);
+        std::vector<double> g(A.S);
+        CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        double acc = 0.0;
+        for (int i = 0; i < A.S; ++i) acc = acc + x1[i] * g[i];
+        *out = acc;
+    });
+}
+
+int scfr_status(scfr_handle* h, int* nonfinite) {
+    return guarded([&] {
+        if (!h || !nonfinite) fail(SCFR_EINVAL, "NULL argument");
+        set_device(h);
+        int v = 0;
+        CUDA_OK(copy_async(&v, h->nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        *nonfinite = v;
+    });
+}
+
+int scfr_device_bytes(const scfr_handle* h, int64_t* out) {
+    return guarded([&] {
+        if (!h || !out) fail(SCFR_EINVAL, "NULL argument");
+        int64_t s = 0;
+        for (const Player& P : h->P) {
+            s += P.seq_ptr.bytes() + P.dp_parent.bytes() + P.child.bytes();
+            for (const DevBuf<double>* b : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V, &P.g, &P.W, &P.xbar})
+                s += b->bytes();
+        }
+        for (const DevCsr* m : {&h->U, &h->UT}) s += m->indptr.bytes() + m->indices.bytes() + m->data.bytes();
+        s += h->wsched.bytes() + h->pfsched.bytes() + h->nfsched.bytes();
+        *out = s;
+    });
+}
+
+int scfr_launch_count(const scfr_handle* h, int64_t* out) {
+    return guarded([&] {
+        if (!h || !out) fail(SCFR_EINVAL, "NULL argument");
+        *out = h->launches;
+    });
+}
+
+int scfr_last_step_ms(scfr_handle* h, double* total_ms) {
+    return guarded([&] {
+        if (!h || !total_ms) fail(SCFR_EINVAL, "NULL argument");
+        if (!h->timed) fail(SCFR_EINVAL, "no step has run yet");
+        set_device(h);
+        CUDA_OK(cudaEventSynchronize(h->ev1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        *total_ms = ms;
+    });
+}
+
+int scfr_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+    return guarded([&] {
+        if (!h2d || !d2h) fail(SCFR_EINVAL, "NULL argument");
+        *h2d = g_h2d.load();
+        *d2h = g_d2h.load();
+    });
+}
+
+int scfr_destroy(scfr_handle* h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->device);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        delete h;
+    });
+}
+
+}  // extern "C"
