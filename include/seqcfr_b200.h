@@ -69,8 +69,9 @@ extern "C" {
 
 /* Engines (scfr_config.engine). */
 #define SCFR_ENGINE_AUTO 0
-#define SCFR_ENGINE_LEVELS 1     /* one kernel per DP level, captured in a CUDA graph */
-#define SCFR_ENGINE_PERSISTENT 2 /* whole iterations inside one cooperative kernel */
+#define SCFR_ENGINE_LEVELS 1          /* one kernel per DP level, captured in a CUDA graph */
+#define SCFR_ENGINE_PERSISTENT 2      /* whole iterations in one kernel, one CTA per solve */
+#define SCFR_ENGINE_PERSISTENT_GRID 3 /* whole iterations in one cooperative grid (batch 1) */
 
 const char* scfr_last_error(void);
 int scfr_abi_version(void);
@@ -166,6 +167,8 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
 /* Runs n full iterations (_step semantics incl. t++ for both players) on the
  * handle's stream; asynchronous. */
 int scfr_step(scfr_handle* h, int64_t n_iter);
+/* The engine the handle runs (SCFR_ENGINE_*; AUTO resolved at creation). */
+int scfr_engine(const scfr_handle* h, int* engine);
 int scfr_synchronize(scfr_handle* h);
 /* Completed iterations (the reference's RegretState.t - 1). */
 int scfr_iterations(const scfr_handle* h, int64_t* out);

@@ -1,13 +1,13 @@
-// sm_100a kernels for one CFR iteration over per-DP-level index arrays.
+// sm_100a device functions for one CFR iteration, per decision point (DP).
 //
 // Bit-faithful fp64: every operation is an explicit round-to-nearest
 // intrinsic in the exact association order of the reference (SURVEY.md
-// §8(a) "exact arithmetic contract"); the translation unit is also compiled
-// with -fmad=false so nothing is contracted into an FMA.  Sums are
-// sequential per output element, exactly one thread owns each output, so
+// §8(a) "exact arithmetic contract"); the translation units are also
+// compiled with -fmad=false so nothing is contracted into an FMA.  Sums are
+// sequential per output element and exactly one thread owns each output, so
 // results are deterministic and equal to the numba loops bit for bit.
 //
-// Layout (per player, per solve; all solves of a batch are strided copies):
+// Layout (per player, per solve; solves of a batch are strided copies):
 //   seq-indexed fp64 vectors over Σ (slot 0 = empty sequence): r, b, x,
 //     xpost, avg, u, g   — r/b slot 0 unused (reference Σ+ index = s-1)
 //   dp-indexed fp64 temporaries over J: V (sum pass), W (max pass)
@@ -16,6 +16,12 @@
 //     sequence s: cnt 0 = end node, 1 = a single DP, >1 = observation point)
 //   DP levels: DPs grouped by process-tree depth; BFS numbering makes each
 //     level a contiguous j range (pkg/decision_process.py:9-13).
+//
+// Loads: structure goes through the read-only path (__ldg).  Mutable state
+// uses the policy `Ld`: plain (L1-cacheable) loads where every producer ran
+// in an earlier launch or in the same CTA (level engine, CTA-persistent
+// engine), L2-only loads (ld.global.cg) in the grid-persistent engine whose
+// producers are other SMs within the same launch.
 #pragma once
 
 #include <cstdint>
@@ -32,145 +38,275 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// Value flowing up into sequence s from the decision points below it.
-// End node: the zero-initialised v (0.0).  One DP: v of that DP node (its
-// V).  Observation point: sequential sum over its child DPs in j order
-// starting at 0.0 (pkg/solvers.py:195-199 / pkg/oracle.py:91-95).
-__device__ __forceinline__ double child_sum(int2 c, const double* __restrict__ V) {
-    if (c.y == 0) return 0.0;
-    if (c.y == 1) return __ldcg(V + c.x);
-    double acc = 0.0;
-    for (int k = 0; k < c.y; ++k) acc = dadd(acc, __ldcg(V + c.x + k));
-    return acc;
-}
-
-// Counterfactual value of action s: q = (0.0 + u[s]) + C_s, which is
-// (w + v)[node(s)] read back through Bᵀ (pkg/solvers.py:192-202).
-__device__ __forceinline__ double qval(const DevTree& T, const double* __restrict__ u,
-                                       const double* __restrict__ V, int s) {
-    return dadd(dadd(0.0, __ldcg(u + s)), child_sum(__ldg(T.child + s), V));
-}
+struct LdL1 {
+    static __device__ __forceinline__ double ld(const double* p) { return *p; }
+};
+struct LdL2 {
+    static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+};
 
 enum : int { POST_NONE = 0, POST_PLUS = 1, POST_DCFR = 2 };
 
-// Regret matching of one DP block (pkg/solvers.py:156-160): positive part,
-// sequential block sum from 0.0, IEEE division, uniform 1.0/n fallback.
-__device__ __forceinline__ double rm_sum(const double* __restrict__ r, int s0, int s1) {
-    double S = 0.0;
-    for (int s = s0; s < s1; ++s) {
-        const double v = __ldcg(r + s);
-        S = dadd(S, v > 0.0 ? v : 0.0);
+// Value flowing up into a sequence from the DPs below it, given its child
+// range c and (already loaded) V of its first child `v0`:
+//   end node: 0.0 (the zero-initialised v); one DP: V of that DP;
+//   observation point: ((0.0 + V_lo) + V_lo+1) + ... in j order
+// (pkg/solvers.py:195-199, pkg/oracle.py:91-95).
+template <class Ld>
+__device__ __forceinline__ double child_value(int2 c, double v0, const double* __restrict__ V) {
+    if (c.y == 0) return 0.0;
+    if (c.y == 1) return v0;
+    double acc = dadd(0.0, v0);
+    int k = 1;
+    for (; k + 4 <= c.y; k += 4) {  // loads first, adds in order
+        const double a0 = Ld::ld(V + c.x + k), a1 = Ld::ld(V + c.x + k + 1);
+        const double a2 = Ld::ld(V + c.x + k + 2), a3 = Ld::ld(V + c.x + k + 3);
+        acc = dadd(dadd(dadd(dadd(acc, a0), a1), a2), a3);
     }
-    return S;
+    for (; k < c.y; ++k) acc = dadd(acc, Ld::ld(V + c.x + k));
+    return acc;
 }
+
+template <class Ld>
+__device__ __forceinline__ double child_sum(int2 c, const double* __restrict__ V) {
+    return child_value<Ld>(c, c.y > 0 ? Ld::ld(V + c.x) : 0.0, V);
+}
+
+// q[a] = (0.0 + u[s0+a]) + C_{s0+a} for a < n <= MAXA, all loads issued
+// before the dependent adds ((w + v)[node(s)] read back through Bᵀ,
+// pkg/solvers.py:192-202).
+template <int MAXA, class Ld>
+__device__ __forceinline__ void load_q(const DevTree& T, const double* __restrict__ u,
+                                       const double* __restrict__ V, int s0, int n,
+                                       double (&q)[MAXA]) {
+    int2 c[MAXA];
+    double uu[MAXA], v0[MAXA];
+#pragma unroll
+    for (int a = 0; a < MAXA; ++a)
+        if (a < n) {
+            c[a] = __ldg(T.child + s0 + a);
+            uu[a] = Ld::ld(u + s0 + a);
+        }
+#pragma unroll
+    for (int a = 0; a < MAXA; ++a)
+        if (a < n) v0[a] = c[a].y > 0 ? Ld::ld(V + c[a].x) : 0.0;
+#pragma unroll
+    for (int a = 0; a < MAXA; ++a)
+        if (a < n) q[a] = dadd(dadd(0.0, uu[a]), child_value<Ld>(c[a], v0[a], V));
+}
+
+template <class Ld>
+__device__ __forceinline__ double qval(const DevTree& T, const double* __restrict__ u,
+                                       const double* __restrict__ V, int s) {
+    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(__ldg(T.child + s), V));
+}
+
+__device__ __forceinline__ double post_op(double rv, int post, double pf, double nf) {
+    if (post == POST_PLUS) return rv > 0.0 ? rv : 0.0;
+    if (post == POST_DCFR) return rv > 0.0 ? dmul(rv, pf) : (rv < 0.0 ? dmul(rv, nf) : rv);
+    return rv;
+}
+
+// Regret matching of one block (pkg/solvers.py:156-160): positive part,
+// sequential sum from 0.0, IEEE division, uniform 1.0/n fallback.
 __device__ __forceinline__ double rm_prob(double rv, double S, int n) {
     const double p = rv > 0.0 ? rv : 0.0;
     return S != 0.0 ? ddiv(p, S) : ddiv(1.0, (double)n);
 }
 
+
 // ---------------------------------------------------------------------------
-// OBS: bottom-up counterfactual values + regret update (+ variant post-op)
-// (+ regret matching of the updated regrets into b for the next iteration).
+// OBS: counterfactual values + regret update (+ variant post-op) (+ regret
+// matching of the updated regrets into b for the next iteration).
 // pkg/solvers.py:178-224 and :143-160, fused per decision point.
+// MAXA: actions held in registers; wider DPs take the generic (recompute) path.
+template <int MAXA, class Ld>
 __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __restrict__ u,
                                        double* __restrict__ r, double* __restrict__ b,
                                        double* __restrict__ V, int post, double pf, double nf,
                                        bool do_rm, int* nonfinite) {
-    const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
-    double E = 0.0;
-    for (int s = s0; s < s1; ++s) E = dadd(E, dmul(__ldcg(b + s), qval(T, u, V, s)));
-    V[j] = E;
-    const double negE = dmul(-1.0, dadd(0.0, E));
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
     bool bad = false;
-    for (int s = s0; s < s1; ++s) {
-        const double q = qval(T, u, V, s);
-        bad |= !isfinite(q);
-        double rv = dadd(__ldcg(r + s), dadd(negE, q));
-        if (post == POST_PLUS) {
-            rv = rv > 0.0 ? rv : 0.0;
-        } else if (post == POST_DCFR) {
-            rv = rv > 0.0 ? dmul(rv, pf) : (rv < 0.0 ? dmul(rv, nf) : rv);
+    if (n <= MAXA) {
+        double q[MAXA], bb[MAXA], rr[MAXA];
+        load_q<MAXA, Ld>(T, u, V, s0, n, q);
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) {
+                bb[a] = Ld::ld(b + s0 + a);
+                rr[a] = Ld::ld(r + s0 + a);
+            }
+        double E = 0.0;
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) E = dadd(E, dmul(bb[a], q[a]));
+        V[j] = E;
+        const double negE = dmul(-1.0, dadd(0.0, E));
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) {
+                bad |= !isfinite(q[a]);
+                const double rv = post_op(dadd(rr[a], dadd(negE, q[a])), post, pf, nf);
+                bad |= !isfinite(rv);
+                rr[a] = rv;
+                r[s0 + a] = rv;
+                S = dadd(S, rv > 0.0 ? rv : 0.0);
+            }
+        if (do_rm) {
+#pragma unroll
+            for (int a = 0; a < MAXA; ++a)
+                if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
         }
-        bad |= !isfinite(rv);
-        r[s] = rv;
+    } else {
+        double E = 0.0;
+        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, u, V, s)));
+        V[j] = E;
+        const double negE = dmul(-1.0, dadd(0.0, E));
+        double S = 0.0;
+        for (int s = s0; s < s0 + n; ++s) {
+            const double q = qval<Ld>(T, u, V, s);
+            bad |= !isfinite(q);
+            const double rv = post_op(dadd(Ld::ld(r + s), dadd(negE, q)), post, pf, nf);
+            bad |= !isfinite(rv);
+            r[s] = rv;
+            S = dadd(S, rv > 0.0 ? rv : 0.0);
+        }
+        if (do_rm)
+            for (int s = s0; s < s0 + n; ++s) b[s] = rm_prob(Ld::ld(r + s), S, n);
     }
     if (bad) atomicOr(nonfinite, 1);
-    if (do_rm) {
-        const double S = rm_sum(r, s0, s1);
-        for (int s = s0; s < s1; ++s) b[s] = rm_prob(__ldcg(r + s), S, s1 - s0);
-    }
 }
 
 // PRED: observe the prediction m against the previous behaviour, floor if
 // plus, regret-match the predicted regrets into b; r itself is untouched
-// (snapshot/restore of pkg/solvers.py:227-245 without the copy).
+// (the snapshot/restore of pkg/solvers.py:227-245 without the copy).
+// MAXA: actions held in registers; wider DPs take the generic (recompute) path.
+template <int MAXA, class Ld>
 __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* __restrict__ m,
                                         const double* __restrict__ r, double* __restrict__ b,
                                         double* __restrict__ V, bool plus) {
-    const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
-    double E = 0.0;
-    for (int s = s0; s < s1; ++s) E = dadd(E, dmul(__ldcg(b + s), qval(T, m, V, s)));
-    V[j] = E;
-    const double negE = dmul(-1.0, dadd(0.0, E));
-    double S = 0.0;
-    for (int s = s0; s < s1; ++s) {
-        double rv = dadd(__ldcg(r + s), dadd(negE, qval(T, m, V, s)));
-        if (plus) rv = rv > 0.0 ? rv : 0.0;
-        S = dadd(S, rv > 0.0 ? rv : 0.0);
-    }
-    for (int s = s0; s < s1; ++s) {
-        double rv = dadd(__ldcg(r + s), dadd(negE, qval(T, m, V, s)));
-        if (plus) rv = rv > 0.0 ? rv : 0.0;
-        b[s] = rm_prob(rv, S, s1 - s0);
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    if (n <= MAXA) {
+        double q[MAXA], bb[MAXA], rr[MAXA];
+        load_q<MAXA, Ld>(T, m, V, s0, n, q);
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) {
+                bb[a] = Ld::ld(b + s0 + a);
+                rr[a] = Ld::ld(r + s0 + a);
+            }
+        double E = 0.0;
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) E = dadd(E, dmul(bb[a], q[a]));
+        V[j] = E;
+        const double negE = dmul(-1.0, dadd(0.0, E));
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) {
+                double rv = dadd(rr[a], dadd(negE, q[a]));
+                if (plus) rv = rv > 0.0 ? rv : 0.0;
+                rr[a] = rv;
+                S = dadd(S, rv > 0.0 ? rv : 0.0);
+            }
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
+    } else {
+        double E = 0.0;
+        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, m, V, s)));
+        V[j] = E;
+        const double negE = dmul(-1.0, dadd(0.0, E));
+        double S = 0.0;
+        for (int s = s0; s < s0 + n; ++s) {
+            double rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            if (plus) rv = rv > 0.0 ? rv : 0.0;
+            S = dadd(S, rv > 0.0 ? rv : 0.0);
+        }
+        for (int s = s0; s < s0 + n; ++s) {
+            double rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            if (plus) rv = rv > 0.0 ? rv : 0.0;
+            b[s] = rm_prob(rv, S, n);
+        }
     }
 }
 
 // TD: x[(j,a)] = b[(j,a)] * x[parent(j)] (pkg/solvers.py:163-170), with the
 // fused average update avg = w*x + avg (pkg/solvers.py:172-174).
+template <class Ld>
 __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __restrict__ b,
                                       double* __restrict__ x, double* __restrict__ avg,
                                       double w) {
     const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
-    const double xp = __ldcg(x + __ldg(T.dp_parent + j));
+    const double xp = Ld::ld(x + __ldg(T.dp_parent + j));
     for (int s = s0; s < s1; ++s) {
-        const double xa = dmul(__ldcg(b + s), xp);
+        const double xa = dmul(Ld::ld(b + s), xp);
         x[s] = xa;
-        if (avg) avg[s] = dadd(dmul(w, xa), __ldcg(avg + s));
+        if (avg) avg[s] = dadd(dmul(w, xa), Ld::ld(avg + s));
     }
 }
 
 // CUR: side-effect-free current strategy (pkg/solvers.py:270-291): regret
-// matching on the fly, then the top-down product into xpost.
+// matching on the fly, then the top-down product into x.
+// MAXA: actions held in registers; wider DPs take the generic (recompute) path.
+template <int MAXA, class Ld>
 __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __restrict__ r,
                                        double* __restrict__ x) {
-    const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
-    const double S = rm_sum(r, s0, s1);
-    const double xp = __ldcg(x + __ldg(T.dp_parent + j));
-    for (int s = s0; s < s1; ++s) x[s] = dmul(rm_prob(__ldcg(r + s), S, s1 - s0), xp);
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const double xp = Ld::ld(x + __ldg(T.dp_parent + j));
+    if (n <= MAXA) {
+        double rr[MAXA];
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) rr[a] = Ld::ld(r + s0 + a);
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) S = dadd(S, rr[a] > 0.0 ? rr[a] : 0.0);
+#pragma unroll
+        for (int a = 0; a < MAXA; ++a)
+            if (a < n) x[s0 + a] = dmul(rm_prob(rr[a], S, n), xp);
+    } else {
+        double S = 0.0;
+        for (int s = s0; s < s0 + n; ++s) {
+            const double v = Ld::ld(r + s);
+            S = dadd(S, v > 0.0 ? v : 0.0);
+        }
+        for (int s = s0; s < s0 + n; ++s) x[s] = dmul(rm_prob(Ld::ld(r + s), S, n), xp);
+    }
 }
 
 // BR: best response to gradient g (pkg/oracle.py:186-221): strict '>' from
-// -inf in action order; s = g + C_s with C_s the child-DP sum as above.
+// -inf in action order; value g + C_s with C_s the child sum as above.
+template <class Ld>
 __device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __restrict__ g,
                                       double* __restrict__ W) {
     const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
     double best = -INFINITY;
     for (int s = s0; s < s1; ++s) {
-        const double v = dadd(__ldcg(g + s), child_sum(__ldg(T.child + s), W));
+        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(__ldg(T.child + s), W));
         if (v > best) best = v;
     }
     W[j] = best;
 }
 
-// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154),
-// optionally scaled by -1.0 (backend.scale(-1.0, ...), pkg/solvers.py:359,368).
+// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
+template <class Ld>
 __device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,
                                            const int* __restrict__ indices,
                                            const double* __restrict__ data,
                                            const double* __restrict__ x, int row) {
     const int k0 = __ldg(indptr + row), k1 = __ldg(indptr + row + 1);
     double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc = dadd(acc, dmul(__ldg(data + k), __ldcg(x + __ldg(indices + k))));
+    int k = k0;
+    for (; k + 2 <= k1; k += 2) {
+        const double d0 = __ldg(data + k), d1 = __ldg(data + k + 1);
+        const double x0 = Ld::ld(x + __ldg(indices + k)), x1 = Ld::ld(x + __ldg(indices + k + 1));
+        acc = dadd(dadd(acc, dmul(d0, x0)), dmul(d1, x1));
+    }
+    if (k < k1) acc = dadd(acc, dmul(__ldg(data + k), Ld::ld(x + __ldg(indices + k))));
     return acc;
 }
 

@@ -1,0 +1,351 @@
+// Persistent engine: whole CFR iterations inside ONE kernel launch.
+//
+// The level engine pays one kernel launch (~2-4 µs of graph-node latency)
+// per DP level and pass, which is all of the time for games whose levels
+// hold a few hundred DPs (Kuhn, Leduc, batched sweeps) and most of it for
+// Liar's dice.  Here the iteration is a host-built program of phases; a
+// phase is one DP level of one or both players (independent players share a
+// phase: both next() passes, both observe passes in simultaneous mode) or a
+// payoff SpMV, and phases are separated by a barrier:
+//
+//   CTA mode   one CTA per solve (batch = grid), barrier = __syncthreads,
+//              plain L1-cacheable loads — the whole solve lives on one SM.
+//   grid mode  one solve over a cooperative grid (co-residency guaranteed by
+//              cudaLaunchCooperativeKernel), barrier = atomic arrive +
+//              generation spin with gpu-scope fences, mutable state read
+//              L2-only (ld.global.cg) because producers are other SMs.
+//
+// The per-DP arithmetic is the same code as the level engine
+// (kernels.cuh), so iterates are bit-identical across engines.
+
+#include <algorithm>
+#include <type_traits>
+
+#include "runtime.h"
+
+namespace scfr {
+
+struct PArgs {
+    DevTree T[2];
+    double* r[2];
+    double* b[2];
+    double* x[2];
+    double* xpost[2];
+    double* avg[2];
+    double* u[2];
+    double* V[2];
+    int S[2], J[2];
+    const int* Uip;
+    const int* Uix;
+    const double* Ud;
+    int Urows;
+    const int* Tip;
+    const int* Tix;
+    const double* Td;
+    int Trows;
+    const double* wsched;
+    const double* pfsched;
+    const double* nfsched;
+    int cap;
+    const Phase* prog;
+    int nphase;
+    long long t0;
+    int n_iter;
+    int post, pred, plus, alt;
+    int* nonfinite;
+    long long* tdev;
+    unsigned* barrier;
+};
+
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// One phase's share of DPs for player-K, run by this thread: items
+// begin, begin+stride, ... < n of the level starting at DP lo.  Out of line
+// (one call per phase per thread) so each pass is register-allocated on its
+// own instead of every pass being inlined into the persistent loop.
+template <int MAXA, class Ld>
+__device__ __noinline__ void phase_dps(int kind, DevTree T, int lo, int n, int begin, int stride,
+                                       const double* u, double* r, double* b, double* x,
+                                       double* xpost, double* avg, double* V, double w, int post,
+                                       double pf, double nf, int pred, int plus, int* nonfinite) {
+    for (int i = begin; i < n; i += stride) {
+        const int j = lo + i;
+        switch (kind) {
+            case PH_TD_AVG:
+                if (j == 0) avg[0] = dadd(dmul(w, Ld::ld(x)), Ld::ld(avg));
+                td_dp<Ld>(T, j, b, x, avg, w);
+                break;
+            case PH_TD_POST:
+                td_dp<Ld>(T, j, b, xpost, nullptr, 0.0);
+                break;
+            case PH_CUR:
+                cur_dp<MAXA, Ld>(T, j, r, xpost);
+                break;
+            case PH_OBS:
+                obs_dp<MAXA, Ld>(T, j, u, r, b, V, post, pf, nf, pred == 0, nonfinite);
+                break;
+            case PH_PRED:
+                pred_dp<MAXA, Ld>(T, j, u, r, b, V, plus != 0);
+                break;
+        }
+    }
+}
+
+// Payoff SpMV share: rows [begin, n) step stride of M applied to x into out
+// (optionally scaled by -1).
+template <class Ld>
+__device__ __noinline__ void phase_spmv(const int* ip, const int* ix, const double* d, int n,
+                                        int begin, int stride, const double* x, double* out,
+                                        bool neg, int* nonfinite) {
+    for (int i = begin; i < n; i += stride) {
+        double acc = spmv_row<Ld>(ip, ix, d, x, i);
+        if (neg) acc = dmul(-1.0, acc);
+        if (!isfinite(acc)) atomicOr(nonfinite, 1);
+        out[i] = acc;
+    }
+}
+
+template <int K, int MAXA, class Ld>
+__device__ __forceinline__ void player_phase(const PArgs& a, const Phase& ph, int lo, int n,
+                                             int begin, int stride, int solve, double w,
+                                             double pf, double nf) {
+    if (n <= 0) return;
+    const size_t o = (size_t)solve * a.S[K];
+    phase_dps<MAXA, Ld>(ph.kind, a.T[K], lo, n, begin, stride, a.u[K] + o, a.r[K] + o,
+                        a.b[K] + o, a.x[K] + o, a.xpost[K] + o, a.avg[K] + o,
+                        a.V[K] + (size_t)solve * (a.J[K] > 0 ? a.J[K] : 1), w, a.post, pf, nf,
+                        a.pred, a.plus, a.nonfinite);
+}
+
+template <bool GRID, int MAXA, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_persistent(const __grid_constant__ PArgs a) {
+    using Ld = std::conditional_t<GRID, LdL2, LdL1>;
+    const int solve = GRID ? 0 : blockIdx.x;
+    const int rank = GRID ? blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
+    const int size = GRID ? gridDim.x * blockDim.x : blockDim.x;
+    const size_t o1 = (size_t)solve * a.S[0], o2 = (size_t)solve * a.S[1];
+    for (int it = 0; it < a.n_iter; ++it) {
+        const size_t si = (size_t)solve * a.cap + (size_t)(a.t0 + it);
+        const double w = a.wsched[si];
+        const double pf = a.post == POST_DCFR ? a.pfsched[si] : 1.0;
+        const double nf = a.post == POST_DCFR ? a.nfsched[si] : 1.0;
+        for (int p = 0; p < a.nphase; ++p) {
+            const Phase ph = a.prog[p];
+            if (ph.kind < PH_SPMV_U) {
+                // items [0,n1) are player-1 DPs, [n1,n1+n2) player-2 DPs
+                player_phase<0, MAXA, Ld>(a, ph, ph.lo1, ph.n1, rank, size, solve, w, pf, nf);
+                const int b2 = ((rank - ph.n1) % size + size) % size;
+                player_phase<1, MAXA, Ld>(a, ph, ph.lo2, ph.n2, b2, size, solve, w, pf, nf);
+            } else {
+                // payoff SpMV: rows of U (-> u1), then rows of Uᵀ (-> u2 = -Uᵀ x1)
+                const double* x1 = (a.alt ? a.xpost[0] : a.x[0]) + o1;
+                if (ph.kind != PH_SPMV_UT)
+                    phase_spmv<Ld>(a.Uip, a.Uix, a.Ud, a.Urows, rank, size, a.x[1] + o2,
+                                   a.u[0] + o1, false, a.nonfinite);
+                if (ph.kind != PH_SPMV_U) {
+                    const int b2 = ph.kind == PH_SPMV_BOTH ? ((rank - a.Urows) % size + size) % size : rank;
+                    phase_spmv<Ld>(a.Tip, a.Tix, a.Td, a.Trows, b2, size, x1, a.u[1] + o2, true,
+                                   a.nonfinite);
+                }
+            }
+            // a player without decision points still averages x[0] = 1
+            if (ph.first_avg && rank == 0) {
+                if (a.J[0] == 0) a.avg[0][o1] = dadd(dmul(w, Ld::ld(a.x[0] + o1)), Ld::ld(a.avg[0] + o1));
+                if (a.J[1] == 0) a.avg[1][o2] = dadd(dmul(w, Ld::ld(a.x[1] + o2)), Ld::ld(a.avg[1] + o2));
+            }
+            if (GRID) grid_sync(a.barrier);
+            else __syncthreads();
+        }
+    }
+    if (rank == 0 && (GRID || blockIdx.x == 0)) *a.tdev = a.t0 + a.n_iter;
+}
+
+// --- host side ---------------------------------------------------------------
+
+// CTA mode: 256 threads, 4 actions in registers; grid mode: 128 threads x
+// all SMs, 8 actions in registers (Liar's dice has up to 12-way DPs).
+static constexpr auto kCta = k_persistent<false, 4, 256>;
+static constexpr auto kGrid = k_persistent<true, 8, 128>;
+
+static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, const Player* B,
+                        bool deep_first) {
+    const int LA = A ? A->levels() : 0, LB = B ? B->levels() : 0;
+    const int L = std::max(LA, LB);
+    for (int k = 0; k < L; ++k) {
+        Phase ph{kind, 0, 0, 0, 0, 0};
+        const int la = deep_first ? LA - 1 - k : k, lb = deep_first ? LB - 1 - k : k;
+        if (A && la >= 0 && la < LA) {
+            ph.lo1 = A->lvl[la];
+            ph.n1 = A->lvl[la + 1] - A->lvl[la];
+        }
+        if (B && lb >= 0 && lb < LB) {
+            ph.lo2 = B->lvl[lb];
+            ph.n2 = B->lvl[lb + 1] - B->lvl[lb];
+        }
+        prog.push_back(ph);
+    }
+}
+
+static std::vector<Phase> build_program(const scfr_handle* h) {
+    const Player* A = &h->P[0];
+    const Player* Bp = &h->P[1];
+    const bool pr = predictive(h->variant);
+    std::vector<Phase> prog;
+    if (pr) push_levels(prog, PH_PRED, A, Bp, true);
+    const size_t first_td = prog.size();
+    push_levels(prog, PH_TD_AVG, A, Bp, false);
+    if (prog.size() == first_td) prog.push_back(Phase{PH_TD_AVG, 0, 0, 0, 0, 0});
+    prog[first_td].first_avg = 1;
+    if (h->mode == SCFR_MODE_SIM) {
+        prog.push_back(Phase{PH_SPMV_BOTH, 0, h->U.rows + h->UT.rows, 0, 0, 0});
+        push_levels(prog, PH_OBS, A, Bp, true);
+    } else {
+        prog.push_back(Phase{PH_SPMV_U, 0, h->U.rows, 0, 0, 0});
+        push_levels(prog, PH_OBS, A, nullptr, true);
+        push_levels(prog, pr ? PH_CUR : PH_TD_POST, A, nullptr, false);
+        prog.push_back(Phase{PH_SPMV_UT, 0, h->UT.rows, 0, 0, 0});
+        push_levels(prog, PH_OBS, nullptr, Bp, true);
+    }
+    return prog;
+}
+
+// Engine choice by size (sequences of both players, per solve): batches of
+// small games -> one CTA per solve; one small game -> one CTA; medium ->
+// cooperative grid; large (every level fills the GPU) -> level kernels.
+int choose_engine(scfr_handle* h) {
+    const int64_t S = (int64_t)h->P[0].S + h->P[1].S;
+    if (h->B > 1) return S <= 262144 ? SCFR_ENGINE_PERSISTENT : SCFR_ENGINE_LEVELS;
+    if (S <= 8192) return SCFR_ENGINE_PERSISTENT;
+    return S <= 262144 ? SCFR_ENGINE_PERSISTENT_GRID : SCFR_ENGINE_LEVELS;
+}
+
+void prepare_persistent(scfr_handle* h) {
+    PersistentPlan& pl = h->plan;
+    pl.grid = h->engine == SCFR_ENGINE_PERSISTENT_GRID;
+    pl.threads = pl.grid ? 128 : 256;  // must match kGrid / kCta
+    if (pl.grid) {
+        int occ = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kGrid, pl.threads, 0));
+        if (occ < 1) fail(SCFR_ECUDA, "persistent kernel cannot be resident");
+        int want = h->num_sms;
+        const char* env_ctas = std::getenv("SCFR_PERSIST_CTAS");
+        if (env_ctas) want = std::max(1, std::atoi(env_ctas));
+        pl.ctas = std::min(want, h->num_sms * occ);
+    } else {
+        pl.ctas = h->B;
+    }
+    pl.host_program = build_program(h);
+    pl.program.alloc(pl.host_program.size());
+    CUDA_OK(copy_async(pl.program.p, pl.host_program.data(), pl.host_program.size() * sizeof(Phase),
+                       cudaMemcpyHostToDevice, h->stream));
+    pl.barrier.alloc(2);
+    pl.barrier.zero(h->stream);
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+}
+
+int64_t launch_persistent(scfr_handle* h, int64_t n) {
+    PersistentPlan& pl = h->plan;
+    PArgs a;
+    for (int k = 0; k < 2; ++k) {
+        Player& P = h->P[k];
+        a.T[k] = P.tree();
+        a.r[k] = P.r.p;
+        a.b[k] = P.b.p;
+        a.x[k] = P.x.p;
+        a.xpost[k] = P.xpost.p;
+        a.avg[k] = P.avg.p;
+        a.u[k] = P.u.p;
+        a.V[k] = P.V.p;
+        a.S[k] = P.S;
+        a.J[k] = P.J;
+    }
+    a.Uip = h->U.indptr.p;
+    a.Uix = h->U.indices.p;
+    a.Ud = h->U.data.p;
+    a.Urows = h->U.rows;
+    a.Tip = h->UT.indptr.p;
+    a.Tix = h->UT.indices.p;
+    a.Td = h->UT.data.p;
+    a.Trows = h->UT.rows;
+    a.wsched = h->wsched.p;
+    a.pfsched = h->pfsched.p;
+    a.nfsched = h->nfsched.p;
+    a.cap = h->cap;
+    a.prog = pl.program.p;
+    a.nphase = (int)pl.host_program.size();
+    a.post = post_of(h->variant);
+    a.pred = predictive(h->variant) ? 1 : 0;
+    a.plus = h->variant == SCFR_PCFR_PLUS ? 1 : 0;
+    a.alt = h->mode == SCFR_MODE_ALT ? 1 : 0;
+    a.nonfinite = h->nonfinite.p;
+    a.tdev = h->tdev.p;
+    a.barrier = pl.barrier.p;
+    int64_t launches = 0;
+    // Chunk long requests so one launch stays well under the watchdog-free
+    // but still bounded duration, and the schedule index fits in int.
+    const int64_t chunk = 1 << 16;
+    for (int64_t done = 0; done < n; done += chunk) {
+        a.t0 = h->t + done;
+        a.n_iter = (int)std::min<int64_t>(chunk, n - done);
+        if (pl.grid) {
+            void* args[] = {&a};
+            CUDA_OK(cudaLaunchCooperativeKernel((const void*)kGrid, dim3(pl.ctas),
+                                                dim3(pl.threads), args, 0, h->stream));
+        } else {
+            kCta<<<pl.ctas, pl.threads, 0, h->stream>>>(a);
+            CUDA_OK(cudaGetLastError());
+        }
+        ++launches;
+    }
+    return launches;
+}
+
+double persistent_bytes_per_iter(const scfr_handle* h) {
+    // Same algorithmic-byte model as the level engine (solver.cu LevelBytes).
+    double total = 0.0;
+    for (const Phase& ph : h->plan.host_program) {
+        for (int k = 0; k < 2; ++k) {
+            const int lo = k == 0 ? ph.lo1 : ph.lo2, n = k == 0 ? ph.n1 : ph.n2;
+            if (n == 0 || ph.kind >= PH_SPMV_U) continue;
+            const Player& P = h->P[k];
+            int l = (int)(std::upper_bound(P.lvl.begin(), P.lvl.end(), lo) - P.lvl.begin()) - 1;
+            if (l < 0 || l >= P.levels()) continue;
+            const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
+            switch (ph.kind) {
+                case PH_TD_AVG: total += 32 * ns + 16 * nj; break;
+                case PH_TD_POST:
+                case PH_CUR: total += 16 * ns + 16 * nj; break;
+                case PH_OBS: total += (predictive(h->variant) ? 40 : 48) * ns + 12 * nj + 8 * nc; break;
+                case PH_PRED: total += 40 * ns + 12 * nj + 8 * nc; break;
+            }
+        }
+        if (ph.kind >= PH_SPMV_U) {
+            const DevCsr* ms[2] = {&h->U, &h->UT};
+            for (int k = 0; k < 2; ++k) {
+                if ((ph.kind == PH_SPMV_U && k == 1) || (ph.kind == PH_SPMV_UT && k == 0)) continue;
+                const DevCsr& M = *ms[k];
+                total += 4.0 * (M.rows + 1) + 12.0 * M.nnz + 8.0 * M.cols + 8.0 * M.rows;
+            }
+        }
+    }
+    return total * h->B;
+}
+
+}  // namespace scfr

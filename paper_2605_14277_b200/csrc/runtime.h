@@ -1,0 +1,158 @@
+// Device-runtime types shared by the level engine (solver.cu) and the
+// persistent engine (persistent.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+
+#define CUDA_OK(expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            ::scfr::fail(SCFR_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));     \
+    } while (0)
+
+namespace scfr {
+
+constexpr int TPB = 128;
+
+// Process-wide host<->device byte counters (scfr_transfer_bytes).
+inline std::atomic<int64_t> g_h2d{0}, g_d2h{0};
+inline void count_copy(size_t n, cudaMemcpyKind k) {
+    if (k == cudaMemcpyHostToDevice) g_h2d += (int64_t)n;
+    else if (k == cudaMemcpyDeviceToHost) g_d2h += (int64_t)n;
+}
+inline cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k,
+                              cudaStream_t s) {
+    count_copy(n, k);
+    return cudaMemcpyAsync(dst, src, n, k, s);
+}
+inline cudaError_t copy_sync(void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+    count_copy(n, k);
+    return cudaMemcpy(dst, src, n, k);
+}
+
+enum KernelKind : int {
+    KK_TD_AVG = 0, KK_TD, KK_CUR, KK_OBS_RM, KK_OBS, KK_PRED, KK_SPMV, KK_TICK, KK_PERSIST,
+    KK_COUNT
+};
+inline const char* kKernelNames[KK_COUNT] = {"td_avg", "td", "cur", "obs_rm", "obs",
+                                             "pred", "spmv", "tick", "persistent"};
+struct KernelRecord {
+    int kind;
+    double bytes;
+    cudaEvent_t e0, e1;
+};
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CUDA_OK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    ~DevBuf() { free(); }
+};
+
+struct Player {
+    int S = 0, J = 0;
+    int max_actions = 0;
+    std::vector<int> lvl;                        // DP level starts (process depth), size L+1
+    std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
+    std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
+    DevBuf<int> seq_ptr, dp_parent;
+    DevBuf<int2> child;
+    DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
+    DevBuf<double> g, W, xbar;                 // best-response scratch, one solve
+    DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
+    int levels() const { return (int)lvl.size() - 1; }
+};
+
+struct DevCsr {
+    int rows = 0, cols = 0, nnz = 0;
+    DevBuf<int> indptr, indices;
+    DevBuf<double> data;
+};
+
+// One phase of the persistent program: a DP level of one or both players
+// (items [0,n1) -> player 1 DPs lo1.., [n1,n1+n2) -> player 2 DPs lo2..),
+// or a payoff SpMV over rows.
+struct Phase {
+    int kind;  // PH_*
+    int lo1, n1, lo2, n2;
+    int first_avg;  // the first TD_AVG phase also averages x[0] of DP-less players
+};
+enum : int { PH_TD_AVG = 0, PH_TD_POST, PH_CUR, PH_OBS, PH_PRED, PH_SPMV_U, PH_SPMV_UT,
+             PH_SPMV_BOTH };
+
+struct PersistentPlan {
+    bool grid = false;  // true: one solve over a cooperative grid; false: one CTA per solve
+    int ctas = 0, threads = 0;
+    std::vector<Phase> host_program;
+    DevBuf<Phase> program;
+    DevBuf<unsigned> barrier;  // {count, generation}
+};
+
+bool predictive(int v);
+int post_of(int v);
+inline int grid_for(int n) { return n <= 0 ? 1 : (n + TPB - 1) / TPB; }
+
+}  // namespace scfr
+
+struct scfr_handle {
+    int device = 0;
+    int B = 1;
+    int variant = 0, mode = 0;
+    int engine = SCFR_ENGINE_LEVELS;
+    int num_sms = 148;
+    std::vector<double> alpha, beta, gamma;
+    scfr::Player P[2];
+    scfr::DevCsr U, UT;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int cap = 0;                 // schedule capacity (iterations)
+    std::vector<double> w_host;  // [B][cap]
+    scfr::DevBuf<double> wsched, pfsched, nfsched;
+    scfr::DevBuf<long long> tdev;
+    scfr::DevBuf<int> nonfinite;
+    scfr::DevBuf<double> brout;
+    int64_t t = 0;                   // completed iterations
+    std::vector<double> avg_weight;  // [B]
+    cudaGraphExec_t exec = nullptr;
+    int64_t nodes_per_iter = 0;
+    int64_t launches = 0;
+    bool use_graph = true;
+    bool timed = false;
+    scfr::PersistentPlan plan;
+    ~scfr_handle() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace scfr {
+int choose_engine(scfr_handle* h);
+void prepare_persistent(scfr_handle* h);
+// Enqueues n iterations; returns the number of kernel launches issued.
+int64_t launch_persistent(scfr_handle* h, int64_t n);
+double persistent_bytes_per_iter(const scfr_handle* h);
+}  // namespace scfr

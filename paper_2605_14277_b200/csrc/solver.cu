@@ -1,5 +1,7 @@
-// Device runtime behind the C-ABI: structure upload, per-iteration kernel
-// schedule captured as a CUDA graph, on-device best response.
+// Device runtime behind the C-ABI: structure upload, the level engine (one
+// kernel per DP level, captured once as a CUDA graph), on-device best
+// response, and the C entry points.  The persistent engine is in
+// persistent.cu.
 //
 // One iteration is the reference _step (pkg/solvers.py:351-372):
 //   sim:  next1, next2, u1 = U x2, u2 = -Uᵀ x1, observe1(u1), observe2(u2)
@@ -14,55 +16,29 @@
 // schedules indexed by a device-side iteration counter, so one captured
 // graph serves every iteration.
 
-#include <cuda_runtime.h>
-
 #include <algorithm>
-#include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
 
-#include "common.h"
-#include "kernels.cuh"
-#include "persistent.cuh"
+#include "runtime.h"
 
 namespace scfr {
 
-#define CUDA_OK(expr)                                                                       \
-    do {                                                                                    \
-        cudaError_t _e = (expr);                                                            \
-        if (_e != cudaSuccess)                                                              \
-            ::scfr::fail(SCFR_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));      \
-    } while (0)
-
-constexpr int TPB = 128;
-
-// Process-wide host<->device byte counters (scfr_transfer_bytes).
-static std::atomic<int64_t> g_h2d{0}, g_d2h{0};
-static void count_copy(size_t n, cudaMemcpyKind k) {
-    if (k == cudaMemcpyHostToDevice) g_h2d += (int64_t)n;
-    else if (k == cudaMemcpyDeviceToHost) g_d2h += (int64_t)n;
+bool predictive(int v) { return v == SCFR_PCFR || v == SCFR_PCFR_PLUS; }
+int post_of(int v) {
+    if (v == SCFR_CFR_PLUS || v == SCFR_PCFR_PLUS) return POST_PLUS;
+    if (v == SCFR_DCFR) return POST_DCFR;
+    return POST_NONE;
 }
-static cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t s) {
-    count_copy(n, k);
-    return cudaMemcpyAsync(dst, src, n, k, s);
-}
-static cudaError_t copy_sync(void* dst, const void* src, size_t n, cudaMemcpyKind k) {
-    count_copy(n, k);
-    return cudaMemcpy(dst, src, n, k);
-}
-
-enum KernelKind : int { KK_TD_AVG = 0, KK_TD, KK_CUR, KK_OBS_RM, KK_OBS, KK_PRED, KK_SPMV, KK_TICK, KK_COUNT };
-static const char* kKernelNames[KK_COUNT] = {"td_avg", "td", "cur", "obs_rm", "obs", "pred", "spmv", "tick"};
-struct KernelRecord {
-    int kind;
-    double bytes;
-    cudaEvent_t e0, e1;
-};
 
 // ---------------------------------------------------------------------------
-// Level kernels (blockIdx.y = solve within the batch).
+// Level kernels (blockIdx.y = solve within the batch).  Producers of every
+// value read here ran in earlier launches, so plain L1-cacheable loads are
+// coherent.
 
 __global__ void k_td(DevTree T, int lo, int hi, int S, const double* __restrict__ b,
                      double* __restrict__ x, double* __restrict__ avg,
@@ -76,9 +52,9 @@ __global__ void k_td(DevTree T, int lo, int hi, int S, const double* __restrict_
         w = wsched[(size_t)blockIdx.y * cap + *tdev];
         a = avg + o;
         // the reference axpy also covers the empty sequence (x[0] = 1)
-        if (j == 0) a[0] = dadd(dmul(w, __ldcg(x + o)), __ldcg(a));
+        if (j == 0) a[0] = dadd(dmul(w, x[o]), a[0]);
     }
-    td_dp(T, j, b + o, x + o, a, w);
+    td_dp<LdL1>(T, j, b + o, x + o, a, w);
 }
 
 // avg[0] update for a player without decision points (no TD levels).
@@ -89,14 +65,16 @@ __global__ void k_avg0(int S, const double* __restrict__ x, double* __restrict__
     avg[o] = dadd(dmul(w, x[o]), avg[o]);
 }
 
+template <int MAXA>
 __global__ void k_cur(DevTree T, int lo, int hi, int S, const double* __restrict__ r,
                       double* __restrict__ x) {
     const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= hi) return;
     const size_t o = (size_t)blockIdx.y * S;
-    cur_dp(T, j, r + o, x + o);
+    cur_dp<MAXA, LdL1>(T, j, r + o, x + o);
 }
 
+template <int MAXA>
 __global__ void k_obs(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ u,
                       double* __restrict__ r, double* __restrict__ b, double* __restrict__ V,
                       int post, const double* __restrict__ pfs, const double* __restrict__ nfs,
@@ -110,30 +88,31 @@ __global__ void k_obs(DevTree T, int lo, int hi, int S, int J, const double* __r
         pf = pfs[k];
         nf = nfs[k];
     }
-    obs_dp(T, j, u + o, r + o, b + o, V + (size_t)blockIdx.y * J, post, pf, nf, do_rm != 0,
-           nonfinite);
+    obs_dp<MAXA, LdL1>(T, j, u + o, r + o, b + o, V + (size_t)blockIdx.y * J, post, pf, nf, do_rm != 0,
+                 nonfinite);
 }
 
+template <int MAXA>
 __global__ void k_pred(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ m,
                        const double* __restrict__ r, double* __restrict__ b,
                        double* __restrict__ V, int plus) {
     const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= hi) return;
     const size_t o = (size_t)blockIdx.y * S;
-    pred_dp(T, j, m + o, r + o, b + o, V + (size_t)blockIdx.y * J, plus != 0);
+    pred_dp<MAXA, LdL1>(T, j, m + o, r + o, b + o, V + (size_t)blockIdx.y * J, plus != 0);
 }
 
 __global__ void k_br(DevTree T, int lo, int hi, const double* __restrict__ g,
                      double* __restrict__ W) {
     const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= hi) return;
-    br_dp(T, j, g, W);
+    br_dp<LdL1>(T, j, g, W);
 }
 
 // br = g[0] + value of the root (the empty sequence's child sum).
 __global__ void k_br_root(DevTree T, const double* __restrict__ g, const double* __restrict__ W,
                           double* out) {
-    *out = dadd(g[0], child_sum(T.child[0], W));
+    *out = dadd(g[0], child_sum<LdL1>(T.child[0], W));
 }
 
 __global__ void k_spmv(int rows, const int* __restrict__ indptr, const int* __restrict__ indices,
@@ -141,7 +120,7 @@ __global__ void k_spmv(int rows, const int* __restrict__ indptr, const int* __re
                        double* __restrict__ out, int so, int negate, int* nonfinite) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
-    double acc = spmv_row(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
+    double acc = spmv_row<LdL1>(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
     if (negate) acc = dmul(-1.0, acc);
     if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);
     out[(size_t)blockIdx.y * so + row] = acc;
@@ -154,93 +133,6 @@ __global__ void k_normalize(const double* __restrict__ a, double w, double* __re
 
 __global__ void k_tick(long long* tdev) { *tdev += 1; }
 
-// ---------------------------------------------------------------------------
-
-template <class T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    void alloc(size_t count) {
-        free();
-        n = count;
-        if (count) CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
-    }
-    void zero(cudaStream_t s) {
-        if (n) CUDA_OK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
-    }
-    void free() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    size_t bytes() const { return n * sizeof(T); }
-    ~DevBuf() { free(); }
-};
-
-struct Player {
-    int S = 0, J = 0;
-    std::vector<int> lvl;  // DP level starts (by process-tree depth), size L+1
-    std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
-    std::vector<double> uniform;  // host copy of the uniform behaviour (slot 0 = 0)
-    DevBuf<int> seq_ptr, dp_parent;
-    DevBuf<int2> child;
-    DevBuf<double> r, b, x, xpost, avg, u, V;   // batched [B][...]
-    DevBuf<double> g, W, xbar;                   // best-response scratch, one solve
-    DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
-    int levels() const { return (int)lvl.size() - 1; }
-};
-
-struct DevCsr {
-    int rows = 0, cols = 0, nnz = 0;
-    DevBuf<int> indptr, indices;
-    DevBuf<double> data;
-};
-
-}  // namespace scfr
-
-struct scfr_handle {
-    int device = 0;
-    int B = 1;
-    int variant = 0, mode = 0;
-    int engine = SCFR_ENGINE_LEVELS;
-    std::vector<double> alpha, beta, gamma;
-    scfr::Player P[2];
-    scfr::DevCsr U, UT;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // schedules [B][cap]
-    int cap = 0;
-    std::vector<double> w_host;  // [B][cap]
-    scfr::DevBuf<double> wsched, pfsched, nfsched;
-    scfr::DevBuf<long long> tdev;
-    scfr::DevBuf<int> nonfinite;
-    scfr::DevBuf<double> brout;
-    int64_t t = 0;                 // completed iterations
-    std::vector<double> avg_weight;  // [B]
-    cudaGraphExec_t exec = nullptr;
-    int64_t nodes_per_iter = 0;
-    int64_t launches = 0;
-    int64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued by the API
-    bool use_graph = true;
-    bool timed = false;
-    scfr::PersistentPlan plan;
-    ~scfr_handle() {
-        if (exec) cudaGraphExecDestroy(exec);
-        if (ev0) cudaEventDestroy(ev0);
-        if (ev1) cudaEventDestroy(ev1);
-        if (stream) cudaStreamDestroy(stream);
-    }
-};
-
-namespace scfr {
-
-static bool predictive(int v) { return v == SCFR_PCFR || v == SCFR_PCFR_PLUS; }
-static int post_of(int v) {
-    if (v == SCFR_CFR_PLUS || v == SCFR_PCFR_PLUS) return POST_PLUS;
-    if (v == SCFR_DCFR) return POST_DCFR;
-    return POST_NONE;
-}
-
 // float(t) ** e with the reference's semantics (pkg/solvers.py:82-94, :172):
 // both go through libm pow(); an infinite power gives DCFR factor 1.
 static double tpow(int64_t t, double e) { return std::pow((double)t, e); }
@@ -249,8 +141,6 @@ static double dfactor(int64_t t, double e) {
     if (std::isinf(p)) return 1.0;
     return p / (p + 1.0);
 }
-
-static int grid_for(int n) { return std::max(1, (n + TPB - 1) / TPB); }
 
 static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s) {
     if (!p || p->num_seqs < 1 || p->num_decisions < 0 || p->num_nodes < 1)
@@ -261,9 +151,10 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     const int S = (int)p->num_seqs, J = (int)p->num_decisions;
     P.S = S;
     P.J = J;
+    P.max_actions = 0;
     std::vector<int> seq_ptr(J + 1), dp_parent(J);
     std::vector<int2> child(S, make_int2(0, 0));
-    P.uniform.assign(S, 0.0);
+    std::vector<double> uniform(S, 0.0);
     int64_t next = 1;
     int64_t prev_depth = -1;
     P.lvl.clear();
@@ -271,8 +162,9 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
         if (p->dp_first_seq[j] != next) fail(SCFR_EINVAL, "dp_first_seq is not contiguous in j");
         const int64_t n = p->dp_num_actions[j];
         if (n < 1) fail(SCFR_EINVAL, "decision point without actions");
+        P.max_actions = std::max<int>(P.max_actions, (int)n);
         seq_ptr[j] = (int)next;
-        for (int64_t a = 0; a < n; ++a) P.uniform[next + a] = 1.0 / (double)n;
+        for (int64_t a = 0; a < n; ++a) uniform[next + a] = 1.0 / (double)n;
         next += n;
         const int64_t ps = p->dp_parent_seq[j];
         if (ps < 0 || ps >= S) fail(SCFR_EINVAL, "dp_parent_seq out of range");
@@ -291,21 +183,24 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.lvl.push_back(J);
     if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     seq_ptr[J] = S;
+    for (int j = 0; j < J; ++j)
+        if (dp_parent[j] >= seq_ptr[j]) fail(SCFR_EINVAL, "parent sequence after its decision point");
     P.lvl_ns.clear();
     P.lvl_nj.clear();
     P.lvl_nc.clear();
+    P.lvl_maxa.clear();
     for (size_t l = 0; l + 1 < P.lvl.size(); ++l) {
         const int j0 = P.lvl[l], j1 = P.lvl[l + 1];
-        const int s0 = seq_ptr[j0], s1 = j1 < J ? seq_ptr[j1] : (int)next;
+        const int s0 = seq_ptr[j0], s1 = seq_ptr[j1];
         double nc = 0;
-        for (int s = s0; s < s1; ++s) nc += child[s].y;
+        for (int q = s0; q < s1; ++q) nc += child[q].y;
+        int ma = 0;
+        for (int j = j0; j < j1; ++j) ma = std::max(ma, seq_ptr[j + 1] - seq_ptr[j]);
+        P.lvl_maxa.push_back(ma);
         P.lvl_ns.push_back(s1 - s0);
         P.lvl_nj.push_back(j1 - j0);
         P.lvl_nc.push_back(nc);
     }
-    // parent sequences precede their decision point's level
-    for (int j = 0; j < J; ++j)
-        if (dp_parent[j] >= seq_ptr[j]) fail(SCFR_EINVAL, "parent sequence after its decision point");
 
     P.seq_ptr.alloc(J + 1);
     P.dp_parent.alloc(std::max(J, 1));
@@ -326,19 +221,16 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.W.alloc(std::max(J, 1));
     P.xbar.alloc(S);
     for (auto* buf : {&P.r, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
-    // b = uniform; x[0] = xpost[0] = 1 (the empty sequence's mass).
-    std::vector<double> init((size_t)S * B);
-    for (int k = 0; k < B; ++k) std::copy(P.uniform.begin(), P.uniform.end(), init.begin() + (size_t)k * S);
-    CUDA_OK(copy_async(P.b.p, init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaStreamSynchronize(s));
-    std::vector<double> ones((size_t)S * B, 0.0);
-    for (int k = 0; k < B; ++k) ones[(size_t)k * S] = 1.0;
-    // set slot 0 of every solve to 1.0 via a strided copy
-    CUDA_OK(cudaMemcpy2DAsync(P.x.p, S * sizeof(double), ones.data(), S * sizeof(double),
-                              sizeof(double), B, cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaMemcpy2DAsync(P.xpost.p, S * sizeof(double), ones.data(), S * sizeof(double),
-                              sizeof(double), B, cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaStreamSynchronize(s));
+    // b = uniform for every solve; x[0] = xpost[0] = 1 (the empty sequence's mass)
+    for (int k = 0; k < B; ++k)
+        CUDA_OK(copy_async(P.b.p + (size_t)k * S, uniform.data(), S * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+    const double one = 1.0;
+    for (int k = 0; k < B; ++k) {
+        CUDA_OK(copy_async(P.x.p + (size_t)k * S, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+        CUDA_OK(copy_async(P.xpost.p + (size_t)k * S, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    CUDA_OK(cudaStreamSynchronize(s));  // host staging vectors die at return
 }
 
 static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s) {
@@ -443,7 +335,8 @@ struct Launcher {
             const int lo = P.lvl[l], hi = P.lvl[l + 1];
             launch(KK_CUR, LevelBytes::cur(P, l), [&] {
                 dim3 grid(grid_for(hi - lo), h->B);
-                k_cur<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, P.r.p, P.xpost.p);
+                auto kern = P.lvl_maxa[l] <= 2 ? k_cur<2> : P.lvl_maxa[l] <= 4 ? k_cur<4> : k_cur<8>;
+                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, P.r.p, P.xpost.p);
             });
         }
     }
@@ -452,8 +345,9 @@ struct Launcher {
             const int lo = P.lvl[l], hi = P.lvl[l + 1];
             launch(KK_PRED, LevelBytes::pred(P, l), [&] {
                 dim3 grid(grid_for(hi - lo), h->B);
-                k_pred<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
-                                                    P.r.p, P.b.p, P.V.p, plus ? 1 : 0);
+                auto kern = P.lvl_maxa[l] <= 2 ? k_pred<2> : P.lvl_maxa[l] <= 4 ? k_pred<4> : k_pred<8>;
+                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
+                                                  P.r.p, P.b.p, P.V.p, plus ? 1 : 0);
             });
         }
     }
@@ -462,10 +356,11 @@ struct Launcher {
             const int lo = P.lvl[l], hi = P.lvl[l + 1];
             launch(rm ? KK_OBS_RM : KK_OBS, LevelBytes::obs(P, l, rm), [&] {
                 dim3 grid(grid_for(hi - lo), h->B);
-                k_obs<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
-                                                   P.r.p, P.b.p, P.V.p, post, h->pfsched.p,
-                                                   h->nfsched.p, h->cap, h->tdev.p, rm ? 1 : 0,
-                                                   h->nonfinite.p);
+                auto kern = P.lvl_maxa[l] <= 2 ? k_obs<2> : P.lvl_maxa[l] <= 4 ? k_obs<4> : k_obs<8>;
+                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
+                                                  P.r.p, P.b.p, P.V.p, post, h->pfsched.p,
+                                                  h->nfsched.p, h->cap, h->tdev.p, rm ? 1 : 0,
+                                                  h->nonfinite.p);
             });
         }
     }
@@ -476,21 +371,19 @@ struct Launcher {
         const bool pr = predictive(h->variant);
         const int post = post_of(h->variant);
         const bool plus = h->variant == SCFR_PCFR_PLUS;
-        // next_strategy for both players
-        for (Player* P : {&A, &Bp}) {
+        for (Player* P : {&A, &Bp}) {  // next_strategy for both players
             if (pr) pred(*P, plus);
             td(*P, P->b.p, P->x.p, true);
         }
-        // u1 = U x2 ; sim: u2 = -Uᵀ x1
-        spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);
+        spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
-            spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);
+            spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1
             obs(A, post, !pr);
         } else {
             obs(A, post, !pr);
             if (pr) cur(A);
             else td(A, A.b.p, A.xpost.p, false);
-            spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);
+            spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1'
         }
         obs(Bp, post, !pr);
         launch(KK_TICK, 0.0, [&] { k_tick<<<1, 1, 0, h->stream>>>(h->tdev.p); });
@@ -545,12 +438,16 @@ static void check_player(const scfr_handle* h, int player, int solve) {
     if (solve < 0 || solve >= h->B) fail(SCFR_EINVAL, "solve index out of range");
 }
 
+static void add_weights(scfr_handle* h, int64_t n) {
+    ensure_schedule(h, h->t + n);
+    for (int k = 0; k < h->B; ++k)
+        for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
+}
+
 // Best response of `player` against the opponent's strategy x_opp (one solve).
 static double best_response(scfr_handle* h, int player, const double* x_opp) {
     Player& P = h->P[player - 1];
     const DevCsr& M = player == 1 ? h->U : h->UT;
-    Player& O = h->P[2 - player];
-    (void)O;
     k_spmv<<<dim3(grid_for(M.rows), 1), TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p, M.data.p,
                                                             x_opp, 0, P.g.p, 0, player == 2 ? 1 : 0,
                                                             nullptr);
@@ -578,14 +475,6 @@ static const double* profile(scfr_handle* h, int player, int solve, int which) {
     return P.xbar.p;
 }
 
-static int choose_engine(scfr_handle*) { return SCFR_ENGINE_LEVELS; }
-static void prepare_persistent(scfr_handle*) {
-    fail(SCFR_EINVAL, "persistent engine not available in this build");
-}
-static int64_t launch_persistent(scfr_handle*, int64_t) {
-    fail(SCFR_EINVAL, "persistent engine not available in this build");
-}
-
 }  // namespace scfr
 
 using namespace scfr;
@@ -595,10 +484,13 @@ extern "C" {
 int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, const scfr_csr* UT,
                 const scfr_config* cfg, int device, scfr_handle** out) {
     return guarded([&] {
-        if (!out || !cfg) fail(SCFR_EINVAL, "NULL argument");
+        if (!out || !cfg || !p1 || !p2 || !U || !UT) fail(SCFR_EINVAL, "NULL argument");
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
         if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
         if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
+        if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_PERSISTENT_GRID) fail(SCFR_EINVAL, "unknown engine");
+        if (cfg->engine == SCFR_ENGINE_PERSISTENT_GRID && cfg->batch != 1)
+            fail(SCFR_EINVAL, "the grid-persistent engine runs a single solve (batch 1)");
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
         if (e != cudaSuccess || ndev == 0) fail(SCFR_ECUDA, "no CUDA device available: %s", cudaGetErrorString(e));
@@ -609,6 +501,7 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         if (prop.major < 10) fail(SCFR_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
         std::unique_ptr<scfr_handle> h(new scfr_handle());
         h->device = device;
+        h->num_sms = prop.multiProcessorCount;
         h->B = cfg->batch;
         h->variant = cfg->variant;
         h->mode = cfg->mode;
@@ -641,10 +534,19 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         h->avg_weight.assign(h->B, 0.0);
         const char* ng = std::getenv("SCFR_NO_GRAPH");
         h->use_graph = !(ng && ng[0] == '1');
+        const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
+        if (eng && h->engine == SCFR_ENGINE_AUTO) h->engine = std::atoi(eng);
         if (h->engine == SCFR_ENGINE_AUTO) h->engine = choose_engine(h.get());
-        if (h->engine == SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
+        if (h->engine >= SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
         *out = h.release();
+    });
+}
+
+int scfr_engine(const scfr_handle* h, int* engine) {
+    return guarded([&] {
+        if (!h || !engine) fail(SCFR_EINVAL, "NULL argument");
+        *engine = h->engine;
     });
 }
 
@@ -654,11 +556,9 @@ int scfr_step(scfr_handle* h, int64_t n) {
         if (n < 0) fail(SCFR_EINVAL, "n_iter must be >= 0");
         if (n == 0) return;
         set_device(h);
-        ensure_schedule(h, h->t + n);
-        for (int k = 0; k < h->B; ++k)
-            for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
+        add_weights(h, n);
         CUDA_OK(cudaEventRecord(h->ev0, h->stream));
-        if (h->engine == SCFR_ENGINE_PERSISTENT) {
+        if (h->engine >= SCFR_ENGINE_PERSISTENT) {
             h->launches += launch_persistent(h, n);
         } else if (h->use_graph) {
             if (!h->exec) build_graph(h);
@@ -681,20 +581,30 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
         if (!h || !out || !count || cap < KK_COUNT) fail(SCFR_EINVAL, "bad arguments");
         if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
         set_device(h);
-        ensure_schedule(h, h->t + n);
-        for (int k = 0; k < h->B; ++k)
-            for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
+        add_weights(h, n);
         std::vector<KernelRecord> recs;
-        Launcher L{h};
-        L.prof = &recs;
-        CUDA_OK(cudaEventRecord(h->ev0, h->stream));
-        for (int64_t i = 0; i < n; ++i) L.iteration();
-        CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+        int64_t issued = 0;
+        if (h->engine >= SCFR_ENGINE_PERSISTENT) {
+            KernelRecord r;
+            r.kind = KK_PERSIST;
+            r.bytes = persistent_bytes_per_iter(h) * (double)n;
+            CUDA_OK(cudaEventCreate(&r.e0));
+            CUDA_OK(cudaEventCreate(&r.e1));
+            CUDA_OK(cudaEventRecord(r.e0, h->stream));
+            issued = launch_persistent(h, n);
+            CUDA_OK(cudaEventRecord(r.e1, h->stream));
+            recs.push_back(r);
+        } else {
+            Launcher L{h};
+            L.prof = &recs;
+            for (int64_t i = 0; i < n; ++i) L.iteration();
+            issued = L.count;
+        }
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaStreamSynchronize(h->stream));
-        h->timed = true;
+        h->timed = false;
         h->t += n;
-        h->launches += L.count;
+        h->launches += issued;
         for (int k = 0; k < KK_COUNT; ++k) {
             std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[k]);
             out[k].launches = 0;
@@ -748,10 +658,9 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
         size_t off = 0, cnt = P.S;
         switch (which) {
             case SCFR_STATE_REGRETS: src = P.r.p; off = 1; cnt = P.S - 1; break;
-            case SCFR_STATE_BEHAVIOR:
-                // non-predictive OBS regret-matches ahead of time; expose the
-                // behaviour the reference holds (the one used last iteration)
-                src = P.b.p; off = 1; cnt = P.S - 1; break;
+            // Non-predictive variants regret-match inside OBS, so this is the
+            // behaviour the *next* iteration will play.
+            case SCFR_STATE_BEHAVIOR: src = P.b.p; off = 1; cnt = P.S - 1; break;
             case SCFR_STATE_ACCUM: src = P.avg.p; break;
             case SCFR_STATE_UTILITY: src = P.u.p; break;
             default: fail(SCFR_EINVAL, "unknown state selector");
@@ -769,7 +678,7 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         set_device(h);
         Player& P = h->P[player - 1];
         CUDA_OK(copy_async(host_out, P.avg.p + (size_t)solve * P.S, P.S * sizeof(double),
-                                cudaMemcpyDeviceToHost, h->stream));
+                           cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         const double w = h->avg_weight[solve];
         for (int i = 0; i < P.S; ++i) host_out[i] = host_out[i] / w;
@@ -784,7 +693,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
         set_device(h);
         Player& P = h->P[player - 1];
         CUDA_OK(copy_async(host_out, P.x.p + (size_t)solve * P.S, P.S * sizeof(double),
-                                cudaMemcpyDeviceToHost, h->stream));
+                           cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
     });
 }
@@ -807,6 +716,12 @@ int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl, doub
     });
 }
 
+static double host_dot(const std::vector<double>& x, const std::vector<double>& g) {
+    double acc = 0.0;  // Backend.dot: sequential (pkg/kernels.py:278-283)
+    for (size_t i = 0; i < x.size(); ++i) acc = acc + x[i] * g[i];
+    return acc;
+}
+
 int scfr_expected_value(scfr_handle* h, int solve, double* out) {
     return guarded([&] {
         check_player(h, 1, solve);
@@ -821,9 +736,7 @@ int scfr_expected_value(scfr_handle* h, int solve, double* out) {
         CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(copy_async(x.data(), A.xbar.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
-        double acc = 0.0;  // Backend.dot: sequential (pkg/kernels.py:278-283)
-        for (int i = 0; i < A.S; ++i) acc = acc + x[i] * g[i];
-        *out = acc;
+        *out = host_dot(x, g);
     });
 }
 
@@ -852,12 +765,10 @@ int scfr_expected_value_of(scfr_handle* h, const double* x1, const double* x2, d
         CUDA_OK(copy_async(Bp.xbar.p, x2, Bp.S * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         k_spmv<<<dim3(grid_for(h->U.rows), 1), TPB, 0, h->stream>>>(h->U.rows, h->U.indptr.p, h->U.indices.p,
                                                                    h->U.data.p, Bp.xbar.p, 0, A.g.p, 0, 0, nullptr);
-        std::vector<double> g(A.S);
+        std::vector<double> g(A.S), x(x1, x1 + A.S);
         CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
-        double acc = 0.0;
-        for (int i = 0; i < A.S; ++i) acc = acc + x1[i] * g[i];
-        *out = acc;
+        *out = host_dot(x, g);
     });
 }
 
@@ -897,7 +808,7 @@ int scfr_launch_count(const scfr_handle* h, int64_t* out) {
 int scfr_last_step_ms(scfr_handle* h, double* total_ms) {
     return guarded([&] {
         if (!h || !total_ms) fail(SCFR_EINVAL, "NULL argument");
-        if (!h->timed) fail(SCFR_EINVAL, "no step has run yet");
+        if (!h->timed) fail(SCFR_EINVAL, "no timed step has run yet");
         set_device(h);
         CUDA_OK(cudaEventSynchronize(h->ev1));
         float ms = 0.f;

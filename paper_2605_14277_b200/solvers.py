@@ -160,6 +160,13 @@ class Solver:
         if flag.value:
             raise FloatingPointError("non-finite regrets or utilities")
 
+    @property
+    def engine(self) -> str:
+        """Engine the handle runs: levels / persistent / persistent_grid."""
+        v = C.c_int()
+        N.check(N.lib().scfr_engine(self._h, C.byref(v)))
+        return N.ENGINE_NAME[int(v.value)]
+
     def last_step_ms(self) -> float:
         v = C.c_double()
         N.check(N.lib().scfr_last_step_ms(self._h, C.byref(v)))

@@ -93,6 +93,7 @@ def test_best_response_uniform(gpu):
 
 
 def test_deterministic_and_graph_free_path_agree(gpu, monkeypatch):
+    """The level engine with and without CUDA-graph replay."""
     rec = golden_meta()["lockstep"]["liars3.pcfr+.alt.60"]
     a = Solver(bundle("liars3"), _cfg(rec), device=gpu)
     a.step(rec["iters"])
@@ -105,14 +106,19 @@ def test_deterministic_and_graph_free_path_agree(gpu, monkeypatch):
 
 def test_nonfinite_regrets_raise(gpu):
     from paper_2605_14277_b200 import games as G
+    # H always pays +1.7e308, T -1.7e308: after one iteration r_T = -1.7e308,
+    # the next update adds (-E) + q = -3.4e308 -> -inf (the reference raises
+    # FloatingPointError at the following next_strategy, pkg/solvers.py:154).
     g = G.GameBuilder("huge")
     top = g.decision(None, None, 1, "p1")
     for a in ("H", "T"):
         sub = g.decision(top, a, 2, "p2")
         for b_ in ("H", "T"):
-            g.terminal(sub, b_, 1.7e308 if a == b_ else -1.7e308)
+            g.terminal(sub, b_, 1.7e308 if a == "H" else -1.7e308)
     s = Solver(GameBundle(g.build()), SolverConfig("cfr"), device=gpu)
-    s.step(4)
+    s.step(1)
+    s.check_finite()
+    s.step(3)
     with pytest.raises(FloatingPointError):
         s.check_finite()
 
@@ -137,3 +143,48 @@ def test_goofspiel5_full_size_against_oracle(gpu):
         assert x[0] == 1.0
         sums = np.add.reduceat(x[1:], p.dp_first_seq - 1)
         np.testing.assert_allclose(sums, x[p.dp_parent_seq], rtol=0, atol=1e-11)
+
+
+ENGINES = ["levels", "persistent", "persistent_grid"]
+ENGINE_CASES = ["kuhn.cfr.sim.200", "leduc.cfr+.alt.100", "leduc.pcfr+.alt.100",
+                "random6.dcfr.sim.200", "random7.pcfr.alt.40", "liars3.dcfr.alt.60",
+                "goof3.pcfr+.sim.60", "mp.cfr+.alt.50", "liars6.dcfr.alt.30"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("key", ENGINE_CASES)
+def test_engines_bit_exact(gpu, engine, key):
+    """Every engine reproduces the reference bit for bit (same per-DP code)."""
+    rec = golden_meta()["lockstep"][key]
+    s = Solver(bundle(rec["game"]), _cfg(rec), device=gpu, engine=engine)
+    assert s.engine == engine
+    # uneven step sizes exercise the iteration counter / schedule indexing
+    done = 0
+    for chunk in (1, 2, 7):
+        if done + chunk <= rec["iters"]:
+            s.step(chunk)
+            done += chunk
+    s.step(rec["iters"] - done)
+    st = _state(s)
+    for k in ("avg1", "avg2", "r1", "r2", "x1", "x2", "u1", "u2"):
+        assert digest(st[k]) == rec["digests"][k], (key, engine, k)
+    assert s.exploitability("average")[0] == rec["expl"]
+
+
+def test_batched_persistent_sweep(gpu):
+    """Config 5 shape: 256 Leduc DCFR solves in one handle, one CTA each; the
+    8 golden parameter points are embedded in the batch and must match."""
+    recs = [r for k, r in sorted(golden_meta()["lockstep"].items())
+            if k.startswith("leduc.dcfr.alt.200.")]
+    grid = [(a, b, g) for a in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 8.0)
+            for b in (-1.0, -0.5, 0.0, 0.5) for g in (0.0, 1.0, 2.0, 3.0)][:256]
+    for k, r in enumerate(recs):
+        grid[k * 31] = (r["alpha"], r["beta"], r["gamma"])
+    s = Solver(bundle("leduc"), SolverConfig("dcfr"), device=gpu, batch_params=grid,
+               engine="auto")
+    assert s.engine == "persistent" and s.batch == 256
+    s.step(200)
+    for k, rec in enumerate(recs):
+        assert digest(s.average(1, k * 31)) == rec["digests"]["avg1"]
+        assert digest(s.regrets(2, k * 31)) == rec["digests"]["r2"]
+        assert s.exploitability("average", k * 31)[0] == rec["expl"]
