@@ -292,6 +292,124 @@ __device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __r
     W[j] = best;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-DP variants for "fat" levels (few DPs, many child DPs per action,
+// e.g. the top rounds of Goofspiel: 5 actions x 20 observed outcomes).  A
+// thread-per-DP walk of those is a serial chain of dependent loads; here lane
+// a owns action a, issues all of its child loads at once (32 in flight), sums
+// them in order, and the per-DP sums run over lanes in action order through
+// shuffles — the same association order, so still bit-exact.  All 32 lanes
+// must call these together (j is warp-uniform).
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+template <class Ld>
+__device__ __forceinline__ double lane_child_value(int2 c, const double* __restrict__ V) {
+    if (c.y == 0) return 0.0;
+    if (c.y == 1) return Ld::ld(V + c.x);
+    double acc = 0.0;
+    for (int base = 0; base < c.y; base += 32) {
+        double vv[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            if (base + k < c.y) vv[k] = Ld::ld(V + c.x + base + k);
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            if (base + k < c.y) acc = dadd(acc, vv[k]);
+    }
+    return acc;
+}
+
+// Sequential sum over lanes 0..n-1 of v: ((0.0 + v0) + v1) + ...
+__device__ __forceinline__ double lane_seq_sum(double v, int n) {
+    double acc = 0.0;
+    for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, a));
+    return acc;
+}
+
+template <class Ld>
+__device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const double* __restrict__ u,
+                                            double* __restrict__ r, double* __restrict__ b,
+                                            double* __restrict__ V, int post, double pf, double nf,
+                                            bool do_rm, int* nonfinite, int lane) {
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    if (n > 32) {  // wider than a warp: single-lane generic path
+        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite);
+        return;
+    }
+    double q = 0.0, bb = 0.0, rr = 0.0;
+    if (lane < n) {
+        const int s = s0 + lane;
+        const int2 c = __ldg(T.child + s);
+        const double uu = Ld::ld(u + s);
+        bb = Ld::ld(b + s);
+        rr = Ld::ld(r + s);
+        q = dadd(dadd(0.0, uu), lane_child_value<Ld>(c, V));
+    }
+    const double E = lane_seq_sum(dmul(bb, q), n);
+    if (lane == 0) V[j] = E;
+    const double negE = dmul(-1.0, dadd(0.0, E));
+    double rv = 0.0;
+    bool bad = false;
+    if (lane < n) {
+        bad = !isfinite(q);
+        rv = post_op(dadd(rr, dadd(negE, q)), post, pf, nf);
+        bad |= !isfinite(rv);
+        r[s0 + lane] = rv;
+    }
+    const double S = lane_seq_sum(rv > 0.0 ? rv : 0.0, n);
+    if (do_rm && lane < n) b[s0 + lane] = rm_prob(rv, S, n);
+    if (__any_sync(kFullMask, bad) && lane == 0) atomicOr(nonfinite, 1);
+}
+
+template <class Ld>
+__device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const double* __restrict__ m,
+                                             const double* __restrict__ r, double* __restrict__ b,
+                                             double* __restrict__ V, bool plus, int lane) {
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    if (n > 32) {
+        if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus);
+        return;
+    }
+    double q = 0.0, bb = 0.0, rr = 0.0;
+    if (lane < n) {
+        const int s = s0 + lane;
+        const int2 c = __ldg(T.child + s);
+        const double mm = Ld::ld(m + s);
+        bb = Ld::ld(b + s);
+        rr = Ld::ld(r + s);
+        q = dadd(dadd(0.0, mm), lane_child_value<Ld>(c, V));
+    }
+    const double E = lane_seq_sum(dmul(bb, q), n);
+    if (lane == 0) V[j] = E;
+    const double negE = dmul(-1.0, dadd(0.0, E));
+    double rv = 0.0;
+    if (lane < n) {
+        rv = dadd(rr, dadd(negE, q));
+        if (plus) rv = rv > 0.0 ? rv : 0.0;
+    }
+    const double S = lane_seq_sum(rv > 0.0 ? rv : 0.0, n);
+    if (lane < n) b[s0 + lane] = rm_prob(rv, S, n);
+}
+
+template <class Ld>
+__device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const double* __restrict__ g,
+                                           double* __restrict__ W, int lane) {
+    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    if (n > 32) {
+        if (lane == 0) br_dp<Ld>(T, j, g, W);
+        return;
+    }
+    double v = 0.0;
+    if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(__ldg(T.child + s0 + lane), W));
+    double best = -INFINITY;
+    for (int a = 0; a < n; ++a) {
+        const double x = __shfl_sync(kFullMask, v, a);
+        if (x > best) best = x;
+    }
+    if (lane == 0) W[j] = best;
+}
+
 // Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
 template <class Ld>
 __device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,

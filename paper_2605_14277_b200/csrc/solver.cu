@@ -36,25 +36,102 @@ int post_of(int v) {
 }
 
 // ---------------------------------------------------------------------------
-// Level kernels (blockIdx.y = solve within the batch).  Producers of every
-// value read here ran in earlier launches, so plain L1-cacheable loads are
-// coherent.
+// Level kernels.  One launch covers one DP level of up to two players (the
+// passes of player 1 and player 2 are independent in next() and, in
+// simultaneous mode, in observe()): blocks [0, t0.nblk) serve task t0, the
+// rest t1; blockIdx.y is the solve within a batch.  Producers of every value
+// read here ran in earlier launches, so plain L1-cacheable loads are
+// coherent.  Thread-per-DP for thin levels, warp-per-DP (lane = action) for
+// fat ones.
 
-__global__ void k_td(DevTree T, int lo, int hi, int S, const double* __restrict__ b,
-                     double* __restrict__ x, double* __restrict__ avg,
-                     const double* __restrict__ wsched, int cap, const long long* __restrict__ tdev) {
-    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= hi) return;
-    const size_t o = (size_t)blockIdx.y * S;
-    double w = 0.0;
-    double* a = nullptr;
-    if (avg) {
-        w = wsched[(size_t)blockIdx.y * cap + *tdev];
-        a = avg + o;
+struct Task {
+    DevTree T;
+    int lo, n;   // DPs [lo, lo+n)
+    int S, J;    // per-solve strides of seq- and dp-indexed state
+    int nblk;    // blocks of the launch serving this task
+    const double* u;  // utility (OBS) / prediction (PRED)
+    double* r;
+    double* b;
+    double* x;
+    double* avg;
+    double* V;
+};
+
+struct KParams {
+    const double* wsched;
+    const double* pfsched;
+    const double* nfsched;
+    int cap;
+    const long long* tdev;
+    int post, do_rm, plus;
+    int* nonfinite;
+};
+
+enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
+
+template <int KIND, int MAXA, bool WARP>
+__device__ __forceinline__ void level_body(const Task& t, int blk, const KParams& kp) {
+    constexpr int kPerBlock = WARP ? TPB / 32 : TPB;
+    const int item = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
+    if (item >= t.n) return;  // warp-uniform in warp mode
+    const int j = t.lo + item;
+    const size_t so = (size_t)blockIdx.y * t.S;
+    double* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
+    const int lane = threadIdx.x & 31;
+    if constexpr (KIND == LK_TD_AVG) {
+        const double w = kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+        double* avg = t.avg + so;
         // the reference axpy also covers the empty sequence (x[0] = 1)
-        if (j == 0) a[0] = dadd(dmul(w, x[o]), a[0]);
+        if (j == 0) avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
+        td_dp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w);
+    } else if constexpr (KIND == LK_TD) {
+        td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, 0.0);
+    } else if constexpr (KIND == LK_CUR) {
+        cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
+    } else if constexpr (KIND == LK_OBS) {
+        double pf = 1.0, nf = 1.0;
+        if (kp.post == POST_DCFR) {
+            const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+            pf = kp.pfsched[k];
+            nf = kp.nfsched[k];
+        }
+        if constexpr (WARP)
+            obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                              kp.do_rm != 0, kp.nonfinite, lane);
+        else
+            obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                               kp.do_rm != 0, kp.nonfinite);
+    } else {
+        if constexpr (WARP)
+            pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane);
+        else
+            pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0);
     }
-    td_dp<LdL1>(T, j, b + o, x + o, a, w);
+}
+
+template <int KIND, int MAXA, bool WARP>
+__global__ void __launch_bounds__(TPB) k_level(const __grid_constant__ Task t0,
+                                               const __grid_constant__ Task t1,
+                                               const __grid_constant__ KParams kp) {
+    if ((int)blockIdx.x < t0.nblk) level_body<KIND, MAXA, WARP>(t0, blockIdx.x, kp);
+    else level_body<KIND, MAXA, WARP>(t1, blockIdx.x - t0.nblk, kp);
+}
+
+using LevelKernel = void (*)(Task, Task, KParams);
+
+static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
+    const int m = maxa <= 2 ? 0 : maxa <= 4 ? 1 : 2;
+    switch (kind) {
+        case LK_TD_AVG: return k_level<LK_TD_AVG, 1, false>;
+        case LK_TD: return k_level<LK_TD, 1, false>;
+        case LK_CUR: return m == 0 ? k_level<LK_CUR, 2, false> : m == 1 ? k_level<LK_CUR, 4, false> : k_level<LK_CUR, 8, false>;
+        case LK_OBS:
+            if (warp) return k_level<LK_OBS, 1, true>;
+            return m == 0 ? k_level<LK_OBS, 2, false> : m == 1 ? k_level<LK_OBS, 4, false> : k_level<LK_OBS, 8, false>;
+        default:
+            if (warp) return k_level<LK_PRED, 1, true>;
+            return m == 0 ? k_level<LK_PRED, 2, false> : m == 1 ? k_level<LK_PRED, 4, false> : k_level<LK_PRED, 8, false>;
+    }
 }
 
 // avg[0] update for a player without decision points (no TD levels).
@@ -65,48 +142,18 @@ __global__ void k_avg0(int S, const double* __restrict__ x, double* __restrict__
     avg[o] = dadd(dmul(w, x[o]), avg[o]);
 }
 
-template <int MAXA>
-__global__ void k_cur(DevTree T, int lo, int hi, int S, const double* __restrict__ r,
-                      double* __restrict__ x) {
-    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= hi) return;
-    const size_t o = (size_t)blockIdx.y * S;
-    cur_dp<MAXA, LdL1>(T, j, r + o, x + o);
-}
-
-template <int MAXA>
-__global__ void k_obs(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ u,
-                      double* __restrict__ r, double* __restrict__ b, double* __restrict__ V,
-                      int post, const double* __restrict__ pfs, const double* __restrict__ nfs,
-                      int cap, const long long* __restrict__ tdev, int do_rm, int* nonfinite) {
-    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= hi) return;
-    const size_t o = (size_t)blockIdx.y * S;
-    double pf = 1.0, nf = 1.0;
-    if (post == POST_DCFR) {
-        const size_t k = (size_t)blockIdx.y * cap + *tdev;
-        pf = pfs[k];
-        nf = nfs[k];
-    }
-    obs_dp<MAXA, LdL1>(T, j, u + o, r + o, b + o, V + (size_t)blockIdx.y * J, post, pf, nf, do_rm != 0,
-                 nonfinite);
-}
-
-template <int MAXA>
-__global__ void k_pred(DevTree T, int lo, int hi, int S, int J, const double* __restrict__ m,
-                       const double* __restrict__ r, double* __restrict__ b,
-                       double* __restrict__ V, int plus) {
-    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= hi) return;
-    const size_t o = (size_t)blockIdx.y * S;
-    pred_dp<MAXA, LdL1>(T, j, m + o, r + o, b + o, V + (size_t)blockIdx.y * J, plus != 0);
-}
-
 __global__ void k_br(DevTree T, int lo, int hi, const double* __restrict__ g,
                      double* __restrict__ W) {
     const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= hi) return;
     br_dp<LdL1>(T, j, g, W);
+}
+
+__global__ void k_br_warp(DevTree T, int lo, int hi, const double* __restrict__ g,
+                          double* __restrict__ W) {
+    const int j = lo + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (j >= hi) return;  // warp-uniform
+    br_dp_warp<LdL1>(T, j, g, W, threadIdx.x & 31);
 }
 
 // br = g[0] + value of the root (the empty sequence's child sum).
@@ -307,6 +354,67 @@ struct Launcher {
         ++count;
     }
 
+    KParams kparams(bool do_rm) const {
+        return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
+                       post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
+                       h->nonfinite.p};
+    }
+
+    // Task for level l of player P (l outside [0, L) -> empty task).
+    static Task task(Player& P, int l, const double* u, double* x) {
+        Task t{};
+        t.T = P.tree();
+        t.S = P.S;
+        t.J = P.J;
+        t.u = u;
+        t.r = P.r.p;
+        t.b = P.b.p;
+        t.x = x;
+        t.avg = P.avg.p;
+        t.V = P.V.p;
+        if (l >= 0 && l < P.levels()) {
+            t.lo = P.lvl[l];
+            t.n = P.lvl[l + 1] - P.lvl[l];
+        }
+        return t;
+    }
+    static bool fat(const Player& P, int l) {
+        return l >= 0 && l < P.levels() && P.lvl_nc[l] >= 4.0 * P.lvl_nj[l];
+    }
+
+    // One launch over level la of A and level lb of Bp (either may be absent).
+    void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const double* ua,
+               const double* ub, double* xa, double* xb, bool do_rm) {
+        Task t0 = A ? task(*A, la, ua, xa) : Task{};
+        Task t1 = Bp ? task(*Bp, lb, ub, xb) : Task{};
+        if (t0.n == 0 && t1.n == 0) return;
+        const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
+                          ((A && fat(*A, la)) || (Bp && fat(*Bp, lb)));
+        const int per = warp ? TPB / 32 : TPB;
+        t0.nblk = (t0.n + per - 1) / per;
+        t1.nblk = (t1.n + per - 1) / per;
+        int maxa = 1;
+        double bytes = 0.0;
+        for (int k = 0; k < 2; ++k) {
+            Player* P = k == 0 ? A : Bp;
+            const int l = k == 0 ? la : lb;
+            if (!P || l < 0 || l >= P->levels()) continue;
+            maxa = std::max(maxa, P->lvl_maxa[l]);
+            switch (lk) {
+                case LK_TD_AVG: bytes += LevelBytes::td(*P, l, true); break;
+                case LK_TD: bytes += LevelBytes::td(*P, l, false); break;
+                case LK_CUR: bytes += LevelBytes::cur(*P, l); break;
+                case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm); break;
+                default: bytes += LevelBytes::pred(*P, l); break;
+            }
+        }
+        const LevelKernel kern = pick_level_kernel(lk, maxa, warp);
+        const KParams kp = kparams(do_rm);
+        launch(kk, bytes, [&] {
+            kern<<<dim3(t0.nblk + t1.nblk, h->B), TPB, 0, h->stream>>>(t0, t1, kp);
+        });
+    }
+
     void spmv(const DevCsr& M, const double* x, int sx, double* out, int so, bool neg) {
         launch(KK_SPMV, LevelBytes::spmv(M), [&] {
             dim3 grid(grid_for(M.rows), h->B);
@@ -314,78 +422,46 @@ struct Launcher {
                                                 out, so, neg ? 1 : 0, h->nonfinite.p);
         });
     }
-    void td(Player& P, const double* b, double* x, bool avg) {
-        if (avg && P.J == 0) {
-            launch(KK_TD_AVG, 16.0, [&] {
-                k_avg0<<<h->B, 1, 0, h->stream>>>(P.S, x, P.avg.p, h->wsched.p, h->cap, h->tdev.p);
-            });
-        }
-        for (int l = 0; l < P.levels(); ++l) {
-            const int lo = P.lvl[l], hi = P.lvl[l + 1];
-            launch(avg ? KK_TD_AVG : KK_TD, LevelBytes::td(P, l, avg), [&] {
-                dim3 grid(grid_for(hi - lo), h->B);
-                k_td<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, b, x,
-                                                  avg ? P.avg.p : nullptr, h->wsched.p, h->cap,
-                                                  h->tdev.p);
-            });
-        }
-    }
-    void cur(Player& P) {
-        for (int l = 0; l < P.levels(); ++l) {
-            const int lo = P.lvl[l], hi = P.lvl[l + 1];
-            launch(KK_CUR, LevelBytes::cur(P, l), [&] {
-                dim3 grid(grid_for(hi - lo), h->B);
-                auto kern = P.lvl_maxa[l] <= 2 ? k_cur<2> : P.lvl_maxa[l] <= 4 ? k_cur<4> : k_cur<8>;
-                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, P.r.p, P.xpost.p);
-            });
-        }
-    }
-    void pred(Player& P, bool plus) {
-        for (int l = P.levels() - 1; l >= 0; --l) {
-            const int lo = P.lvl[l], hi = P.lvl[l + 1];
-            launch(KK_PRED, LevelBytes::pred(P, l), [&] {
-                dim3 grid(grid_for(hi - lo), h->B);
-                auto kern = P.lvl_maxa[l] <= 2 ? k_pred<2> : P.lvl_maxa[l] <= 4 ? k_pred<4> : k_pred<8>;
-                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
-                                                  P.r.p, P.b.p, P.V.p, plus ? 1 : 0);
-            });
-        }
-    }
-    void obs(Player& P, int post, bool rm) {
-        for (int l = P.levels() - 1; l >= 0; --l) {
-            const int lo = P.lvl[l], hi = P.lvl[l + 1];
-            launch(rm ? KK_OBS_RM : KK_OBS, LevelBytes::obs(P, l, rm), [&] {
-                dim3 grid(grid_for(hi - lo), h->B);
-                auto kern = P.lvl_maxa[l] <= 2 ? k_obs<2> : P.lvl_maxa[l] <= 4 ? k_obs<4> : k_obs<8>;
-                kern<<<grid, TPB, 0, h->stream>>>(P.tree(), lo, hi, P.S, std::max(P.J, 1), P.u.p,
-                                                  P.r.p, P.b.p, P.V.p, post, h->pfsched.p,
-                                                  h->nfsched.p, h->cap, h->tdev.p, rm ? 1 : 0,
-                                                  h->nonfinite.p);
-            });
-        }
-    }
 
     void iteration() {
         Player& A = h->P[0];
         Player& Bp = h->P[1];
         const bool pr = predictive(h->variant);
-        const int post = post_of(h->variant);
-        const bool plus = h->variant == SCFR_PCFR_PLUS;
-        for (Player* P : {&A, &Bp}) {  // next_strategy for both players
-            if (pr) pred(*P, plus);
-            td(*P, P->b.p, P->x.p, true);
-        }
+        const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
+        // next_strategy of both players (independent): PRED deep -> shallow,
+        // then TD + average shallow -> deep, the two players sharing launches.
+        if (pr)
+            for (int k = 0; k < L; ++k)
+                level(LK_PRED, KK_PRED, &A, LA - 1 - k, &Bp, LB - 1 - k, A.u.p, Bp.u.p, A.x.p,
+                      Bp.x.p, false);
+        for (Player* P : {&A, &Bp})
+            if (P->J == 0)
+                launch(KK_TD_AVG, 16.0, [&] {
+                    k_avg0<<<h->B, 1, 0, h->stream>>>(P->S, P->x.p, P->avg.p, h->wsched.p, h->cap,
+                                                      h->tdev.p);
+                });
+        for (int k = 0; k < L; ++k)
+            level(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, A.x.p, Bp.x.p, false);
         spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
             spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1
-            obs(A, post, !pr);
+            for (int k = 0; k < L; ++k)
+                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, A.u.p,
+                      Bp.u.p, A.x.p, Bp.x.p, !pr);
         } else {
-            obs(A, post, !pr);
-            if (pr) cur(A);
-            else td(A, A.b.p, A.xpost.p, false);
+            for (int k = 0; k < LA; ++k)
+                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, A.u.p, nullptr,
+                      A.x.p, nullptr, !pr);
+            // current_strategy of player 1 into xpost: RM on the fly
+            // (predictive) or TD of the b that OBS already regret-matched
+            for (int k = 0; k < LA; ++k)
+                level(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, k, nullptr, -1, nullptr,
+                      nullptr, A.xpost.p, nullptr, false);
             spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1'
+            for (int k = 0; k < LB; ++k)
+                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr,
+                      Bp.u.p, nullptr, Bp.x.p, !pr);
         }
-        obs(Bp, post, !pr);
         launch(KK_TICK, 0.0, [&] { k_tick<<<1, 1, 0, h->stream>>>(h->tdev.p); });
     }
 };
@@ -453,7 +529,10 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
                                                             nullptr);
     for (int l = P.levels() - 1; l >= 0; --l) {
         const int lo = P.lvl[l], hi = P.lvl[l + 1];
-        k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
+        if (P.lvl_nc[l] >= 4.0 * P.lvl_nj[l])
+            k_br_warp<<<(hi - lo + TPB / 32 - 1) / (TPB / 32), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
+        else
+            k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
     }
     k_br_root<<<1, 1, 0, h->stream>>>(P.tree(), P.g.p, P.W.p, h->brout.p + (player - 1));
     CUDA_OK(cudaGetLastError());
