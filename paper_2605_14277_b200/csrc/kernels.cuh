@@ -17,11 +17,12 @@
 //   DP levels: DPs grouped by process-tree depth; BFS numbering makes each
 //     level a contiguous j range (pkg/decision_process.py:9-13).
 //
-// Loads: structure goes through the read-only path (__ldg).  Mutable state
-// uses the policy `Ld`: plain (L1-cacheable) loads where every producer ran
-// in an earlier launch or in the same CTA (level engine, CTA-persistent
-// engine), L2-only loads (ld.global.cg) in the grid-persistent engine whose
-// producers are other SMs within the same launch.
+// Loads go through the policy `Ld`: structure via the read-only path
+// (__ldg) and mutable state with plain (L1-cacheable) loads where every
+// producer ran in an earlier launch or in the same CTA (LdL1: level engine,
+// CTA-persistent engine); L2-only loads (ld.global.cg) in the grid-persistent
+// engine whose producers are other SMs in the same launch (LdL2); plain loads
+// of everything when state and structure live in shared memory (LdS).
 #pragma once
 
 #include <cstdint>
@@ -40,9 +41,19 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 
 struct LdL1 {
     static __device__ __forceinline__ double ld(const double* p) { return *p; }
+    template <class X>
+    static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
 struct LdL2 {
     static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+    template <class X>
+    static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
+};
+// Shared-memory resident state and structure (CTA-resident small-game engine).
+struct LdS {
+    static __device__ __forceinline__ double ld(const double* p) { return *p; }
+    template <class X>
+    static __device__ __forceinline__ X st(const X* p) { return *p; }
 };
 
 enum : int { POST_NONE = 0, POST_PLUS = 1, POST_DCFR = 2 };
@@ -84,7 +95,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const double* __restric
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
         if (a < n) {
-            c[a] = __ldg(T.child + s0 + a);
+            c[a] = Ld::st(T.child + s0 + a);
             uu[a] = Ld::ld(u + s0 + a);
         }
 #pragma unroll
@@ -98,7 +109,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const double* __restric
 template <class Ld>
 __device__ __forceinline__ double qval(const DevTree& T, const double* __restrict__ u,
                                        const double* __restrict__ V, int s) {
-    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(__ldg(T.child + s), V));
+    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(Ld::st(T.child + s), V));
 }
 
 __device__ __forceinline__ double post_op(double rv, int post, double pf, double nf) {
@@ -125,7 +136,7 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
                                        double* __restrict__ r, double* __restrict__ b,
                                        double* __restrict__ V, int post, double pf, double nf,
                                        bool do_rm, int* nonfinite) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     bool bad = false;
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
@@ -186,7 +197,7 @@ template <int MAXA, class Ld>
 __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* __restrict__ m,
                                         const double* __restrict__ r, double* __restrict__ b,
                                         double* __restrict__ V, bool plus) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, m, V, s0, n, q);
@@ -239,8 +250,8 @@ template <class Ld>
 __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __restrict__ b,
                                       double* __restrict__ x, double* __restrict__ avg,
                                       double w) {
-    const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
-    const double xp = Ld::ld(x + __ldg(T.dp_parent + j));
+    const int s0 = Ld::st(T.seq_ptr + j), s1 = Ld::st(T.seq_ptr + j + 1);
+    const double xp = Ld::ld(x + Ld::st(T.dp_parent + j));
     for (int s = s0; s < s1; ++s) {
         const double xa = dmul(Ld::ld(b + s), xp);
         x[s] = xa;
@@ -254,8 +265,8 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __r
 template <int MAXA, class Ld>
 __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __restrict__ r,
                                        double* __restrict__ x) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
-    const double xp = Ld::ld(x + __ldg(T.dp_parent + j));
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    const double xp = Ld::ld(x + Ld::st(T.dp_parent + j));
     if (n <= MAXA) {
         double rr[MAXA];
 #pragma unroll
@@ -283,10 +294,10 @@ __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __
 template <class Ld>
 __device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __restrict__ g,
                                       double* __restrict__ W) {
-    const int s0 = __ldg(T.seq_ptr + j), s1 = __ldg(T.seq_ptr + j + 1);
+    const int s0 = Ld::st(T.seq_ptr + j), s1 = Ld::st(T.seq_ptr + j + 1);
     double best = -INFINITY;
     for (int s = s0; s < s1; ++s) {
-        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(__ldg(T.child + s), W));
+        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(Ld::st(T.child + s), W));
         if (v > best) best = v;
     }
     W[j] = best;
@@ -332,7 +343,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const doubl
                                             double* __restrict__ r, double* __restrict__ b,
                                             double* __restrict__ V, int post, double pf, double nf,
                                             bool do_rm, int* nonfinite, int lane) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     if (n > 32) {  // wider than a warp: single-lane generic path
         if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite);
         return;
@@ -340,7 +351,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const doubl
     double q = 0.0, bb = 0.0, rr = 0.0;
     if (lane < n) {
         const int s = s0 + lane;
-        const int2 c = __ldg(T.child + s);
+        const int2 c = Ld::st(T.child + s);
         const double uu = Ld::ld(u + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
@@ -366,7 +377,7 @@ template <class Ld>
 __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const double* __restrict__ m,
                                              const double* __restrict__ r, double* __restrict__ b,
                                              double* __restrict__ V, bool plus, int lane) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     if (n > 32) {
         if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus);
         return;
@@ -374,7 +385,7 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const doub
     double q = 0.0, bb = 0.0, rr = 0.0;
     if (lane < n) {
         const int s = s0 + lane;
-        const int2 c = __ldg(T.child + s);
+        const int2 c = Ld::st(T.child + s);
         const double mm = Ld::ld(m + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
@@ -395,13 +406,13 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const doub
 template <class Ld>
 __device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const double* __restrict__ g,
                                            double* __restrict__ W, int lane) {
-    const int s0 = __ldg(T.seq_ptr + j), n = __ldg(T.seq_ptr + j + 1) - s0;
+    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     if (n > 32) {
         if (lane == 0) br_dp<Ld>(T, j, g, W);
         return;
     }
     double v = 0.0;
-    if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(__ldg(T.child + s0 + lane), W));
+    if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(Ld::st(T.child + s0 + lane), W));
     double best = -INFINITY;
     for (int a = 0; a < n; ++a) {
         const double x = __shfl_sync(kFullMask, v, a);

@@ -177,12 +177,154 @@ __global__ void __launch_bounds__(THREADS) k_persistent(const __grid_constant__ 
     if (rank == 0 && (GRID || blockIdx.x == 0)) *a.tdev = a.t0 + a.n_iter;
 }
 
+// ---------------------------------------------------------------------------
+// SMEM-resident CTA engine: when one solve's state and structure fit in
+// shared memory (Kuhn, Leduc, ...), each CTA stages them in once per launch,
+// runs every phase of every iteration against shared memory (LdS: ~30-cycle
+// loads instead of L1/L2 round trips on the per-phase critical path), and
+// writes the state back at the end.  U and Uᵀ stay in global memory behind
+// the read-only path.
+
+struct SPtrs {
+    double *r, *b, *x, *xpost, *avg, *u, *V;
+    DevTree T;
+};
+
+__device__ __forceinline__ SPtrs carve(unsigned char* sm, const SmemSide& o, bool has_xpost) {
+    SPtrs p;
+    p.r = reinterpret_cast<double*>(sm + o.r);
+    p.b = reinterpret_cast<double*>(sm + o.b);
+    p.x = reinterpret_cast<double*>(sm + o.x);
+    p.xpost = has_xpost ? reinterpret_cast<double*>(sm + o.xpost) : nullptr;
+    p.avg = reinterpret_cast<double*>(sm + o.avg);
+    p.u = reinterpret_cast<double*>(sm + o.u);
+    p.V = reinterpret_cast<double*>(sm + o.V);
+    p.T.seq_ptr = reinterpret_cast<const int*>(sm + o.seq_ptr);
+    p.T.dp_parent = reinterpret_cast<const int*>(sm + o.dp_parent);
+    p.T.child = reinterpret_cast<const int2*>(sm + o.child);
+    return p;
+}
+
+// Copies one player's state (and, when `structure`, its index arrays)
+// between global memory (solve slice) and shared memory.
+template <int K>
+__device__ __forceinline__ void stage(const PArgs& a, const SPtrs& s, int solve, bool in) {
+    const size_t o = (size_t)solve * a.S[K];
+    const int S = a.S[K];
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        if (in) {
+            s.r[i] = a.r[K][o + i];
+            s.b[i] = a.b[K][o + i];
+            s.x[i] = a.x[K][o + i];
+            if (s.xpost) s.xpost[i] = a.xpost[K][o + i];
+            s.avg[i] = a.avg[K][o + i];
+            s.u[i] = a.u[K][o + i];
+            const_cast<int2*>(s.T.child)[i] = __ldg(a.T[K].child + i);
+        } else {
+            a.r[K][o + i] = s.r[i];
+            a.b[K][o + i] = s.b[i];
+            a.x[K][o + i] = s.x[i];
+            if (s.xpost) a.xpost[K][o + i] = s.xpost[i];
+            a.avg[K][o + i] = s.avg[i];
+            a.u[K][o + i] = s.u[i];
+        }
+    }
+    if (in) {
+        const int J = a.J[K];
+        for (int i = threadIdx.x; i <= J; i += blockDim.x) {
+            const_cast<int*>(s.T.seq_ptr)[i] = __ldg(a.T[K].seq_ptr + i);
+            if (i < J) const_cast<int*>(s.T.dp_parent)[i] = __ldg(a.T[K].dp_parent + i);
+        }
+    }
+}
+
+template <int MAXA, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs a,
+                                                   const __grid_constant__ SmemPlan sp) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int solve = blockIdx.x;
+    const SPtrs P0 = carve(sm, sp.p[0], true), P1 = carve(sm, sp.p[1], false);
+    stage<0>(a, P0, solve, true);
+    stage<1>(a, P1, solve, true);
+    __syncthreads();
+    const int rank = threadIdx.x, size = blockDim.x;
+    for (int it = 0; it < a.n_iter; ++it) {
+        const size_t si = (size_t)solve * a.cap + (size_t)(a.t0 + it);
+        const double w = a.wsched[si];
+        const double pf = a.post == POST_DCFR ? a.pfsched[si] : 1.0;
+        const double nf = a.post == POST_DCFR ? a.nfsched[si] : 1.0;
+        for (int p = 0; p < a.nphase; ++p) {
+            const Phase ph = a.prog[p];
+            if (ph.kind < PH_SPMV_U) {
+                if (ph.n1 > 0)
+                    phase_dps<MAXA, LdS>(ph.kind, P0.T, ph.lo1, ph.n1, rank, size, P0.u, P0.r, P0.b,
+                                         P0.x, P0.xpost, P0.avg, P0.V, w, a.post, pf, nf, a.pred,
+                                         a.plus, a.nonfinite);
+                if (ph.n2 > 0) {
+                    const int b2 = ((rank - ph.n1) % size + size) % size;
+                    phase_dps<MAXA, LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, size, P1.u, P1.r, P1.b,
+                                         P1.x, P1.xpost, P1.avg, P1.V, w, a.post, pf, nf, a.pred,
+                                         a.plus, a.nonfinite);
+                }
+            } else {
+                const double* x1 = a.alt ? P0.xpost : P0.x;
+                if (ph.kind != PH_SPMV_UT)
+                    phase_spmv<LdS>(a.Uip, a.Uix, a.Ud, a.Urows, rank, size, P1.x, P0.u, false,
+                                    a.nonfinite);
+                if (ph.kind != PH_SPMV_U) {
+                    const int b2 = ph.kind == PH_SPMV_BOTH ? ((rank - a.Urows) % size + size) % size : rank;
+                    phase_spmv<LdS>(a.Tip, a.Tix, a.Td, a.Trows, b2, size, x1, P1.u, true,
+                                    a.nonfinite);
+                }
+            }
+            if (ph.first_avg && rank == 0) {
+                if (a.J[0] == 0) P0.avg[0] = dadd(dmul(w, P0.x[0]), P0.avg[0]);
+                if (a.J[1] == 0) P1.avg[0] = dadd(dmul(w, P1.x[0]), P1.avg[0]);
+            }
+            __syncthreads();
+        }
+    }
+    stage<0>(a, P0, solve, false);
+    stage<1>(a, P1, solve, false);
+    if (rank == 0 && blockIdx.x == 0) *a.tdev = a.t0 + a.n_iter;
+}
+
 // --- host side ---------------------------------------------------------------
 
 // CTA mode: 256 threads, 4 actions in registers; grid mode: 128 threads x
 // all SMs, 8 actions in registers (Liar's dice has up to 12-way DPs).
 static constexpr auto kCta = k_persistent<false, 4, 256>;
 static constexpr auto kGrid = k_persistent<true, 8, 128>;
+static constexpr int kSmallThreads = 512;
+static constexpr auto kSmall = k_small<4, kSmallThreads>;
+static constexpr int kSmemLimit = 220 * 1024;
+
+// Byte layout of one solve in the SMEM engine; returns the total size.
+static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const int at = (int)off;
+        off += (bytes + 15) & ~size_t(15);
+        return at;
+    };
+    for (int k = 0; k < 2; ++k) {
+        const Player& P = h->P[k];
+        const size_t S = P.S, J = std::max(P.J, 1);
+        SmemSide& o = sp.p[k];
+        o.r = take(8 * S);
+        o.b = take(8 * S);
+        o.x = take(8 * S);
+        o.xpost = k == 0 ? take(8 * S) : 0;
+        o.avg = take(8 * S);
+        o.u = take(8 * S);
+        o.V = take(8 * J);
+        o.child = take(8 * S);
+        o.seq_ptr = take(4 * (J + 1));
+        o.dp_parent = take(4 * J);
+    }
+    sp.bytes = off > (size_t)INT32_MAX ? INT32_MAX : (int)off;
+    return sp.bytes;
+}
 
 static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, const Player* B,
                         bool deep_first) {
@@ -250,6 +392,13 @@ void prepare_persistent(scfr_handle* h) {
         pl.ctas = std::min(want, h->num_sms * occ);
     } else {
         pl.ctas = h->B;
+        const char* env_small = std::getenv("SCFR_NO_SMEM");
+        pl.small = plan_smem(h, pl.smem) <= kSmemLimit && !(env_small && env_small[0] == '1');
+        if (pl.small) {
+            pl.threads = kSmallThreads;
+            CUDA_OK(cudaFuncSetAttribute(kSmall, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pl.smem.bytes));
+        }
     }
     pl.host_program = build_program(h);
     pl.program.alloc(pl.host_program.size());
@@ -309,7 +458,8 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
             CUDA_OK(cudaLaunchCooperativeKernel((const void*)kGrid, dim3(pl.ctas),
                                                 dim3(pl.threads), args, 0, h->stream));
         } else {
-            kCta<<<pl.ctas, pl.threads, 0, h->stream>>>(a);
+            if (pl.small) kSmall<<<pl.ctas, pl.threads, pl.smem.bytes, h->stream>>>(a, pl.smem);
+            else kCta<<<pl.ctas, pl.threads, 0, h->stream>>>(a);
             CUDA_OK(cudaGetLastError());
         }
         ++launches;

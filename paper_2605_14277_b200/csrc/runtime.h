@@ -102,8 +102,18 @@ struct Phase {
 enum : int { PH_TD_AVG = 0, PH_TD_POST, PH_CUR, PH_OBS, PH_PRED, PH_SPMV_U, PH_SPMV_UT,
              PH_SPMV_BOTH };
 
+struct SmemSide {  // byte offsets of one player's arrays in the SMEM engine's buffer
+    int r, b, x, xpost, avg, u, V, seq_ptr, dp_parent, child;
+};
+struct SmemPlan {
+    SmemSide p[2];
+    int bytes;
+};
+
 struct PersistentPlan {
-    bool grid = false;  // true: one solve over a cooperative grid; false: one CTA per solve
+    bool grid = false;   // true: one solve over a cooperative grid; false: one CTA per solve
+    bool small = false;  // CTA mode with state + structure resident in shared memory
+    SmemPlan smem{};
     int ctas = 0, threads = 0;
     std::vector<Phase> host_program;
     DevBuf<Phase> program;

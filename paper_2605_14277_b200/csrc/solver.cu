@@ -119,6 +119,15 @@ __global__ void __launch_bounds__(TPB) k_level(const __grid_constant__ Task t0,
 
 using LevelKernel = void (*)(Task, Task, KParams);
 
+// Warp-per-DP only pays on small, fat levels: few DPs (parallelism is
+// scarce, so per-DP latency is the critical path) with >= 8 child-DP
+// references per DP (long serial chains in a single thread).  Measured on
+// Goofspiel-5: the 5- and 500-DP top levels drop from 8-16 µs to ~5 µs;
+// warp mode on the 24K/432K-DP levels is 2-20x slower than thread mode.
+static bool warp_level(const Player& P, int l) {
+    return P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l];
+}
+
 static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
     const int m = maxa <= 2 ? 0 : maxa <= 4 ? 1 : 2;
     switch (kind) {
@@ -379,7 +388,7 @@ struct Launcher {
         return t;
     }
     static bool fat(const Player& P, int l) {
-        return l >= 0 && l < P.levels() && P.lvl_nc[l] >= 4.0 * P.lvl_nj[l];
+        return l >= 0 && l < P.levels() && warp_level(P, l);
     }
 
     // One launch over level la of A and level lb of Bp (either may be absent).
@@ -529,7 +538,7 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
                                                             nullptr);
     for (int l = P.levels() - 1; l >= 0; --l) {
         const int lo = P.lvl[l], hi = P.lvl[l + 1];
-        if (P.lvl_nc[l] >= 4.0 * P.lvl_nj[l])
+        if (warp_level(P, l))
             k_br_warp<<<(hi - lo + TPB / 32 - 1) / (TPB / 32), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
         else
             k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
