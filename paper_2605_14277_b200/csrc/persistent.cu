@@ -55,6 +55,7 @@ struct PArgs {
     int* nonfinite;
     long long* tdev;
     unsigned* barrier;
+    long long* trace;  // SCFR_PHASE_TRACE=1: per-phase clock64 deltas (CTA 0, thread 0)
 };
 
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
     stage<1>(a, P1, solve, true);
     __syncthreads();
     const int rank = threadIdx.x, size = blockDim.x;
+    long long t_last = clock64();
     for (int it = 0; it < a.n_iter; ++it) {
         const size_t si = (size_t)solve * a.cap + (size_t)(a.t0 + it);
         const double w = a.wsched[si];
@@ -282,6 +284,11 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
                 if (a.J[1] == 0) P1.avg[0] = dadd(dmul(w, P1.x[0]), P1.avg[0]);
             }
             __syncthreads();
+            if (a.trace && rank == 0 && blockIdx.x == 0) {
+                const long long now = clock64();
+                a.trace[p] += now - t_last;
+                t_last = now;
+            }
         }
     }
     stage<0>(a, P0, solve, false);
@@ -374,8 +381,9 @@ static std::vector<Phase> build_program(const scfr_handle* h) {
 int choose_engine(scfr_handle* h) {
     const int64_t S = (int64_t)h->P[0].S + h->P[1].S;
     if (h->B > 1) return S <= 262144 ? SCFR_ENGINE_PERSISTENT : SCFR_ENGINE_LEVELS;
-    if (S <= 8192) return SCFR_ENGINE_PERSISTENT;
-    return S <= 262144 ? SCFR_ENGINE_PERSISTENT_GRID : SCFR_ENGINE_LEVELS;
+    // The grid-persistent engine measured slower than PDL-chained level
+    // kernels on Liar's dice (468 vs 184 µs/iter), so medium games use levels.
+    return S <= 8192 ? SCFR_ENGINE_PERSISTENT : SCFR_ENGINE_LEVELS;
 }
 
 void prepare_persistent(scfr_handle* h) {
@@ -446,6 +454,14 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
     a.nonfinite = h->nonfinite.p;
     a.tdev = h->tdev.p;
     a.barrier = pl.barrier.p;
+    a.trace = nullptr;
+    const char* tr = std::getenv("SCFR_PHASE_TRACE");
+    DevBuf<long long> trace_buf;
+    if (tr && tr[0] == '1' && pl.small) {
+        trace_buf.alloc(pl.host_program.size());
+        trace_buf.zero(h->stream);
+        a.trace = trace_buf.p;
+    }
     int64_t launches = 0;
     // Chunk long requests so one launch stays well under the watchdog-free
     // but still bounded duration, and the schedule index fits in int.
@@ -463,6 +479,18 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
             CUDA_OK(cudaGetLastError());
         }
         ++launches;
+    }
+    if (a.trace) {  // debug: average cycles per phase per iteration, on stderr
+        std::vector<long long> cyc(pl.host_program.size());
+        CUDA_OK(cudaMemcpyAsync(cyc.data(), a.trace, cyc.size() * sizeof(long long),
+                                cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        static const char* names[] = {"td_avg", "td_post", "cur", "obs", "pred", "spmv_u", "spmv_ut", "spmv_both"};
+        for (size_t p = 0; p < cyc.size(); ++p) {
+            const Phase& ph = pl.host_program[p];
+            std::fprintf(stderr, "[phase %2zu] %-9s n1=%6d n2=%6d  %9.1f cycles/iter\n", p,
+                         names[ph.kind], ph.n1, ph.n2, (double)cyc[p] / (double)n);
+        }
     }
     return launches;
 }

@@ -120,6 +120,13 @@ struct PersistentPlan {
     DevBuf<unsigned> barrier;  // {count, generation}
 };
 
+// Programmatic Dependent Launch (sm_90+): let the next kernel in the stream
+// start launching now / wait until the previous grid's writes are visible.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 bool predictive(int v);
 int post_of(int v);
 inline int grid_for(int n) { return n <= 0 ? 1 : (n + TPB - 1) / TPB; }
@@ -149,6 +156,7 @@ struct scfr_handle {
     int64_t nodes_per_iter = 0;
     int64_t launches = 0;
     bool use_graph = true;
+    bool pdl = true;  // programmatic dependent launch between level kernels
     bool timed = false;
     scfr::PersistentPlan plan;
     ~scfr_handle() {

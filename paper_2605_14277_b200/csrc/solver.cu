@@ -17,6 +17,7 @@
 // graph serves every iteration.
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -113,6 +114,8 @@ template <int KIND, int MAXA, bool WARP>
 __global__ void __launch_bounds__(TPB) k_level(const __grid_constant__ Task t0,
                                                const __grid_constant__ Task t1,
                                                const __grid_constant__ KParams kp) {
+    pdl_launch_dependents();
+    pdl_wait();
     if ((int)blockIdx.x < t0.nblk) level_body<KIND, MAXA, WARP>(t0, blockIdx.x, kp);
     else level_body<KIND, MAXA, WARP>(t1, blockIdx.x - t0.nblk, kp);
 }
@@ -146,6 +149,8 @@ static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
 // avg[0] update for a player without decision points (no TD levels).
 __global__ void k_avg0(int S, const double* __restrict__ x, double* __restrict__ avg,
                        const double* __restrict__ wsched, int cap, const long long* __restrict__ tdev) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t o = (size_t)blockIdx.x * S;
     const double w = wsched[(size_t)blockIdx.x * cap + *tdev];
     avg[o] = dadd(dmul(w, x[o]), avg[o]);
@@ -174,6 +179,8 @@ __global__ void k_br_root(DevTree T, const double* __restrict__ g, const double*
 __global__ void k_spmv(int rows, const int* __restrict__ indptr, const int* __restrict__ indices,
                        const double* __restrict__ data, const double* __restrict__ x, int sx,
                        double* __restrict__ out, int so, int negate, int* nonfinite) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
     double acc = spmv_row<LdL1>(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
@@ -187,7 +194,11 @@ __global__ void k_normalize(const double* __restrict__ a, double w, double* __re
     if (i < n) out[i] = ddiv(a[i], w);
 }
 
-__global__ void k_tick(long long* tdev) { *tdev += 1; }
+__global__ void k_tick(long long* tdev) {
+    pdl_launch_dependents();
+    pdl_wait();
+    *tdev += 1;
+}
 
 // float(t) ** e with the reference's semantics (pkg/solvers.py:82-94, :172):
 // both go through libm pow(); an infinite power gives DCFR factor 1.
@@ -363,6 +374,32 @@ struct Launcher {
         ++count;
     }
 
+    // Kernel launch with Programmatic Dependent Launch allowed (the kernels
+    // call griddepcontrol.launch_dependents / .wait), so the next level's grid
+    // is set up while this one drains.  SCFR_NO_PDL=1 turns it off.
+    template <class... KArgs, class... Args>
+    void run_threads(void (*kern)(KArgs...), dim3 grid, int threads, Args... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = h->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args...));
+    }
+    template <class... KArgs, class... Args>
+    void run(void (*kern)(KArgs...), dim3 grid, Args... args) {
+        run_threads(kern, grid, TPB, args...);
+    }
+    template <class... KArgs, class... Args>
+    void run1(void (*kern)(KArgs...), dim3 grid, Args... args) {
+        run_threads(kern, grid, 1, args...);
+    }
+
     KParams kparams(bool do_rm) const {
         return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
                        post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
@@ -420,15 +457,15 @@ struct Launcher {
         const LevelKernel kern = pick_level_kernel(lk, maxa, warp);
         const KParams kp = kparams(do_rm);
         launch(kk, bytes, [&] {
-            kern<<<dim3(t0.nblk + t1.nblk, h->B), TPB, 0, h->stream>>>(t0, t1, kp);
+            run(kern, dim3(t0.nblk + t1.nblk, h->B), t0, t1, kp);
         });
     }
 
     void spmv(const DevCsr& M, const double* x, int sx, double* out, int so, bool neg) {
         launch(KK_SPMV, LevelBytes::spmv(M), [&] {
             dim3 grid(grid_for(M.rows), h->B);
-            k_spmv<<<grid, TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p, M.data.p, x, sx,
-                                                out, so, neg ? 1 : 0, h->nonfinite.p);
+            run(k_spmv, grid, M.rows, (const int*)M.indptr.p, (const int*)M.indices.p,
+                (const double*)M.data.p, x, sx, out, so, neg ? 1 : 0, h->nonfinite.p);
         });
     }
 
@@ -446,8 +483,8 @@ struct Launcher {
         for (Player* P : {&A, &Bp})
             if (P->J == 0)
                 launch(KK_TD_AVG, 16.0, [&] {
-                    k_avg0<<<h->B, 1, 0, h->stream>>>(P->S, P->x.p, P->avg.p, h->wsched.p, h->cap,
-                                                      h->tdev.p);
+                    run1(k_avg0, dim3(h->B), P->S, (const double*)P->x.p, P->avg.p,
+                         (const double*)h->wsched.p, h->cap, (const long long*)h->tdev.p);
                 });
         for (int k = 0; k < L; ++k)
             level(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, A.x.p, Bp.x.p, false);
@@ -471,7 +508,7 @@ struct Launcher {
                 level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr,
                       Bp.u.p, nullptr, Bp.x.p, !pr);
         }
-        launch(KK_TICK, 0.0, [&] { k_tick<<<1, 1, 0, h->stream>>>(h->tdev.p); });
+        launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p); });
     }
 };
 
@@ -607,13 +644,26 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         if (p1->num_seqs != U->rows || p2->num_seqs != U->cols || UT->rows != U->cols ||
             UT->cols != U->rows || UT->nnz != U->nnz)
             fail(SCFR_EINVAL, "dimension mismatch between the payoff matrix and the decision processes");
+        const char* trace = std::getenv("SCFR_TRACE");
+        auto t_prev = std::chrono::steady_clock::now();
+        auto stage = [&](const char* what) {  // SCFR_TRACE=1: create-time breakdown on stderr
+            if (!(trace && trace[0] == '1')) return;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[scfr_create] %-12s %8.2f ms\n", what,
+                         std::chrono::duration<double, std::milli>(now - t_prev).count());
+            t_prev = now;
+        };
         CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreate(&h->ev0));
         CUDA_OK(cudaEventCreate(&h->ev1));
+        stage("stream");
         upload_player(p1, h->P[0], h->B, h->stream);
+        stage("player1");
         upload_player(p2, h->P[1], h->B, h->stream);
+        stage("player2");
         upload_csr(U, h->U, h->stream);
         upload_csr(UT, h->UT, h->stream);
+        stage("payoff");
         h->tdev.alloc(1);
         h->tdev.zero(h->stream);
         h->nonfinite.alloc(1);
@@ -622,11 +672,14 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         h->avg_weight.assign(h->B, 0.0);
         const char* ng = std::getenv("SCFR_NO_GRAPH");
         h->use_graph = !(ng && ng[0] == '1');
+        const char* np = std::getenv("SCFR_NO_PDL");
+        h->pdl = !(np && np[0] == '1');
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
         if (eng && h->engine == SCFR_ENGINE_AUTO) h->engine = std::atoi(eng);
         if (h->engine == SCFR_ENGINE_AUTO) h->engine = choose_engine(h.get());
         if (h->engine >= SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
+        stage("engine");
         *out = h.release();
     });
 }
