@@ -83,20 +83,60 @@ __device__ __forceinline__ double child_sum(int2 c, const double* __restrict__ V
     return child_value<Ld>(c, c.y > 0 ? Ld::ld(V + c.x) : 0.0, V);
 }
 
+// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
+template <class Ld>
+__device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,
+                                           const int* __restrict__ indices,
+                                           const double* __restrict__ data,
+                                           const double* __restrict__ x, int row) {
+    const int k0 = __ldg(indptr + row), k1 = __ldg(indptr + row + 1);
+    double acc = 0.0;
+    int k = k0;
+    for (; k + 2 <= k1; k += 2) {
+        const double d0 = __ldg(data + k), d1 = __ldg(data + k + 1);
+        const double x0 = Ld::ld(x + __ldg(indices + k)), x1 = Ld::ld(x + __ldg(indices + k + 1));
+        acc = dadd(dadd(acc, dmul(d0, x0)), dmul(d1, x1));
+    }
+    if (k < k1) acc = dadd(acc, dmul(__ldg(data + k), Ld::ld(x + __ldg(indices + k))));
+    return acc;
+}
+
+// Optional fusion of the payoff SpMV into the observe pass: when `ip` is set
+// the utility of sequence s is computed here as row s of M applied to the
+// opponent's strategy x (scaled by -1 for player 2, pkg/solvers.py:359,368),
+// stored to u[s] (it is the next iteration's prediction), and used directly.
+struct FuseU {
+    const int* ip;
+    const int* ix;
+    const double* d;
+    const double* x;
+    int neg;
+};
+
+template <class Ld>
+__device__ __forceinline__ double fused_u(const FuseU& f, double* u, int s, bool& bad) {
+    double v = spmv_row<Ld>(f.ip, f.ix, f.d, f.x, s);
+    if (f.neg) v = dmul(-1.0, v);
+    bad |= !isfinite(v);
+    u[s] = v;
+    return v;
+}
+
 // q[a] = (0.0 + u[s0+a]) + C_{s0+a} for a < n <= MAXA, all loads issued
 // before the dependent adds ((w + v)[node(s)] read back through Bᵀ,
 // pkg/solvers.py:192-202).
 template <int MAXA, class Ld>
 __device__ __forceinline__ void load_q(const DevTree& T, const double* __restrict__ u,
                                        const double* __restrict__ V, int s0, int n,
-                                       double (&q)[MAXA]) {
+                                       double (&q)[MAXA], const FuseU f = FuseU{},
+                                       bool* bad = nullptr) {
     int2 c[MAXA];
     double uu[MAXA], v0[MAXA];
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
         if (a < n) {
             c[a] = Ld::st(T.child + s0 + a);
-            uu[a] = Ld::ld(u + s0 + a);
+            uu[a] = f.ip ? fused_u<Ld>(f, const_cast<double*>(u), s0 + a, *bad) : Ld::ld(u + s0 + a);
         }
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
@@ -135,12 +175,12 @@ template <int MAXA, class Ld>
 __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __restrict__ u,
                                        double* __restrict__ r, double* __restrict__ b,
                                        double* __restrict__ V, int post, double pf, double nf,
-                                       bool do_rm, int* nonfinite) {
+                                       bool do_rm, int* nonfinite, FuseU fuse = FuseU{}) {
     const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     bool bad = false;
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
-        load_q<MAXA, Ld>(T, u, V, s0, n, q);
+        load_q<MAXA, Ld>(T, u, V, s0, n, q, fuse, &bad);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) {
@@ -170,6 +210,8 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
                 if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
         }
     } else {
+        if (fuse.ip)  // wide DP: materialise u first, then the generic path re-reads it
+            for (int s = s0; s < s0 + n; ++s) fused_u<Ld>(fuse, const_cast<double*>(u), s, bad);
         double E = 0.0;
         for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, u, V, s)));
         V[j] = E;
@@ -342,17 +384,19 @@ template <class Ld>
 __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const double* __restrict__ u,
                                             double* __restrict__ r, double* __restrict__ b,
                                             double* __restrict__ V, int post, double pf, double nf,
-                                            bool do_rm, int* nonfinite, int lane) {
+                                            bool do_rm, int* nonfinite, int lane,
+                                            FuseU fuse = FuseU{}) {
     const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
     if (n > 32) {  // wider than a warp: single-lane generic path
-        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite);
+        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse);
         return;
     }
     double q = 0.0, bb = 0.0, rr = 0.0;
+    bool bad = false;
     if (lane < n) {
         const int s = s0 + lane;
         const int2 c = Ld::st(T.child + s);
-        const double uu = Ld::ld(u + s);
+        const double uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<double*>(u), s, bad) : Ld::ld(u + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
         q = dadd(dadd(0.0, uu), lane_child_value<Ld>(c, V));
@@ -361,9 +405,8 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const doubl
     if (lane == 0) V[j] = E;
     const double negE = dmul(-1.0, dadd(0.0, E));
     double rv = 0.0;
-    bool bad = false;
     if (lane < n) {
-        bad = !isfinite(q);
+        bad |= !isfinite(q);
         rv = post_op(dadd(rr, dadd(negE, q)), post, pf, nf);
         bad |= !isfinite(rv);
         r[s0 + lane] = rv;
@@ -419,24 +462,6 @@ __device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const double
         if (x > best) best = x;
     }
     if (lane == 0) W[j] = best;
-}
-
-// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
-template <class Ld>
-__device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,
-                                           const int* __restrict__ indices,
-                                           const double* __restrict__ data,
-                                           const double* __restrict__ x, int row) {
-    const int k0 = __ldg(indptr + row), k1 = __ldg(indptr + row + 1);
-    double acc = 0.0;
-    int k = k0;
-    for (; k + 2 <= k1; k += 2) {
-        const double d0 = __ldg(data + k), d1 = __ldg(data + k + 1);
-        const double x0 = Ld::ld(x + __ldg(indices + k)), x1 = Ld::ld(x + __ldg(indices + k + 1));
-        acc = dadd(dadd(acc, dmul(d0, x0)), dmul(d1, x1));
-    }
-    if (k < k1) acc = dadd(acc, dmul(__ldg(data + k), Ld::ld(x + __ldg(indices + k))));
-    return acc;
 }
 
 }  // namespace scfr

@@ -77,6 +77,7 @@ struct Player {
     std::vector<int> lvl;                        // DP level starts (process depth), size L+1
     std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
     std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
+    std::vector<int> lvl_s0;                     // per level: first sequence
     DevBuf<int> seq_ptr, dp_parent;
     DevBuf<int2> child;
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
@@ -87,6 +88,7 @@ struct Player {
 
 struct DevCsr {
     int rows = 0, cols = 0, nnz = 0;
+    std::vector<int> h_indptr;  // host copy (per-level byte accounting)
     DevBuf<int> indptr, indices;
     DevBuf<double> data;
 };
@@ -156,7 +158,8 @@ struct scfr_handle {
     int64_t nodes_per_iter = 0;
     int64_t launches = 0;
     bool use_graph = true;
-    bool pdl = true;  // programmatic dependent launch between level kernels
+    bool pdl = true;   // programmatic dependent launch between level kernels
+    bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
     bool timed = false;
     scfr::PersistentPlan plan;
     ~scfr_handle() {

@@ -56,6 +56,8 @@ struct Task {
     double* x;
     double* avg;
     double* V;
+    FuseU fu;  // fu.ip set: OBS computes u from the payoff rows (fused SpMV)
+    int fu_sx; // per-solve stride of fu.x
 };
 
 struct KParams {
@@ -96,12 +98,21 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
             pf = kp.pfsched[k];
             nf = kp.nfsched[k];
         }
+        FuseU fu = t.fu;
+        if (fu.ip) {
+            fu.x += (size_t)blockIdx.y * t.fu_sx;
+            if (j == 0 && lane == 0) {  // the empty sequence's row: u[0] (next prediction)
+                bool bad = false;
+                fused_u<LdL1>(fu, const_cast<double*>(t.u) + so, 0, bad);
+                if (bad) atomicOr(kp.nonfinite, 1);
+            }
+        }
         if constexpr (WARP)
             obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                              kp.do_rm != 0, kp.nonfinite, lane);
+                              kp.do_rm != 0, kp.nonfinite, lane, fu);
         else
             obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                               kp.do_rm != 0, kp.nonfinite);
+                               kp.do_rm != 0, kp.nonfinite, fu);
     } else {
         if constexpr (WARP)
             pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane);
@@ -264,6 +275,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
         int ma = 0;
         for (int j = j0; j < j1; ++j) ma = std::max(ma, seq_ptr[j + 1] - seq_ptr[j]);
         P.lvl_maxa.push_back(ma);
+        P.lvl_s0.push_back(s0);
         P.lvl_ns.push_back(s1 - s0);
         P.lvl_nj.push_back(j1 - j0);
         P.lvl_nc.push_back(nc);
@@ -313,6 +325,7 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s) {
         if (m->indices[k] < 0 || m->indices[k] >= m->cols) fail(SCFR_EINVAL, "column index out of range");
         ix[k] = (int)m->indices[k];
     }
+    D.h_indptr = ip;
     D.indptr.alloc(m->rows + 1);
     D.indices.alloc(std::max<int64_t>(m->nnz, 1));
     D.data.alloc(std::max<int64_t>(m->nnz, 1));
@@ -424,6 +437,10 @@ struct Launcher {
         }
         return t;
     }
+    // SpMV fused into OBS unless a player has no decision points (then no
+    // OBS level would produce its u) or SCFR_NO_FUSE=1.
+    bool fuse_spmv() const { return h->fuse && h->P[0].J > 0 && h->P[1].J > 0; }
+
     static bool fat(const Player& P, int l) {
         return l >= 0 && l < P.levels() && warp_level(P, l);
     }
@@ -434,6 +451,16 @@ struct Launcher {
         Task t0 = A ? task(*A, la, ua, xa) : Task{};
         Task t1 = Bp ? task(*Bp, lb, ub, xb) : Task{};
         if (t0.n == 0 && t1.n == 0) return;
+        const bool fused = lk == LK_OBS && fuse_spmv();
+        if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
+            Player& P1 = h->P[0];
+            Player& P2 = h->P[1];
+            t0.fu = FuseU{h->U.indptr.p, h->U.indices.p, h->U.data.p, P2.x.p, 0};
+            t0.fu_sx = P2.S;
+            t1.fu = FuseU{h->UT.indptr.p, h->UT.indices.p, h->UT.data.p,
+                          h->mode == SCFR_MODE_ALT ? P1.xpost.p : P1.x.p, 1};
+            t1.fu_sx = P1.S;
+        }
         const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
                           ((A && fat(*A, la)) || (Bp && fat(*Bp, lb)));
         const int per = warp ? TPB / 32 : TPB;
@@ -452,6 +479,12 @@ struct Launcher {
                 case LK_CUR: bytes += LevelBytes::cur(*P, l); break;
                 case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm); break;
                 default: bytes += LevelBytes::pred(*P, l); break;
+            }
+            if (fused) {  // this level's payoff rows; u is written instead of read
+                const DevCsr& M = k == 0 ? h->U : h->UT;
+                const int s0 = P->lvl_s0[l], s1 = s0 + (int)P->lvl_ns[l];
+                const double nnz = M.h_indptr[s1] - M.h_indptr[s0];
+                bytes += 4.0 * (s1 - s0 + 1) + 12.0 * nnz + 8.0 * nnz;
             }
         }
         const LevelKernel kern = pick_level_kernel(lk, maxa, warp);
@@ -488,9 +521,10 @@ struct Launcher {
                 });
         for (int k = 0; k < L; ++k)
             level(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, A.x.p, Bp.x.p, false);
-        spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);  // u1 = U x2
+        const bool fused = fuse_spmv();
+        if (!fused) spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
-            spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1
+            if (!fused) spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1
             for (int k = 0; k < L; ++k)
                 level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, A.u.p,
                       Bp.u.p, A.x.p, Bp.x.p, !pr);
@@ -503,7 +537,7 @@ struct Launcher {
             for (int k = 0; k < LA; ++k)
                 level(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, k, nullptr, -1, nullptr,
                       nullptr, A.xpost.p, nullptr, false);
-            spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1'
+            if (!fused) spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
                 level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr,
                       Bp.u.p, nullptr, Bp.x.p, !pr);
@@ -674,6 +708,8 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         h->use_graph = !(ng && ng[0] == '1');
         const char* np = std::getenv("SCFR_NO_PDL");
         h->pdl = !(np && np[0] == '1');
+        const char* nfz = std::getenv("SCFR_NO_FUSE");
+        h->fuse = !(nfz && nfz[0] == '1');
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
         if (eng && h->engine == SCFR_ENGINE_AUTO) h->engine = std::atoi(eng);
         if (h->engine == SCFR_ENGINE_AUTO) h->engine = choose_engine(h.get());
