@@ -39,18 +39,23 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// kChunk: child loads a lane keeps in flight in the warp-per-DP variants
+// (deep for HBM/L2 latency, shallow for shared memory).
 struct LdL1 {
+    static constexpr int kChunk = 32;
     static __device__ __forceinline__ double ld(const double* p) { return *p; }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
 struct LdL2 {
+    static constexpr int kChunk = 32;
     static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
 // Shared-memory resident state and structure (CTA-resident small-game engine).
 struct LdS {
+    static constexpr int kChunk = 8;
     static __device__ __forceinline__ double ld(const double* p) { return *p; }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return *p; }
@@ -360,14 +365,15 @@ template <class Ld>
 __device__ __forceinline__ double lane_child_value(int2 c, const double* __restrict__ V) {
     if (c.y == 0) return 0.0;
     if (c.y == 1) return Ld::ld(V + c.x);
+    constexpr int CH = Ld::kChunk;
     double acc = 0.0;
-    for (int base = 0; base < c.y; base += 32) {
-        double vv[32];
+    for (int base = 0; base < c.y; base += CH) {
+        double vv[CH];
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
+        for (int k = 0; k < CH; ++k)
             if (base + k < c.y) vv[k] = Ld::ld(V + c.x + base + k);
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
+        for (int k = 0; k < CH; ++k)
             if (base + k < c.y) acc = dadd(acc, vv[k]);
     }
     return acc;

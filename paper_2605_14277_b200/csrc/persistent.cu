@@ -239,16 +239,34 @@ __device__ __forceinline__ void stage(const PArgs& a, const SPtrs& s, int solve,
     }
 }
 
+// Warp-per-DP share of a fat OBS/PRED phase for one player (lane = action):
+// warps begin, begin+stride, ... take DPs lo+i.  Out of line like phase_dps.
+template <class Ld>
+__device__ __noinline__ void phase_dps_warp(int kind, DevTree T, int lo, int n, int begin,
+                                            int stride, const double* u, double* r, double* b,
+                                            double* V, int post, double pf, double nf, int pred,
+                                            int plus, int* nonfinite, int lane) {
+    for (int i = begin; i < n; i += stride) {
+        if (kind == PH_OBS)
+            obs_dp_warp<Ld>(T, lo + i, u, r, b, V, post, pf, nf, pred == 0, nonfinite, lane);
+        else
+            pred_dp_warp<Ld>(T, lo + i, u, r, b, V, plus != 0, lane);
+    }
+}
+
 template <int MAXA, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs a,
                                                    const __grid_constant__ SmemPlan sp) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int solve = blockIdx.x;
     const SPtrs P0 = carve(sm, sp.p[0], true), P1 = carve(sm, sp.p[1], false);
+    Phase* prog = reinterpret_cast<Phase*>(sm + sp.prog);
+    for (int i = threadIdx.x; i < a.nphase; i += blockDim.x) prog[i] = a.prog[i];
     stage<0>(a, P0, solve, true);
     stage<1>(a, P1, solve, true);
     __syncthreads();
     const int rank = threadIdx.x, size = blockDim.x;
+    const int warp = rank >> 5, lane = rank & 31, nwarps = size >> 5;
     long long t_last = clock64();
     for (int it = 0; it < a.n_iter; ++it) {
         const size_t si = (size_t)solve * a.cap + (size_t)(a.t0 + it);
@@ -256,17 +274,30 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
         const double pf = a.post == POST_DCFR ? a.pfsched[si] : 1.0;
         const double nf = a.post == POST_DCFR ? a.nfsched[si] : 1.0;
         for (int p = 0; p < a.nphase; ++p) {
-            const Phase ph = a.prog[p];
+            const Phase ph = prog[p];  // staged in shared memory
             if (ph.kind < PH_SPMV_U) {
-                if (ph.n1 > 0)
-                    phase_dps<MAXA, LdS>(ph.kind, P0.T, ph.lo1, ph.n1, rank, size, P0.u, P0.r, P0.b,
-                                         P0.x, P0.xpost, P0.avg, P0.V, w, a.post, pf, nf, a.pred,
-                                         a.plus, a.nonfinite);
-                if (ph.n2 > 0) {
-                    const int b2 = ((rank - ph.n1) % size + size) % size;
-                    phase_dps<MAXA, LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, size, P1.u, P1.r, P1.b,
-                                         P1.x, P1.xpost, P1.avg, P1.V, w, a.post, pf, nf, a.pred,
-                                         a.plus, a.nonfinite);
+                if (ph.warp1 | ph.warp2) {  // fat OBS/PRED level: one warp per DP
+                    if (ph.n1 > 0)
+                        phase_dps_warp<LdS>(ph.kind, P0.T, ph.lo1, ph.n1, warp, nwarps, P0.u, P0.r,
+                                            P0.b, P0.V, a.post, pf, nf, a.pred, a.plus,
+                                            a.nonfinite, lane);
+                    if (ph.n2 > 0) {
+                        const int b2 = ((warp - ph.n1) % nwarps + nwarps) % nwarps;
+                        phase_dps_warp<LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, nwarps, P1.u, P1.r,
+                                            P1.b, P1.V, a.post, pf, nf, a.pred, a.plus,
+                                            a.nonfinite, lane);
+                    }
+                } else {
+                    if (ph.n1 > 0)
+                        phase_dps<MAXA, LdS>(ph.kind, P0.T, ph.lo1, ph.n1, rank, size, P0.u, P0.r,
+                                             P0.b, P0.x, P0.xpost, P0.avg, P0.V, w, a.post, pf, nf,
+                                             a.pred, a.plus, a.nonfinite);
+                    if (ph.n2 > 0) {
+                        const int b2 = ((rank - ph.n1) % size + size) % size;
+                        phase_dps<MAXA, LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, size, P1.u, P1.r,
+                                             P1.b, P1.x, P1.xpost, P1.avg, P1.V, w, a.post, pf,
+                                             nf, a.pred, a.plus, a.nonfinite);
+                    }
                 }
             } else {
                 const double* x1 = a.alt ? P0.xpost : P0.x;
@@ -329,8 +360,14 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
         o.seq_ptr = take(4 * (J + 1));
         o.dp_parent = take(4 * J);
     }
+    sp.prog = take(sizeof(Phase) * h->plan.host_program.size());
     sp.bytes = off > (size_t)INT32_MAX ? INT32_MAX : (int)off;
     return sp.bytes;
+}
+
+// Same rule as the level engine: few DPs, >= 8 child-DP references per DP.
+static bool fat_level(const Player& P, int l) {
+    return P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l];
 }
 
 static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, const Player* B,
@@ -340,13 +377,16 @@ static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, con
     for (int k = 0; k < L; ++k) {
         Phase ph{kind, 0, 0, 0, 0, 0};
         const int la = deep_first ? LA - 1 - k : k, lb = deep_first ? LB - 1 - k : k;
+        const bool sums = kind == PH_OBS || kind == PH_PRED;
         if (A && la >= 0 && la < LA) {
             ph.lo1 = A->lvl[la];
             ph.n1 = A->lvl[la + 1] - A->lvl[la];
+            ph.warp1 = sums && fat_level(*A, la);
         }
         if (B && lb >= 0 && lb < LB) {
             ph.lo2 = B->lvl[lb];
             ph.n2 = B->lvl[lb + 1] - B->lvl[lb];
+            ph.warp2 = sums && fat_level(*B, lb);
         }
         prog.push_back(ph);
     }
@@ -388,6 +428,7 @@ int choose_engine(scfr_handle* h) {
 
 void prepare_persistent(scfr_handle* h) {
     PersistentPlan& pl = h->plan;
+    pl.host_program = build_program(h);
     pl.grid = h->engine == SCFR_ENGINE_PERSISTENT_GRID;
     pl.threads = pl.grid ? 128 : 256;  // must match kGrid / kCta
     if (pl.grid) {
@@ -408,7 +449,6 @@ void prepare_persistent(scfr_handle* h) {
                                          pl.smem.bytes));
         }
     }
-    pl.host_program = build_program(h);
     pl.program.alloc(pl.host_program.size());
     CUDA_OK(copy_async(pl.program.p, pl.host_program.data(), pl.host_program.size() * sizeof(Phase),
                        cudaMemcpyHostToDevice, h->stream));

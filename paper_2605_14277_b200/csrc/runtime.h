@@ -100,6 +100,7 @@ struct Phase {
     int kind;  // PH_*
     int lo1, n1, lo2, n2;
     int first_avg;  // the first TD_AVG phase also averages x[0] of DP-less players
+    int warp1, warp2;  // run this player's DPs warp-per-DP (small fat OBS/PRED levels)
 };
 enum : int { PH_TD_AVG = 0, PH_TD_POST, PH_CUR, PH_OBS, PH_PRED, PH_SPMV_U, PH_SPMV_UT,
              PH_SPMV_BOTH };
@@ -109,6 +110,7 @@ struct SmemSide {  // byte offsets of one player's arrays in the SMEM engine's b
 };
 struct SmemPlan {
     SmemSide p[2];
+    int prog;  // byte offset of the staged phase program
     int bytes;
 };
 
