@@ -239,31 +239,55 @@ __device__ __forceinline__ void stage(const PArgs& a, const SPtrs& s, int solve,
     }
 }
 
-// Warp-per-DP share of a fat OBS/PRED phase for one player (lane = action):
-// warps begin, begin+stride, ... take DPs lo+i.  Out of line like phase_dps.
-template <class Ld>
-__device__ __noinline__ void phase_dps_warp(int kind, DevTree T, int lo, int n, int begin,
-                                            int stride, const double* u, double* r, double* b,
-                                            double* V, int post, double pf, double nf, int pred,
-                                            int plus, int* nonfinite, int lane) {
-    for (int i = begin; i < n; i += stride) {
-        if (kind == PH_OBS)
-            obs_dp_warp<Ld>(T, lo + i, u, r, b, V, post, pf, nf, pred == 0, nonfinite, lane);
-        else
-            pred_dp_warp<Ld>(T, lo + i, u, r, b, V, plus != 0, lane);
+// Shared-memory pointers of player K, derived at the point of use from the
+// layout (a kernel parameter in the constant bank) so they do not stay live
+// in registers across the whole persistent loop.
+extern __shared__ __align__(16) unsigned char g_smem[];
+
+template <int K>
+__device__ __forceinline__ SPtrs sptrs(const SmemPlan& sp) {
+    return carve(g_smem, sp.p[K], K == 0);
+}
+
+// One DP (thread mode) of a phase in the SMEM engine, fully inlined.
+template <int K, int MAXA>
+__device__ __forceinline__ void small_item(int kind, const SmemPlan& sp, int j, double w,
+                                           const PArgs& a, double pf, double nf) {
+    const SPtrs P = sptrs<K>(sp);
+    switch (kind) {
+        case PH_TD_AVG:
+            if (j == 0) P.avg[0] = dadd(dmul(w, P.x[0]), P.avg[0]);
+            td_dp<LdS>(P.T, j, P.b, P.x, P.avg, w);
+            break;
+        case PH_TD_POST: td_dp<LdS>(P.T, j, P.b, P.xpost, nullptr, 0.0); break;
+        case PH_CUR: cur_dp<MAXA, LdS>(P.T, j, P.r, P.xpost); break;
+        case PH_OBS:
+            obs_dp<MAXA, LdS>(P.T, j, P.u, P.r, P.b, P.V, a.post, pf, nf, a.pred == 0, a.nonfinite);
+            break;
+        case PH_PRED: pred_dp<MAXA, LdS>(P.T, j, P.u, P.r, P.b, P.V, a.plus != 0); break;
     }
 }
 
+// One DP of a fat OBS/PRED phase, warp-wide (lane = action).
+template <int K>
+__device__ __forceinline__ void small_warp_item(int kind, const SmemPlan& sp, int j,
+                                                const PArgs& a, double pf, double nf, int lane) {
+    const SPtrs P = sptrs<K>(sp);
+    if (kind == PH_OBS)
+        obs_dp_warp<LdS>(P.T, j, P.u, P.r, P.b, P.V, a.post, pf, nf, a.pred == 0, a.nonfinite,
+                         lane);
+    else
+        pred_dp_warp<LdS>(P.T, j, P.u, P.r, P.b, P.V, a.plus != 0, lane);
+}
+
 template <int MAXA, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs a,
+__global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PArgs a,
                                                    const __grid_constant__ SmemPlan sp) {
-    extern __shared__ __align__(16) unsigned char sm[];
     const int solve = blockIdx.x;
-    const SPtrs P0 = carve(sm, sp.p[0], true), P1 = carve(sm, sp.p[1], false);
-    Phase* prog = reinterpret_cast<Phase*>(sm + sp.prog);
+    Phase* prog = reinterpret_cast<Phase*>(g_smem + sp.prog);
     for (int i = threadIdx.x; i < a.nphase; i += blockDim.x) prog[i] = a.prog[i];
-    stage<0>(a, P0, solve, true);
-    stage<1>(a, P1, solve, true);
+    stage<0>(a, sptrs<0>(sp), solve, true);
+    stage<1>(a, sptrs<1>(sp), solve, true);
     __syncthreads();
     const int rank = threadIdx.x, size = blockDim.x;
     const int warp = rank >> 5, lane = rank & 31, nwarps = size >> 5;
@@ -273,44 +297,43 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
         const double w = a.wsched[si];
         const double pf = a.post == POST_DCFR ? a.pfsched[si] : 1.0;
         const double nf = a.post == POST_DCFR ? a.nfsched[si] : 1.0;
+#pragma unroll 1
         for (int p = 0; p < a.nphase; ++p) {
-            const Phase ph = prog[p];  // staged in shared memory
+            const Phase ph = prog[p];
+            const int total = ph.n1 + ph.n2;
             if (ph.kind < PH_SPMV_U) {
-                if (ph.warp1 | ph.warp2) {  // fat OBS/PRED level: one warp per DP
-                    if (ph.n1 > 0)
-                        phase_dps_warp<LdS>(ph.kind, P0.T, ph.lo1, ph.n1, warp, nwarps, P0.u, P0.r,
-                                            P0.b, P0.V, a.post, pf, nf, a.pred, a.plus,
-                                            a.nonfinite, lane);
-                    if (ph.n2 > 0) {
-                        const int b2 = ((warp - ph.n1) % nwarps + nwarps) % nwarps;
-                        phase_dps_warp<LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, nwarps, P1.u, P1.r,
-                                            P1.b, P1.V, a.post, pf, nf, a.pred, a.plus,
-                                            a.nonfinite, lane);
+                if (ph.warp1 | ph.warp2) {  // fat OBS/PRED level: one warp per DP, lane = action
+#pragma unroll 1
+                    for (int i = warp; i < total; i += nwarps) {
+                        if (i < ph.n1) small_warp_item<0>(ph.kind, sp, ph.lo1 + i, a, pf, nf, lane);
+                        else small_warp_item<1>(ph.kind, sp, ph.lo2 + (i - ph.n1), a, pf, nf, lane);
                     }
                 } else {
-                    if (ph.n1 > 0)
-                        phase_dps<MAXA, LdS>(ph.kind, P0.T, ph.lo1, ph.n1, rank, size, P0.u, P0.r,
-                                             P0.b, P0.x, P0.xpost, P0.avg, P0.V, w, a.post, pf, nf,
-                                             a.pred, a.plus, a.nonfinite);
-                    if (ph.n2 > 0) {
-                        const int b2 = ((rank - ph.n1) % size + size) % size;
-                        phase_dps<MAXA, LdS>(ph.kind, P1.T, ph.lo2, ph.n2, b2, size, P1.u, P1.r,
-                                             P1.b, P1.x, P1.xpost, P1.avg, P1.V, w, a.post, pf,
-                                             nf, a.pred, a.plus, a.nonfinite);
+#pragma unroll 1
+                    for (int i = rank; i < total; i += size) {
+                        if (i < ph.n1) small_item<0, MAXA>(ph.kind, sp, ph.lo1 + i, w, a, pf, nf);
+                        else small_item<1, MAXA>(ph.kind, sp, ph.lo2 + (i - ph.n1), w, a, pf, nf);
                     }
                 }
             } else {
-                const double* x1 = a.alt ? P0.xpost : P0.x;
-                if (ph.kind != PH_SPMV_UT)
-                    phase_spmv<LdS>(a.Uip, a.Uix, a.Ud, a.Urows, rank, size, P1.x, P0.u, false,
-                                    a.nonfinite);
-                if (ph.kind != PH_SPMV_U) {
-                    const int b2 = ph.kind == PH_SPMV_BOTH ? ((rank - a.Urows) % size + size) % size : rank;
-                    phase_spmv<LdS>(a.Tip, a.Tix, a.Td, a.Trows, b2, size, x1, P1.u, true,
-                                    a.nonfinite);
+#pragma unroll 1
+                for (int i = rank; i < total; i += size) {
+                    const bool first = ph.kind == PH_SPMV_U || (ph.kind == PH_SPMV_BOTH && i < a.Urows);
+                    double acc;
+                    if (first) {
+                        acc = spmv_row<LdS>(a.Uip, a.Uix, a.Ud, sptrs<1>(sp).x, i);
+                        sptrs<0>(sp).u[i] = acc;
+                    } else {
+                        const SPtrs P0 = sptrs<0>(sp);
+                        const int row = ph.kind == PH_SPMV_BOTH ? i - a.Urows : i;
+                        acc = dmul(-1.0, spmv_row<LdS>(a.Tip, a.Tix, a.Td, a.alt ? P0.xpost : P0.x, row));
+                        sptrs<1>(sp).u[row] = acc;
+                    }
+                    if (!isfinite(acc)) atomicOr(a.nonfinite, 1);
                 }
             }
             if (ph.first_avg && rank == 0) {
+                const SPtrs P0 = sptrs<0>(sp), P1 = sptrs<1>(sp);
                 if (a.J[0] == 0) P0.avg[0] = dadd(dmul(w, P0.x[0]), P0.avg[0]);
                 if (a.J[1] == 0) P1.avg[0] = dadd(dmul(w, P1.x[0]), P1.avg[0]);
             }
@@ -322,8 +345,8 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
             }
         }
     }
-    stage<0>(a, P0, solve, false);
-    stage<1>(a, P1, solve, false);
+    stage<0>(a, sptrs<0>(sp), solve, false);
+    stage<1>(a, sptrs<1>(sp), solve, false);
     if (rank == 0 && blockIdx.x == 0) *a.tdev = a.t0 + a.n_iter;
 }
 
@@ -333,8 +356,8 @@ __global__ void __launch_bounds__(THREADS) k_small(const __grid_constant__ PArgs
 // all SMs, 8 actions in registers (Liar's dice has up to 12-way DPs).
 static constexpr auto kCta = k_persistent<false, 4, 256>;
 static constexpr auto kGrid = k_persistent<true, 8, 128>;
-static constexpr int kSmallThreads = 512;
-static constexpr auto kSmall = k_small<4, kSmallThreads>;
+static constexpr int kSmallThreads = 256;
+static constexpr auto kSmall = k_small<2, kSmallThreads>;
 static constexpr int kSmemLimit = 220 * 1024;
 
 // Byte layout of one solve in the SMEM engine; returns the total size.
