@@ -131,6 +131,57 @@ def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: flo
     return steps / dt, steps, dt
 
 
+def per_game_suite(device: int, cpu: bool) -> dict:
+    """BASELINE.json configs on one GPU: iterations/s and time to
+    exploitability 1e-4 (device-side best response after every iteration, or
+    every 10 for Liar's dice), the 256-solve Leduc DCFR sweep, and the CPU
+    oracle on the same small configs for context."""
+    from paper_2605_14277_b200 import Solver, SolverConfig, solve_to_target
+
+    out = {}
+    for name, kind, variant, check in (("kuhn_cfr", "kuhn", "cfr", None),
+                                        ("leduc_cfr+", "leduc", "cfr+", 1),
+                                        ("liars_dice_dcfr", "liars", "dcfr", 10)):
+        b = make_bundle(kind)
+        cfg = SolverConfig(variant)
+        s = Solver(b, cfg, device=device)
+        s.step(20)
+        s.synchronize()
+        s.step(500)
+        rate = 500 / (s.last_step_ms() / 1e3)
+        rec = {"engine": s.engine, "iterations_per_s": rate}
+        s.close()
+        if check:
+            r = solve_to_target(b, cfg, 1e-4, check_every=check, device=device)
+            rec.update({"target": 1e-4, "reached": r.reached, "iterations": r.iterations,
+                        "exploitability": r.exploitability, "seconds_wall": r.seconds,
+                        "seconds_solve_only": r.solve_seconds, "check_every": check})
+        else:
+            s = Solver(b, cfg, device=device)
+            s.step(1000)
+            rec["exploitability_at_1000"] = s.exploitability("average")[0]
+            s.close()
+        if cpu:
+            threads = 1  # small trees: the port is latency-bound, one thread is fastest
+            crate, _, _ = cpu_oracle_rate(b, variant, 200, 3, 5.0, threads)
+            rec["cpu_oracle_iterations_per_s"] = crate
+        out[name] = rec
+    # config 5: 256 DCFR(alpha, beta, gamma) Leduc solves, one handle
+    grid = [(a, bb, g) for a in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 8.0)
+            for bb in (-1.0, -0.5, 0.0, 0.5) for g in (0.0, 1.0, 2.0, 3.0)] * 2
+    b = make_bundle("leduc")
+    s = Solver(b, SolverConfig("dcfr"), device=device, batch_params=grid)
+    s.step(5)
+    s.synchronize()
+    s.step(1000)
+    ms = s.last_step_ms()
+    out["leduc_dcfr_sweep_256"] = {"engine": s.engine, "solves": len(grid), "iterations": 1000,
+                                   "seconds": ms / 1e3,
+                                   "solve_iterations_per_s": len(grid) * 1000 / (ms / 1e3)}
+    s.close()
+    return out
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -284,9 +335,11 @@ def run_ours(args):
                                 "kind": "port",
                                 "sample": f"{steps} {args.workload} iterations after 1 warm-up, "
                                           f"{dt:.1f}s (oracle/seqcfr_oracle.c)"}
+    s.close()
+    if rank == 0 and not args.no_suite:
+        line["per_game"] = per_game_suite(device, ws == 1 and not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    s.close()
     if dist:
         dist.destroy_process_group()
 
@@ -302,6 +355,7 @@ def main():
     ap.add_argument("--soak", type=float, default=1.0)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-suite", action="store_true", help="skip the per-game section")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -45,7 +45,9 @@ from .solvers import (
     RunResult,
     Solver,
     SolverConfig,
+    TargetResult,
     benchmark_iterations,
+    solve_to_target,
     discount_factors,
     run,
     work_per_iteration,
@@ -61,5 +63,6 @@ __all__ = [
     "discount_factors", "exploitability", "expected_value", "extract_decision_process",
     "flat_goofspiel", "flat_liars_dice", "goofspiel", "kuhn_poker", "leduc_poker",
     "liars_dice", "load_game", "matching_pennies", "random_game", "records_to_csv",
-    "rock_paper_scissors", "run", "save_game", "validate_game", "work_per_iteration",
+    "rock_paper_scissors", "run", "save_game", "solve_to_target", "TargetResult",
+    "validate_game", "work_per_iteration",
 ]

@@ -220,6 +220,42 @@ static double dfactor(int64_t t, double e) {
     return p / (p + 1.0);
 }
 
+// Child-DP range of every sequence from dp_parent (child DPs of one sequence
+// are contiguous in j, checked on the host): the first DP of each group
+// records {first j, count}.
+__global__ void k_derive_child(int J, const int* __restrict__ dp_parent, int2* __restrict__ child) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= J) return;
+    const int p = dp_parent[j];
+    if (j > 0 && dp_parent[j - 1] == p) return;
+    int c = 1;
+    while (j + c < J && dp_parent[j + c] == p) ++c;
+    child[p] = make_int2(j, c);
+}
+
+// Uniform behaviour 1.0/n per DP block (pkg/decision_process.py:254-261),
+// the RegretState initial b, for every solve of the batch.
+__global__ void k_derive_uniform(int J, int S, int B, const int* __restrict__ seq_ptr,
+                                 double* __restrict__ b) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= J) return;
+    const int s0 = seq_ptr[j], n = seq_ptr[j + 1] - s0;
+    const double v = ddiv(1.0, (double)n);
+    for (int k = 0; k < B; ++k)
+        for (int a = 0; a < n; ++a) b[(size_t)k * S + s0 + a] = v;
+}
+
+// x[0] = xpost[0] = 1 (the empty sequence's mass) for every solve.
+__global__ void k_init_root(int S, int B, double* __restrict__ x, double* __restrict__ xpost) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= B) return;
+    x[(size_t)k * S] = 1.0;
+    xpost[(size_t)k * S] = 1.0;
+}
+
+// Validates the reference DecisionProcess arrays, builds the int32 device
+// structure (seq_ptr, dp_parent on the host: O(J); child ranges and the
+// initial behaviour on the device: O(S)) and the per-level bookkeeping.
 static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s) {
     if (!p || p->num_seqs < 1 || p->num_decisions < 0 || p->num_nodes < 1)
         fail(SCFR_EINVAL, "bad tfsdp sizes");
@@ -230,9 +266,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.S = S;
     P.J = J;
     P.max_actions = 0;
-    std::vector<int> seq_ptr(J + 1), dp_parent(J);
-    std::vector<int2> child(S, make_int2(0, 0));
-    std::vector<double> uniform(S, 0.0);
+    std::vector<int> seq_ptr(J + 1), dp_parent(std::max(J, 1));
+    std::vector<uint64_t> seen((S + 63) / 64, 0);  // parent sequences already grouped
     int64_t next = 1;
     int64_t prev_depth = -1;
     P.lvl.clear();
@@ -242,15 +277,15 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
         if (n < 1) fail(SCFR_EINVAL, "decision point without actions");
         P.max_actions = std::max<int>(P.max_actions, (int)n);
         seq_ptr[j] = (int)next;
-        for (int64_t a = 0; a < n; ++a) uniform[next + a] = 1.0 / (double)n;
-        next += n;
         const int64_t ps = p->dp_parent_seq[j];
-        if (ps < 0 || ps >= S) fail(SCFR_EINVAL, "dp_parent_seq out of range");
+        if (ps < 0 || ps >= next) fail(SCFR_EINVAL, "dp_parent_seq out of range or after its decision point");
         dp_parent[j] = (int)ps;
-        int2& c = child[ps];
-        if (c.y == 0) c.x = j;
-        else if (c.x + c.y != j) fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
-        c.y++;
+        if (j == 0 || dp_parent[j - 1] != ps) {
+            if (seen[ps >> 6] >> (ps & 63) & 1)
+                fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
+            seen[ps >> 6] |= 1ull << (ps & 63);
+        }
+        next += n;
         const int64_t node = p->dp_node[j];
         if (node < 0 || node >= p->num_nodes) fail(SCFR_EINVAL, "dp_node out of range");
         const int64_t d = p->depth[node];
@@ -261,24 +296,26 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.lvl.push_back(J);
     if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     seq_ptr[J] = S;
-    for (int j = 0; j < J; ++j)
-        if (dp_parent[j] >= seq_ptr[j]) fail(SCFR_EINVAL, "parent sequence after its decision point");
-    P.lvl_ns.clear();
-    P.lvl_nj.clear();
-    P.lvl_nc.clear();
-    P.lvl_maxa.clear();
-    for (size_t l = 0; l + 1 < P.lvl.size(); ++l) {
+    const int L = (int)P.lvl.size() - 1;
+    P.lvl_ns.assign(L, 0);
+    P.lvl_nj.assign(L, 0);
+    P.lvl_nc.assign(L, 0);
+    P.lvl_maxa.assign(L, 0);
+    P.lvl_s0.assign(L, 0);
+    for (int l = 0; l < L; ++l) {
         const int j0 = P.lvl[l], j1 = P.lvl[l + 1];
-        const int s0 = seq_ptr[j0], s1 = seq_ptr[j1];
-        double nc = 0;
-        for (int q = s0; q < s1; ++q) nc += child[q].y;
+        P.lvl_s0[l] = seq_ptr[j0];
+        P.lvl_ns[l] = seq_ptr[j1] - seq_ptr[j0];
+        P.lvl_nj[l] = j1 - j0;
         int ma = 0;
         for (int j = j0; j < j1; ++j) ma = std::max(ma, seq_ptr[j + 1] - seq_ptr[j]);
-        P.lvl_maxa.push_back(ma);
-        P.lvl_s0.push_back(s0);
-        P.lvl_ns.push_back(s1 - s0);
-        P.lvl_nj.push_back(j1 - j0);
-        P.lvl_nc.push_back(nc);
+        P.lvl_maxa[l] = ma;
+    }
+    for (int j = 0; j < J; ++j) {  // child-DP references per level = DPs whose parent lies in it
+        const int ps = dp_parent[j];
+        if (ps == 0) continue;
+        const int l = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), ps) - P.lvl_s0.begin()) - 1;
+        if (l >= 0) P.lvl_nc[l] += 1;
     }
 
     P.seq_ptr.alloc(J + 1);
@@ -286,8 +323,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.child.alloc(S);
     CUDA_OK(copy_async(P.seq_ptr.p, seq_ptr.data(), (J + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
     if (J) CUDA_OK(copy_async(P.dp_parent.p, dp_parent.data(), J * sizeof(int), cudaMemcpyHostToDevice, s));
-    CUDA_OK(copy_async(P.child.p, child.data(), S * sizeof(int2), cudaMemcpyHostToDevice, s));
-
+    P.child.zero(s);
     const size_t SB = (size_t)S * B, JB = (size_t)std::max(J, 1) * B;
     P.r.alloc(SB);
     P.b.alloc(SB);
@@ -299,16 +335,13 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.g.alloc(S);
     P.W.alloc(std::max(J, 1));
     P.xbar.alloc(S);
-    for (auto* buf : {&P.r, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
-    // b = uniform for every solve; x[0] = xpost[0] = 1 (the empty sequence's mass)
-    for (int k = 0; k < B; ++k)
-        CUDA_OK(copy_async(P.b.p + (size_t)k * S, uniform.data(), S * sizeof(double),
-                           cudaMemcpyHostToDevice, s));
-    const double one = 1.0;
-    for (int k = 0; k < B; ++k) {
-        CUDA_OK(copy_async(P.x.p + (size_t)k * S, &one, sizeof(double), cudaMemcpyHostToDevice, s));
-        CUDA_OK(copy_async(P.xpost.p + (size_t)k * S, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    for (auto* buf : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
+    if (J) {
+        k_derive_child<<<grid_for(J), TPB, 0, s>>>(J, P.dp_parent.p, P.child.p);
+        k_derive_uniform<<<grid_for(J), TPB, 0, s>>>(J, S, B, P.seq_ptr.p, P.b.p);
     }
+    k_init_root<<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
+    CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(s));  // host staging vectors die at return
 }
 

@@ -353,6 +353,49 @@ def run(game, config: SolverConfig, iterations: int | None = None,
 
 
 @dataclass
+class TargetResult:
+    """Outcome of ``solve_to_target``: the first checked iteration whose
+    average-profile exploitability is <= target."""
+
+    reached: bool
+    iterations: int
+    exploitability: float
+    seconds: float          # wall clock, iterations + exploitability checks
+    solve_seconds: float    # device time of the iterations alone (CUDA events)
+    checks: int
+
+
+def solve_to_target(game, config: SolverConfig, target: float = 1e-4, check_every: int = 1,
+                    max_iterations: int = 1_000_000, device: int = 0,
+                    engine: str = "auto") -> TargetResult:
+    """Iterate until the average profile's exploitability is <= target,
+    checking every ``check_every`` iterations on the device (time-to-target
+    metric of BASELINE.json; the reference computes the same quantity with a
+    checkpointed ``run``, pkg/solvers.py:406-432)."""
+    if target <= 0 or check_every < 1:
+        raise ValueError("target must be > 0 and check_every >= 1")
+    bundle = _as_bundle(game)
+    s = Solver(bundle, config, device=device, engine=engine)
+    t0 = time.perf_counter()
+    solve_ms = 0.0
+    t = checks = 0
+    e = math.inf
+    while t < max_iterations:
+        n = min(check_every, max_iterations - t)
+        s.step(n)
+        solve_ms += s.last_step_ms()
+        t += n
+        e = s.exploitability("average")[0]
+        checks += 1
+        if e <= target:
+            break
+    s.check_finite()
+    out = TargetResult(e <= target, t, e, time.perf_counter() - t0, solve_ms / 1e3, checks)
+    s.close()
+    return out
+
+
+@dataclass
 class IterationBenchmark:
     proc_nodes: int
     backend_kind: str
@@ -396,5 +439,6 @@ def benchmark_iterations(bundle: GameBundle, config: SolverConfig, backend=None,
 
 
 __all__ = ["VARIANTS", "SolverConfig", "discount_factors", "Solver", "RunResult", "run",
+           "TargetResult", "solve_to_target",
            "IterationBenchmark", "benchmark_iterations", "work_per_iteration", "build_bundle",
            "GameBundle", "evaluator"]
