@@ -33,6 +33,12 @@ struct DevTree {
     const int* __restrict__ seq_ptr;    // [J+1]
     const int* __restrict__ dp_parent;  // [J]
     const int2* __restrict__ child;     // [S]
+    // Optional affine shape of the level being processed, set by the host
+    // when it holds exactly (then the index is computed, not loaded):
+    //   un > 0:  DP j has un actions, s0 = s_lo + (j - j_lo) * un
+    //   cn >= 0: sequence s has cn child DPs starting at c_lo + (s - s_lo) * cn
+    //   pc > 0:  DP j's parent sequence is p_lo + (j - j_lo) / pc
+    int j_lo = 0, s_lo = 0, un = 0, cn = -1, c_lo = 0, pc = 0, p_lo = 0;
 };
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -62,6 +68,27 @@ struct LdS {
 };
 
 enum : int { POST_NONE = 0, POST_PLUS = 1, POST_DCFR = 2 };
+
+template <class Ld>
+__device__ __forceinline__ void dp_range(const DevTree& T, int j, int& s0, int& n) {
+    if (T.un > 0) {
+        s0 = T.s_lo + (j - T.j_lo) * T.un;
+        n = T.un;
+    } else {
+        s0 = Ld::st(T.seq_ptr + j);
+        n = Ld::st(T.seq_ptr + j + 1) - s0;
+    }
+}
+template <class Ld>
+__device__ __forceinline__ int2 child_of(const DevTree& T, int s) {
+    if (T.cn >= 0) return make_int2(T.c_lo + (s - T.s_lo) * T.cn, T.cn);
+    return Ld::st(T.child + s);
+}
+template <class Ld>
+__device__ __forceinline__ int parent_of(const DevTree& T, int j) {
+    if (T.pc > 0) return T.p_lo + (j - T.j_lo) / T.pc;
+    return Ld::st(T.dp_parent + j);
+}
 
 // Value flowing up into a sequence from the DPs below it, given its child
 // range c and (already loaded) V of its first child `v0`:
@@ -140,7 +167,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const double* __restric
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
         if (a < n) {
-            c[a] = Ld::st(T.child + s0 + a);
+            c[a] = child_of<Ld>(T, s0 + a);
             uu[a] = f.ip ? fused_u<Ld>(f, const_cast<double*>(u), s0 + a, *bad) : Ld::ld(u + s0 + a);
         }
 #pragma unroll
@@ -154,7 +181,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const double* __restric
 template <class Ld>
 __device__ __forceinline__ double qval(const DevTree& T, const double* __restrict__ u,
                                        const double* __restrict__ V, int s) {
-    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(Ld::st(T.child + s), V));
+    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(child_of<Ld>(T, s), V));
 }
 
 __device__ __forceinline__ double post_op(double rv, int post, double pf, double nf) {
@@ -181,7 +208,8 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
                                        double* __restrict__ r, double* __restrict__ b,
                                        double* __restrict__ V, int post, double pf, double nf,
                                        bool do_rm, int* nonfinite, FuseU fuse = FuseU{}) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
     bool bad = false;
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
@@ -244,7 +272,8 @@ template <int MAXA, class Ld>
 __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* __restrict__ m,
                                         const double* __restrict__ r, double* __restrict__ b,
                                         double* __restrict__ V, bool plus) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, m, V, s0, n, q);
@@ -297,8 +326,10 @@ template <class Ld>
 __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __restrict__ b,
                                       double* __restrict__ x, double* __restrict__ avg,
                                       double w) {
-    const int s0 = Ld::st(T.seq_ptr + j), s1 = Ld::st(T.seq_ptr + j + 1);
-    const double xp = Ld::ld(x + Ld::st(T.dp_parent + j));
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
+    const int s1 = s0 + n;
+    const double xp = Ld::ld(x + parent_of<Ld>(T, j));
     for (int s = s0; s < s1; ++s) {
         const double xa = dmul(Ld::ld(b + s), xp);
         x[s] = xa;
@@ -312,8 +343,9 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __r
 template <int MAXA, class Ld>
 __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __restrict__ r,
                                        double* __restrict__ x) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
-    const double xp = Ld::ld(x + Ld::st(T.dp_parent + j));
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
+    const double xp = Ld::ld(x + parent_of<Ld>(T, j));
     if (n <= MAXA) {
         double rr[MAXA];
 #pragma unroll
@@ -341,10 +373,12 @@ __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __
 template <class Ld>
 __device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __restrict__ g,
                                       double* __restrict__ W) {
-    const int s0 = Ld::st(T.seq_ptr + j), s1 = Ld::st(T.seq_ptr + j + 1);
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
+    const int s1 = s0 + n;
     double best = -INFINITY;
     for (int s = s0; s < s1; ++s) {
-        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(Ld::st(T.child + s), W));
+        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(child_of<Ld>(T, s), W));
         if (v > best) best = v;
     }
     W[j] = best;
@@ -392,7 +426,8 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const doubl
                                             double* __restrict__ V, int post, double pf, double nf,
                                             bool do_rm, int* nonfinite, int lane,
                                             FuseU fuse = FuseU{}) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
     if (n > 32) {  // wider than a warp: single-lane generic path
         if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse);
         return;
@@ -401,7 +436,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const doubl
     bool bad = false;
     if (lane < n) {
         const int s = s0 + lane;
-        const int2 c = Ld::st(T.child + s);
+        const int2 c = child_of<Ld>(T, s);
         const double uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<double*>(u), s, bad) : Ld::ld(u + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
@@ -426,7 +461,8 @@ template <class Ld>
 __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const double* __restrict__ m,
                                              const double* __restrict__ r, double* __restrict__ b,
                                              double* __restrict__ V, bool plus, int lane) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
         if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus);
         return;
@@ -434,7 +470,7 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const doub
     double q = 0.0, bb = 0.0, rr = 0.0;
     if (lane < n) {
         const int s = s0 + lane;
-        const int2 c = Ld::st(T.child + s);
+        const int2 c = child_of<Ld>(T, s);
         const double mm = Ld::ld(m + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
@@ -455,13 +491,14 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const doub
 template <class Ld>
 __device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const double* __restrict__ g,
                                            double* __restrict__ W, int lane) {
-    const int s0 = Ld::st(T.seq_ptr + j), n = Ld::st(T.seq_ptr + j + 1) - s0;
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
         if (lane == 0) br_dp<Ld>(T, j, g, W);
         return;
     }
     double v = 0.0;
-    if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(Ld::st(T.child + s0 + lane), W));
+    if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(child_of<Ld>(T, s0 + lane), W));
     double best = -INFINITY;
     for (int a = 0; a < n; ++a) {
         const double x = __shfl_sync(kFullMask, v, a);

@@ -78,6 +78,7 @@ struct Player {
     std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
     std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
     std::vector<int> lvl_s0;                     // per level: first sequence
+    std::vector<DevTree> lvl_shape;              // per level: affine shape (pointers unset)
     DevBuf<int> seq_ptr, dp_parent;
     DevBuf<int2> child;
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]

@@ -317,6 +317,37 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
         const int l = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), ps) - P.lvl_s0.begin()) - 1;
         if (l >= 0) P.lvl_nc[l] += 1;
     }
+    // Affine level shapes (exact; kernels then compute indices instead of loading them).
+    {
+        std::vector<int> ccnt(S, 0), cfirst(S, -1);
+        for (int j = 0; j < J; ++j) {
+            if (cfirst[dp_parent[j]] < 0) cfirst[dp_parent[j]] = j;
+            ccnt[dp_parent[j]]++;
+        }
+        P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
+        for (int l = 0; l < L; ++l) {
+            DevTree& sh = P.lvl_shape[l];
+            const int j0 = P.lvl[l], j1 = P.lvl[l + 1], s0 = seq_ptr[j0], s1 = seq_ptr[j1];
+            sh.j_lo = j0;
+            sh.s_lo = s0;
+            const int n0 = seq_ptr[j0 + 1] - seq_ptr[j0];
+            bool uni = true;
+            for (int j = j0; j < j1 && uni; ++j) uni = seq_ptr[j + 1] - seq_ptr[j] == n0;
+            sh.un = uni ? n0 : 0;
+            const int c0 = ccnt[s0];
+            bool aff = true;
+            for (int q = s0; q < s1 && aff; ++q)
+                aff = ccnt[q] == c0 && (c0 == 0 || cfirst[q] == cfirst[s0] + (q - s0) * c0);
+            sh.cn = aff ? c0 : -1;
+            sh.c_lo = aff && c0 > 0 ? cfirst[s0] : 0;
+            int pc = 1;
+            while (j0 + pc < j1 && dp_parent[j0 + pc] == dp_parent[j0]) ++pc;
+            bool par = true;
+            for (int j = j0; j < j1 && par; ++j) par = dp_parent[j] == dp_parent[j0] + (j - j0) / pc;
+            sh.pc = par ? pc : 0;
+            sh.p_lo = dp_parent[j0];
+        }
+    }
 
     P.seq_ptr.alloc(J + 1);
     P.dp_parent.alloc(std::max(J, 1));
@@ -374,23 +405,50 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s) {
 
 // Algorithmic (compulsory) HBM bytes of one launch, fp64 values / int32
 // indices, every array touched once (DESIGN.md §4 has the derivation).
+// The player's tree with level l's affine shape attached (SCFR_NO_SHAPE=1:
+// always load indices, for A/B measurements).
+static DevTree shaped_tree(const Player& P, int l) {
+    DevTree t = P.tree();
+    static const bool off = [] {
+        const char* e = std::getenv("SCFR_NO_SHAPE");
+        return e && e[0] == '1';
+    }();
+    if (!off && l >= 0 && l < P.levels()) {
+        const DevTree& sh = P.lvl_shape[l];
+        t.j_lo = sh.j_lo;
+        t.s_lo = sh.s_lo;
+        t.un = sh.un;
+        t.cn = sh.cn;
+        t.c_lo = sh.c_lo;
+        t.pc = sh.pc;
+        t.p_lo = sh.p_lo;
+    }
+    return t;
+}
+
+// Structure bytes are counted only where the kernel loads them: an affine
+// level (lvl_shape) computes seq_ptr / child / dp_parent arithmetically.
 struct LevelBytes {
+    static double seqptr(const Player& P, int l) { return P.lvl_shape[l].un > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
+    static double child(const Player& P, int l) { return P.lvl_shape[l].cn >= 0 ? 0.0 : 8.0 * P.lvl_ns[l]; }
+    static double parent(const Player& P, int l) { return P.lvl_shape[l].pc > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
     static double obs(const Player& P, int l, bool rm) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
-        // u, b read; r RMW; child {lo,cnt}; [b write]; seq_ptr, V write; child V reads
-        return (8 + 8 + 16 + 8 + (rm ? 8 : 0)) * ns + 12 * nj + 8 * nc;
+        // u, b read; r RMW; [b write]; V write; child V reads; structure
+        return (8 + 8 + 16 + (rm ? 8 : 0)) * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
     }
     static double pred(const Player& P, int l) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
-        return (8 + 8 + 8 + 8 + 8) * ns + 12 * nj + 8 * nc;  // m, b, r read; b write; child
+        // m, b, r read; b write; V write; child V reads; structure
+        return 32 * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
     }
     static double td(const Player& P, int l, bool avg) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l];
-        // b read, x write, [avg RMW]; seq_ptr, dp_parent, parent x
-        return (16 + (avg ? 16 : 0)) * ns + 16 * nj;
+        // b read, x write, [avg RMW]; parent x; structure
+        return (16 + (avg ? 16 : 0)) * ns + 8 * nj + seqptr(P, l) + parent(P, l);
     }
-    static double cur(const Player& P, int l) {
-        return 16.0 * P.lvl_ns[l] + 16.0 * P.lvl_nj[l];  // r read, x write; structure
+    static double cur(const Player& P, int l) {  // r read, x write; parent x; structure
+        return 16.0 * P.lvl_ns[l] + 8.0 * P.lvl_nj[l] + seqptr(P, l) + parent(P, l);
     }
     static double spmv(const DevCsr& M) {
         return 4.0 * (M.rows + 1) + 12.0 * M.nnz + 8.0 * M.cols + 8.0 * M.rows;
@@ -455,7 +513,7 @@ struct Launcher {
     // Task for level l of player P (l outside [0, L) -> empty task).
     static Task task(Player& P, int l, const double* u, double* x) {
         Task t{};
-        t.T = P.tree();
+        t.T = shaped_tree(P, l);
         t.S = P.S;
         t.J = P.J;
         t.u = u;
@@ -643,9 +701,9 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
     for (int l = P.levels() - 1; l >= 0; --l) {
         const int lo = P.lvl[l], hi = P.lvl[l + 1];
         if (warp_level(P, l))
-            k_br_warp<<<(hi - lo + TPB / 32 - 1) / (TPB / 32), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
+            k_br_warp<<<(hi - lo + TPB / 32 - 1) / (TPB / 32), TPB, 0, h->stream>>>(shaped_tree(P, l), lo, hi, P.g.p, P.W.p);
         else
-            k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(P.tree(), lo, hi, P.g.p, P.W.p);
+            k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(shaped_tree(P, l), lo, hi, P.g.p, P.W.p);
     }
     k_br_root<<<1, 1, 0, h->stream>>>(P.tree(), P.g.p, P.W.p, h->brout.p + (player - 1));
     CUDA_OK(cudaGetLastError());
