@@ -164,6 +164,20 @@ typedef struct scfr_handle scfr_handle;
 int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                 const scfr_csr* UT, const scfr_config* cfg, int device,
                 scfr_handle** out);
+/* Multi-GPU row-sharded payoff SpMV (BASELINE config 4).  Every rank of a
+ * `world`-rank job holds the whole decision-process state of ONE solve and
+ * rank k computes rows [k*c, (k+1)*c) (c = ceil(rows/world)) of U x2 and of
+ * -Uᵀ x1; the slices are all-gathered in place over NCCL (loaded at run
+ * time) on the handle's stream every iteration, so iterates stay bit-identical
+ * to one GPU.  scfr_nccl_unique_id (rank 0) yields the 128-byte id that the
+ * caller distributes (e.g. torch.distributed broadcast).  Collective: every
+ * rank must call scfr_step / scfr_exploitability / scfr_expected_value
+ * together. */
+int scfr_nccl_unique_id(char* out128);
+int scfr_create_sharded(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                        const scfr_csr* UT, const scfr_config* cfg, int device,
+                        const char* nccl_unique_id, int rank, int world, scfr_handle** out);
+
 /* Runs n full iterations (_step semantics incl. t++ for both players) on the
  * handle's stream; asynchronous. */
 int scfr_step(scfr_handle* h, int64_t n_iter);

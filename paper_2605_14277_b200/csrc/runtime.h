@@ -50,22 +50,45 @@ struct KernelRecord {
     cudaEvent_t e0, e1;
 };
 
+// Device buffers come from the device's stream-ordered memory pool, kept
+// resident (release threshold raised once per device), so building a second
+// solver for the same game reuses memory instead of paying cudaMalloc/cudaFree.
+// The allocating stream is thread-local state set by the API entry points.
+inline thread_local cudaStream_t g_alloc_stream = nullptr;
+struct AllocStream {
+    cudaStream_t prev;
+    explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~AllocStream() { g_alloc_stream = prev; }
+};
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    bool pooled = false;
     void alloc(size_t count) {
         free();
         n = count;
-        if (count) CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+        if (!count) return;
+        if (g_alloc_stream) {
+            CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), g_alloc_stream));
+            pooled = true;
+        } else {
+            CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+        }
     }
     void zero(cudaStream_t s) {
         if (n) CUDA_OK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
     }
     void free() {
-        if (p) cudaFree(p);
+        // callers synchronise the owning stream before buffers die
+        if (p) {
+            if (pooled) cudaFreeAsync(p, 0);
+            else cudaFree(p);
+        }
         p = nullptr;
         n = 0;
+        pooled = false;
     }
     size_t bytes() const { return n * sizeof(T); }
     ~DevBuf() { free(); }
@@ -88,7 +111,8 @@ struct Player {
 };
 
 struct DevCsr {
-    int rows = 0, cols = 0, nnz = 0;
+    int rows = 0, cols = 0, nnz = 0;  // rows / nnz held on this device (a shard if sharded)
+    int full_rows = 0, row0 = 0, chunk = 0;  // global rows; first local row; rows per rank
     std::vector<int> h_indptr;  // host copy (per-level byte accounting)
     DevBuf<int> indptr, indices;
     DevBuf<double> data;
@@ -165,6 +189,10 @@ struct scfr_handle {
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
     bool timed = false;
     scfr::PersistentPlan plan;
+    // Row-sharded payoff SpMV (scfr_create_sharded): NCCL communicator
+    // (ncclComm_t) over `world` ranks, this handle being `rank`.
+    void* comm = nullptr;
+    int world = 1, rank = 0;
     ~scfr_handle() {
         if (exec) cudaGraphExecDestroy(exec);
         if (ev0) cudaEventDestroy(ev0);

@@ -25,6 +25,9 @@
 #include <memory>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'ed by the sharded mode
+
 #include "runtime.h"
 
 namespace scfr {
@@ -376,29 +379,85 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     CUDA_OK(cudaStreamSynchronize(s));  // host staging vectors die at return
 }
 
-static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s) {
+// Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
+// last shard may hold fewer), re-based so local row i is global row0 + i.
+static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, int world = 1, int rank = 0) {
     if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
     if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
     if (m->indptr[0] != 0 || m->indptr[m->rows] != m->nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
-    D.rows = (int)m->rows;
+    const int64_t chunk = (m->rows + world - 1) / world;
+    const int64_t r0 = std::min<int64_t>(m->rows, chunk * rank);
+    const int64_t r1 = std::min<int64_t>(m->rows, r0 + chunk);
+    D.full_rows = (int)m->rows;
+    D.row0 = (int)r0;
+    D.chunk = (int)chunk;
+    D.rows = (int)(r1 - r0);
     D.cols = (int)m->cols;
-    D.nnz = (int)m->nnz;
-    std::vector<int> ip(m->rows + 1), ix(m->nnz);
-    for (int64_t i = 0; i <= m->rows; ++i) ip[i] = (int)m->indptr[i];
-    for (int64_t k = 0; k < m->nnz; ++k) {
+    const int64_t k0 = m->indptr[r0], k1 = m->indptr[r1];
+    D.nnz = (int)(k1 - k0);
+    std::vector<int> ip(D.rows + 1), ix(D.nnz);
+    for (int64_t i = 0; i <= D.rows; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
+    for (int64_t k = k0; k < k1; ++k) {
         if (m->indices[k] < 0 || m->indices[k] >= m->cols) fail(SCFR_EINVAL, "column index out of range");
-        ix[k] = (int)m->indices[k];
+        ix[k - k0] = (int)m->indices[k];
     }
-    D.h_indptr = ip;
-    D.indptr.alloc(m->rows + 1);
-    D.indices.alloc(std::max<int64_t>(m->nnz, 1));
-    D.data.alloc(std::max<int64_t>(m->nnz, 1));
+    D.h_indptr.assign(m->indptr, m->indptr + m->rows + 1);  // global (per-level accounting)
+    D.indptr.alloc(D.rows + 1);
+    D.indices.alloc(std::max(D.nnz, 1));
+    D.data.alloc(std::max(D.nnz, 1));
     CUDA_OK(copy_async(D.indptr.p, ip.data(), ip.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-    if (m->nnz) {
+    if (D.nnz) {
         CUDA_OK(copy_async(D.indices.p, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-        CUDA_OK(copy_async(D.data.p, m->data, m->nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        CUDA_OK(copy_async(D.data.p, m->data + k0, D.nnz * sizeof(double), cudaMemcpyHostToDevice, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
+}
+
+// --- NCCL (loaded at run time; only the row-sharded mode needs it) -------
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (loaded) return api;
+    // Prefer the copy already mapped into the process (torch's), else the system one.
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) fail(SCFR_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+    auto sym = [&](const char* name) {
+        void* p = dlsym(lib, name);
+        if (!p) fail(SCFR_ENCCL, "libnccl lacks %s", name);
+        return p;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+    return api;
+}
+
+#define NCCL_OK(expr)                                                                     \
+    do {                                                                                  \
+        ncclResult_t _r = (expr);                                                         \
+        if (_r != ncclSuccess) ::scfr::fail(SCFR_ENCCL, "%s failed: %s", #expr,          \
+                                            nccl().GetErrorString(_r));                   \
+    } while (0)
+
+// In-place all-gather of the per-rank row slices of a vector laid out as
+// world x chunk (padded) on the handle's stream.
+static void allgather_rows(scfr_handle* h, double* full, int chunk) {
+    NCCL_OK(nccl().AllGather(full + (size_t)h->rank * chunk, full, (size_t)chunk, ncclDouble,
+                             (ncclComm_t)h->comm, h->stream));
 }
 
 // --- per-iteration launch sequence --------------------------------------
@@ -585,12 +644,15 @@ struct Launcher {
         });
     }
 
+    // out[row0 + i] = (±) row i of M applied to x (this rank's rows), then in
+    // the row-sharded mode the slices are all-gathered into the full vector.
     void spmv(const DevCsr& M, const double* x, int sx, double* out, int so, bool neg) {
         launch(KK_SPMV, LevelBytes::spmv(M), [&] {
             dim3 grid(grid_for(M.rows), h->B);
             run(k_spmv, grid, M.rows, (const int*)M.indptr.p, (const int*)M.indices.p,
-                (const double*)M.data.p, x, sx, out, so, neg ? 1 : 0, h->nonfinite.p);
+                (const double*)M.data.p, x, sx, out + M.row0, so, neg ? 1 : 0, h->nonfinite.p);
         });
+        if (h->comm) allgather_rows(h, out, M.chunk);
     }
 
     void iteration() {
@@ -637,8 +699,21 @@ struct Launcher {
     }
 };
 
+// Raise the device pool's release threshold once so freed solver buffers stay
+// in the pool for the next solver (cudaMallocAsync path of DevBuf).
+static void keep_pool_resident(int device) {
+    static std::vector<char> done(64, 0);
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    done[device] = 1;
+}
+
 static void ensure_schedule(scfr_handle* h, int64_t upto) {
     if (upto <= h->cap) return;
+    AllocStream alloc_on(h->stream);
     int64_t cap = std::max<int64_t>(4096, h->cap);
     while (cap < upto) cap *= 2;
     if (cap >= (1ll << 31)) fail(SCFR_EINVAL, "iteration count too large");
@@ -692,12 +767,19 @@ static void add_weights(scfr_handle* h, int64_t n) {
 }
 
 // Best response of `player` against the opponent's strategy x_opp (one solve).
+// out = (±) M x for one solve outside the iteration graph (best response,
+// expected value): this rank's rows, all-gathered when sharded.
+static void solve_spmv(scfr_handle* h, const DevCsr& M, const double* x, double* out, bool neg) {
+    k_spmv<<<dim3(grid_for(M.rows), 1), TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p,
+                                                            M.data.p, x, 0, out + M.row0, 0,
+                                                            neg ? 1 : 0, nullptr);
+    CUDA_OK(cudaGetLastError());
+    if (h->comm) allgather_rows(h, out, M.chunk);
+}
+
 static double best_response(scfr_handle* h, int player, const double* x_opp) {
     Player& P = h->P[player - 1];
-    const DevCsr& M = player == 1 ? h->U : h->UT;
-    k_spmv<<<dim3(grid_for(M.rows), 1), TPB, 0, h->stream>>>(M.rows, M.indptr.p, M.indices.p, M.data.p,
-                                                            x_opp, 0, P.g.p, 0, player == 2 ? 1 : 0,
-                                                            nullptr);
+    solve_spmv(h, player == 1 ? h->U : h->UT, x_opp, P.g.p, player == 2);
     for (int l = P.levels() - 1; l >= 0; --l) {
         const int lo = P.lvl[l], hi = P.lvl[l + 1];
         if (warp_level(P, l))
@@ -731,10 +813,18 @@ using namespace scfr;
 
 extern "C" {
 
-int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, const scfr_csr* UT,
-                const scfr_config* cfg, int device, scfr_handle** out) {
-    return guarded([&] {
+// Shared body of scfr_create / scfr_create_sharded (nccl_id == nullptr: one GPU).
+static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                        const scfr_csr* UT, const scfr_config* cfg, int device,
+                        const char* nccl_id, int rank, int world, scfr_handle** out) {
+    {
         if (!out || !cfg || !p1 || !p2 || !U || !UT) fail(SCFR_EINVAL, "NULL argument");
+        if (nccl_id) {
+            if (world < 1 || rank < 0 || rank >= world) fail(SCFR_EINVAL, "bad rank / world size");
+            if (cfg->batch != 1) fail(SCFR_EINVAL, "the row-sharded mode runs a single solve (batch 1)");
+            if (cfg->engine != SCFR_ENGINE_AUTO && cfg->engine != SCFR_ENGINE_LEVELS)
+                fail(SCFR_EINVAL, "the row-sharded mode runs on the level engine");
+        }
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
         if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
         if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
@@ -779,6 +869,8 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
             t_prev = now;
         };
         CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        keep_pool_resident(device);
+        AllocStream alloc_on(h->stream);
         CUDA_OK(cudaEventCreate(&h->ev0));
         CUDA_OK(cudaEventCreate(&h->ev1));
         stage("stream");
@@ -786,8 +878,28 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         stage("player1");
         upload_player(p2, h->P[1], h->B, h->stream);
         stage("player2");
-        upload_csr(U, h->U, h->stream);
-        upload_csr(UT, h->UT, h->stream);
+        const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
+        upload_csr(U, h->U, h->stream, w, rk);
+        upload_csr(UT, h->UT, h->stream, w, rk);
+        if (nccl_id) {
+            // u and the BR gradient are gathered as world x chunk (padded) vectors
+            for (int k = 0; k < 2; ++k) {
+                Player& P = h->P[k];
+                const size_t pad = (size_t)w * (k == 0 ? h->U.chunk : h->UT.chunk);
+                if (pad > (size_t)P.S) {
+                    P.u.alloc(pad);
+                    P.u.zero(h->stream);
+                    P.g.alloc(pad);
+                }
+            }
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof id);
+            ncclComm_t comm;
+            NCCL_OK(nccl().CommInitRank(&comm, w, id, rk));
+            h->comm = comm;
+            h->world = w;
+            h->rank = rk;
+        }
         stage("payoff");
         h->tdev.alloc(1);
         h->tdev.zero(h->stream);
@@ -800,14 +912,37 @@ int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, c
         const char* np = std::getenv("SCFR_NO_PDL");
         h->pdl = !(np && np[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
-        h->fuse = !(nfz && nfz[0] == '1');
+        h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
-        if (eng && h->engine == SCFR_ENGINE_AUTO) h->engine = std::atoi(eng);
-        if (h->engine == SCFR_ENGINE_AUTO) h->engine = choose_engine(h.get());
+        if (eng && h->engine == SCFR_ENGINE_AUTO && !h->comm) h->engine = std::atoi(eng);
+        if (h->engine == SCFR_ENGINE_AUTO) h->engine = h->comm ? SCFR_ENGINE_LEVELS : choose_engine(h.get());
         if (h->engine >= SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
         stage("engine");
         *out = h.release();
+    }
+}
+
+int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, const scfr_csr* UT,
+                const scfr_config* cfg, int device, scfr_handle** out) {
+    return guarded([&] { create_impl(p1, p2, U, UT, cfg, device, nullptr, 0, 1, out); });
+}
+
+int scfr_nccl_unique_id(char* out) {
+    return guarded([&] {
+        if (!out) fail(SCFR_EINVAL, "NULL argument");
+        ncclUniqueId id;
+        NCCL_OK(nccl().GetUniqueId(&id));
+        std::memcpy(out, &id, sizeof id);
+    });
+}
+
+int scfr_create_sharded(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                        const scfr_csr* UT, const scfr_config* cfg, int device,
+                        const char* nccl_id, int rank, int world, scfr_handle** out) {
+    return guarded([&] {
+        if (!nccl_id) fail(SCFR_EINVAL, "NULL NCCL unique id");
+        create_impl(p1, p2, U, UT, cfg, device, nccl_id, rank, world, out);
     });
 }
 
@@ -997,8 +1132,7 @@ int scfr_expected_value(scfr_handle* h, int solve, double* out) {
         set_device(h);
         const double* x2 = profile(h, 2, solve, 0);
         Player& A = h->P[0];
-        k_spmv<<<dim3(grid_for(h->U.rows), 1), TPB, 0, h->stream>>>(h->U.rows, h->U.indptr.p, h->U.indices.p,
-                                                                   h->U.data.p, x2, 0, A.g.p, 0, 0, nullptr);
+        solve_spmv(h, h->U, x2, A.g.p, false);
         profile(h, 1, solve, 0);
         std::vector<double> g(A.S), x(A.S);
         CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1031,8 +1165,7 @@ int scfr_expected_value_of(scfr_handle* h, const double* x1, const double* x2, d
         Player& A = h->P[0];
         Player& Bp = h->P[1];
         CUDA_OK(copy_async(Bp.xbar.p, x2, Bp.S * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        k_spmv<<<dim3(grid_for(h->U.rows), 1), TPB, 0, h->stream>>>(h->U.rows, h->U.indptr.p, h->U.indices.p,
-                                                                   h->U.data.p, Bp.xbar.p, 0, A.g.p, 0, 0, nullptr);
+        solve_spmv(h, h->U, Bp.xbar.p, A.g.p, false);
         std::vector<double> g(A.S), x(x1, x1 + A.S);
         CUDA_OK(copy_async(g.data(), A.g.p, A.S * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
@@ -1098,6 +1231,7 @@ int scfr_destroy(scfr_handle* h) {
         if (!h) return;
         cudaSetDevice(h->device);
         if (h->stream) cudaStreamSynchronize(h->stream);
+        if (h->comm) nccl().CommDestroy((ncclComm_t)h->comm);
         delete h;
     });
 }

@@ -31,6 +31,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class NcclError(RuntimeError):
+    pass
+
+
 i64p = C.POINTER(C.c_int64)
 f64p = C.POINTER(C.c_double)
 i8p = C.POINTER(C.c_int8)
@@ -86,6 +90,10 @@ _SIGS = {
     "scfr_flat_game_free": ([C.POINTER(FlatGameC)], None),
     "scfr_create": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.POINTER(Csr),
                      C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "scfr_nccl_unique_id": ([C.c_char_p], C.c_int),
+    "scfr_create_sharded": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.POINTER(Csr),
+                             C.POINTER(Config), C.c_int, C.c_char_p, C.c_int, C.c_int,
+                             C.POINTER(C.c_void_p)], C.c_int),
     "scfr_step": ([C.c_void_p, C.c_int64], C.c_int),
     "scfr_engine": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "scfr_synchronize": ([C.c_void_p], C.c_int),
@@ -141,6 +149,8 @@ def check(status: int) -> None:
         raise FloatingPointError(msg)
     if status == ENOMEM:
         raise MemoryError(msg)
+    if status == ENCCL:
+        raise NcclError(msg)
     raise CudaError(f"[{status}] {msg}")
 
 

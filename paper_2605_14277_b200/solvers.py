@@ -107,7 +107,9 @@ class Solver:
     """
 
     def __init__(self, bundle: GameBundle, config: SolverConfig, device: int = 0,
-                 batch_params=None, engine: str = "auto"):
+                 batch_params=None, engine: str = "auto", shard=None):
+        """``shard=(nccl_unique_id, rank, world)`` selects the row-sharded
+        multi-GPU mode (see distributed.sharded_solver)."""
         self.bundle = bundle
         self.config = config
         L = N.lib()
@@ -137,8 +139,18 @@ class Solver:
         self.device = device
         h = C.c_void_p()
         p1, p2, U, UT = bundle._c
-        N.check(L.scfr_create(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT), C.byref(cfg),
-                              int(device), C.byref(h)))
+        self.shard = None
+        if shard is not None:
+            uid, rank, world = shard
+            if len(uid) != 128:
+                raise ValueError("NCCL unique id must be 128 bytes")
+            self.shard = (int(rank), int(world))
+            N.check(L.scfr_create_sharded(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT),
+                                          C.byref(cfg), int(device), uid, int(rank), int(world),
+                                          C.byref(h)))
+        else:
+            N.check(L.scfr_create(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT),
+                                  C.byref(cfg), int(device), C.byref(h)))
         self._h = h
 
     # -- iteration -----------------------------------------------------------

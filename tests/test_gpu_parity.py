@@ -188,3 +188,20 @@ def test_batched_persistent_sweep(gpu):
         assert digest(s.average(1, k * 31)) == rec["digests"]["avg1"]
         assert digest(s.regrets(2, k * 31)) == rec["digests"]["r2"]
         assert s.exploitability("average", k * 31)[0] == rec["expl"]
+
+
+@pytest.mark.parametrize("key", ["leduc.pcfr+.alt.100", "liars3.dcfr.sim.60", "random6.cfr.alt.200",
+                                 "goof3.cfr+.alt.60"])
+def test_row_sharded_mode_world1_bit_exact(gpu, key):
+    """The NCCL row-sharded path (scfr_create_sharded) on a 1-rank
+    communicator: SpMV slices + in-place all-gather inside the iteration graph
+    must leave every iterate bit-identical to the reference."""
+    from paper_2605_14277_b200.distributed import nccl_unique_id
+    rec = golden_meta()["lockstep"][key]
+    s = Solver(bundle(rec["game"]), _cfg(rec), device=gpu, engine="levels",
+               shard=(nccl_unique_id(), 0, 1))
+    s.step(rec["iters"])
+    st = _state(s)
+    for k in ("avg1", "avg2", "r1", "r2", "u1", "u2"):
+        assert digest(st[k]) == rec["digests"][k], (key, k)
+    assert s.exploitability("average")[0] == rec["expl"]
