@@ -124,8 +124,11 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
     }
 }
 
+// Narrow variants (<= 2 actions in registers: the deep, bandwidth-bound
+// levels) are held to 40 registers so 12 CTAs fit per SM (more loads in
+// flight); wide / warp variants keep the default budget.
 template <int KIND, int MAXA, bool WARP>
-__global__ void __launch_bounds__(TPB) k_level(const __grid_constant__ Task t0,
+__global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : 1) k_level(const __grid_constant__ Task t0,
                                                const __grid_constant__ Task t1,
                                                const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
@@ -146,18 +149,21 @@ static bool warp_level(const Player& P, int l) {
 }
 
 static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
-    const int m = maxa <= 2 ? 0 : maxa <= 4 ? 1 : 2;
+    const int m = maxa <= 1 ? 0 : maxa <= 2 ? 1 : maxa <= 4 ? 2 : 3;
+#define SCFR_PICK(K) \
+    (m == 0 ? k_level<K, 1, false> : m == 1 ? k_level<K, 2, false> : m == 2 ? k_level<K, 4, false> : k_level<K, 8, false>)
     switch (kind) {
         case LK_TD_AVG: return k_level<LK_TD_AVG, 1, false>;
         case LK_TD: return k_level<LK_TD, 1, false>;
-        case LK_CUR: return m == 0 ? k_level<LK_CUR, 2, false> : m == 1 ? k_level<LK_CUR, 4, false> : k_level<LK_CUR, 8, false>;
+        case LK_CUR: return SCFR_PICK(LK_CUR);
         case LK_OBS:
             if (warp) return k_level<LK_OBS, 1, true>;
-            return m == 0 ? k_level<LK_OBS, 2, false> : m == 1 ? k_level<LK_OBS, 4, false> : k_level<LK_OBS, 8, false>;
+            return SCFR_PICK(LK_OBS);
         default:
             if (warp) return k_level<LK_PRED, 1, true>;
-            return m == 0 ? k_level<LK_PRED, 2, false> : m == 1 ? k_level<LK_PRED, 4, false> : k_level<LK_PRED, 8, false>;
+            return SCFR_PICK(LK_PRED);
     }
+#undef SCFR_PICK
 }
 
 // avg[0] update for a player without decision points (no TD levels).
