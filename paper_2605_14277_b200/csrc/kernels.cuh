@@ -198,6 +198,16 @@ __device__ __forceinline__ double rm_prob(double rv, double S, int n) {
 }
 
 
+// single_action_note — a DP with exactly one action (a forced move) keeps
+// b = 1.0 and r = +0.0 for ever, in every variant, bit for bit:
+//   RM: S = 0.0 + max(r, 0) = 0.0 -> b = 1.0/1 = 1.0 (and r/r = 1.0 if r > 0);
+//   E = 0.0 + 1.0*q;  r' = r + ((-1.0*(0.0+E)) + q) = r + (+0.0) = r
+//   (r starts at +0.0; the floor and the DCFR scale map +0.0 to +0.0).
+// When the host marks a whole level single-action (DevTree::un == 1) the
+// passes therefore skip the r/b traffic and only produce V (and u, x, avg).
+// A non-finite q still raises the FloatingPointError flag; the run aborts
+// there exactly as the reference would.
+
 // ---------------------------------------------------------------------------
 // OBS: counterfactual values + regret update (+ variant post-op) (+ regret
 // matching of the updated regrets into b for the next iteration).
@@ -211,6 +221,14 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     bool bad = false;
+    if (T.un == 1) {  // single-action level: r and b are constants (see single_action_note)
+        const double uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<double*>(u), s0, bad) : Ld::ld(u + s0);
+        const double q = dadd(dadd(0.0, uu), child_sum<Ld>(child_of<Ld>(T, s0), V));
+        V[j] = dadd(0.0, dmul(1.0, q));
+        bad |= !isfinite(q);
+        if (bad) atomicOr(nonfinite, 1);
+        return;
+    }
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, u, V, s0, n, q, fuse, &bad);
@@ -274,6 +292,11 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* _
                                         double* __restrict__ V, bool plus) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
+    if (T.un == 1) {  // single-action level: b stays 1.0 (see single_action_note)
+        const double q = dadd(dadd(0.0, Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), V));
+        V[j] = dadd(0.0, dmul(1.0, q));
+        return;
+    }
     if (n <= MAXA) {
         double q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, m, V, s0, n, q);
@@ -330,6 +353,12 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __r
     dp_range<Ld>(T, j, s0, n);
     const int s1 = s0 + n;
     const double xp = Ld::ld(x + parent_of<Ld>(T, j));
+    if (T.un == 1) {  // single-action level: b == 1.0, so x = 1.0 * xp (single_action_note)
+        const double xa = dmul(1.0, xp);
+        x[s0] = xa;
+        if (avg) avg[s0] = dadd(dmul(w, xa), Ld::ld(avg + s0));
+        return;
+    }
     for (int s = s0; s < s1; ++s) {
         const double xa = dmul(Ld::ld(b + s), xp);
         x[s] = xa;
@@ -346,6 +375,10 @@ __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     const double xp = Ld::ld(x + parent_of<Ld>(T, j));
+    if (T.un == 1) {  // single-action level: r == +0.0, RM gives 1.0 (single_action_note)
+        x[s0] = dmul(1.0, xp);
+        return;
+    }
     if (n <= MAXA) {
         double rr[MAXA];
 #pragma unroll

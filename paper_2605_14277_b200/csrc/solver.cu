@@ -497,23 +497,27 @@ struct LevelBytes {
     static double seqptr(const Player& P, int l) { return P.lvl_shape[l].un > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
     static double child(const Player& P, int l) { return P.lvl_shape[l].cn >= 0 ? 0.0 : 8.0 * P.lvl_ns[l]; }
     static double parent(const Player& P, int l) { return P.lvl_shape[l].pc > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
+    // single-action levels touch no r / b (kernels.cuh single_action_note)
+    static bool single(const Player& P, int l) { return P.lvl_shape[l].un == 1; }
     static double obs(const Player& P, int l, bool rm) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
         // u, b read; r RMW; [b write]; V write; child V reads; structure
-        return (8 + 8 + 16 + (rm ? 8 : 0)) * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
+        const double rb = single(P, l) ? 0.0 : (8 + 16 + (rm ? 8 : 0)) * ns;
+        return 8 * ns + rb + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
     }
     static double pred(const Player& P, int l) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
         // m, b, r read; b write; V write; child V reads; structure
-        return 32 * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
+        return (single(P, l) ? 8 : 32) * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
     }
     static double td(const Player& P, int l, bool avg) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l];
         // b read, x write, [avg RMW]; parent x; structure
-        return (16 + (avg ? 16 : 0)) * ns + 8 * nj + seqptr(P, l) + parent(P, l);
+        return ((single(P, l) ? 8 : 16) + (avg ? 16 : 0)) * ns + 8 * nj + seqptr(P, l) + parent(P, l);
     }
     static double cur(const Player& P, int l) {  // r read, x write; parent x; structure
-        return 16.0 * P.lvl_ns[l] + 8.0 * P.lvl_nj[l] + seqptr(P, l) + parent(P, l);
+        return (single(P, l) ? 8.0 : 16.0) * P.lvl_ns[l] + 8.0 * P.lvl_nj[l] + seqptr(P, l) +
+               parent(P, l);
     }
     static double spmv(const DevCsr& M) {
         return 4.0 * (M.rows + 1) + 12.0 * M.nnz + 8.0 * M.cols + 8.0 * M.rows;
