@@ -187,6 +187,7 @@ struct scfr_handle {
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
+    int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;
     scfr::PersistentPlan plan;
     // Row-sharded payoff SpMV (scfr_create_sharded): NCCL communicator

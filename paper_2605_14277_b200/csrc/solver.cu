@@ -75,52 +75,55 @@ struct KParams {
 
 enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
 
+// The task's blocks stride over its DPs (grid-stride): a launch is capped at
+// about one resident wave, so the deep levels (10^6 DPs of a few loads each)
+// are not limited by CTA scheduling.
 template <int KIND, int MAXA, bool WARP>
 __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams& kp) {
     constexpr int kPerBlock = WARP ? TPB / 32 : TPB;
-    const int item = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
-    if (item >= t.n) return;  // warp-uniform in warp mode
-    const int j = t.lo + item;
+    const int stride = t.nblk * kPerBlock;
     const size_t so = (size_t)blockIdx.y * t.S;
     double* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
     const int lane = threadIdx.x & 31;
-    if constexpr (KIND == LK_TD_AVG) {
-        const double w = kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
-        double* avg = t.avg + so;
-        // the reference axpy also covers the empty sequence (x[0] = 1)
-        if (j == 0) avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
-        td_dp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w);
-    } else if constexpr (KIND == LK_TD) {
-        td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, 0.0);
-    } else if constexpr (KIND == LK_CUR) {
-        cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
-    } else if constexpr (KIND == LK_OBS) {
-        double pf = 1.0, nf = 1.0;
-        if (kp.post == POST_DCFR) {
-            const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
-            pf = kp.pfsched[k];
-            nf = kp.nfsched[k];
-        }
-        FuseU fu = t.fu;
-        if (fu.ip) {
-            fu.x += (size_t)blockIdx.y * t.fu_sx;
-            if (j == 0 && lane == 0) {  // the empty sequence's row: u[0] (next prediction)
+    double w = 0.0, pf = 1.0, nf = 1.0;
+    if (KIND == LK_TD_AVG) w = kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_OBS && kp.post == POST_DCFR) {
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        pf = kp.pfsched[k];
+        nf = kp.nfsched[k];
+    }
+    FuseU fu = t.fu;
+    if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
+    for (int item = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
+         item < t.n; item += stride) {  // warp-uniform in warp mode
+        const int j = t.lo + item;
+        if constexpr (KIND == LK_TD_AVG) {
+            double* avg = t.avg + so;
+            // the reference axpy also covers the empty sequence (x[0] = 1)
+            if (j == 0) avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
+            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w);
+        } else if constexpr (KIND == LK_TD) {
+            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, 0.0);
+        } else if constexpr (KIND == LK_CUR) {
+            cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
+        } else if constexpr (KIND == LK_OBS) {
+            if (fu.ip && j == 0 && lane == 0) {  // the empty sequence's row: u[0] (next prediction)
                 bool bad = false;
                 fused_u<LdL1>(fu, const_cast<double*>(t.u) + so, 0, bad);
                 if (bad) atomicOr(kp.nonfinite, 1);
             }
+            if constexpr (WARP)
+                obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                                  kp.do_rm != 0, kp.nonfinite, lane, fu);
+            else
+                obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                                   kp.do_rm != 0, kp.nonfinite, fu);
+        } else {
+            if constexpr (WARP)
+                pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane);
+            else
+                pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0);
         }
-        if constexpr (WARP)
-            obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                              kp.do_rm != 0, kp.nonfinite, lane, fu);
-        else
-            obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                               kp.do_rm != 0, kp.nonfinite, fu);
-    } else {
-        if constexpr (WARP)
-            pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane);
-        else
-            pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0);
     }
 }
 
@@ -624,8 +627,10 @@ struct Launcher {
         const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
                           ((A && fat(*A, la)) || (Bp && fat(*Bp, lb)));
         const int per = warp ? TPB / 32 : TPB;
-        t0.nblk = (t0.n + per - 1) / per;
-        t1.nblk = (t1.n + per - 1) / per;
+        // about one resident wave per task; the blocks grid-stride over the DPs
+        const int cap = h->num_sms * h->wave_ctas;
+        t0.nblk = std::min((t0.n + per - 1) / per, cap);
+        t1.nblk = std::min((t1.n + per - 1) / per, cap);
         int maxa = 1;
         double bytes = 0.0;
         for (int k = 0; k < 2; ++k) {
@@ -923,6 +928,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->pdl = !(np && np[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
         h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
+        if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) h->wave_ctas = std::max(1, std::atoi(wc));
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
         if (eng && h->engine == SCFR_ENGINE_AUTO && !h->comm) h->engine = std::atoi(eng);
         if (h->engine == SCFR_ENGINE_AUTO) h->engine = h->comm ? SCFR_ENGINE_LEVELS : choose_engine(h.get());
