@@ -12,6 +12,7 @@ consumes so a solve does not copy them again.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 
@@ -25,7 +26,7 @@ _KIND_NAMES = {0: "decision", 1: "observation", 2: "end"}
 class CsrMatrix:
     """Minimal CSR over float64 (reference pkg/kernels.py:33-127 layout)."""
 
-    __slots__ = ("rows", "cols", "indptr", "indices", "data", "_transpose")
+    __slots__ = ("rows", "cols", "indptr", "indices", "data", "_transpose", "_bundle")
 
     def __init__(self, rows, cols, indptr, indices, data):
         self.rows, self.cols = int(rows), int(cols)
@@ -33,6 +34,7 @@ class CsrMatrix:
         self.indices = np.ascontiguousarray(indices, dtype=np.int64)
         self.data = np.ascontiguousarray(data, dtype=np.float64)
         self._transpose = None
+        self._bundle = None  # weakref to the GameBundle owning this payoff matrix
 
     @property
     def nnz(self) -> int:
@@ -243,6 +245,7 @@ class GameBundle:
         p1, p2, U, UT = compile_flat(flat)
         self.procs = (p1, p2)
         self.payoff, self.payoff_t = U, UT
+        U._bundle = UT._bundle = weakref.ref(self)
         self._c = (p1.as_c(), p2.as_c(), U.as_c(), UT.as_c())
         self._evaluator = None
 

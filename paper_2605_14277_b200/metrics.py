@@ -50,11 +50,18 @@ def exploitability(bundle, x1, x2, backend=None) -> float:
     return (b1 + b2) / 2.0
 
 
-def expected_value(bundle, x1, x2, backend=None) -> float:
-    """x1 . (U x2).  Takes the bundle (the device evaluator needs it); the
-    reference takes the payoff matrix (pkg/metrics.py:50-56)."""
+def expected_value(payoff, x1, x2, backend=None) -> float:
+    """x1 . (U x2) (pkg/metrics.py:50-56).  ``payoff`` is the bundle's payoff
+    matrix, as in the reference, or the bundle itself; the product runs on the
+    device evaluator of the bundle that owns the matrix."""
+    from .compiler import CsrMatrix
     from .solvers import evaluator
     del backend
+    bundle = payoff
+    if isinstance(payoff, CsrMatrix):
+        bundle = payoff._bundle() if payoff._bundle is not None else None
+        if bundle is None or bundle.payoff is not payoff:
+            raise ValueError("expected_value needs the payoff matrix of a live GameBundle")
     if len(x1) != bundle.payoff.rows:
         raise ValueError("dimension mismatch: x1 does not match the payoff rows")
     return evaluator(bundle).expected_value_of(x1, x2)
