@@ -59,6 +59,14 @@ struct LdL2 {
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
+// L2-only loads with a shallow chunk: the tile engine's top pass, which
+// shares a kernel (and so a register budget) with the tile walk.
+struct LdL2s {
+    static constexpr int kChunk = 8;
+    static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+    template <class X>
+    static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
+};
 // Shared-memory resident state and structure (CTA-resident small-game engine).
 struct LdS {
     static constexpr int kChunk = 8;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <utility>
 #include <cstdint>
 #include <vector>
 
@@ -102,6 +103,7 @@ struct Player {
     std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
     std::vector<int> lvl_s0;                     // per level: first sequence
     std::vector<DevTree> lvl_shape;              // per level: affine shape (pointers unset)
+    std::vector<int> h_seq_ptr, h_dp_parent;    // host copies (tile planning)
     DevBuf<int> seq_ptr, dp_parent;
     DevBuf<int2> child;
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
@@ -160,6 +162,45 @@ bool predictive(int v);
 int post_of(int v);
 inline int grid_for(int n) { return n <= 0 ? 1 : (n + TPB - 1) / TPB; }
 
+// Per-iteration parameters shared by every pass kernel: host-computed
+// schedules indexed by the device iteration counter, the variant's post-op.
+struct KParams {
+    const double* wsched;
+    const double* pfsched;
+    const double* nfsched;
+    int cap;
+    const long long* tdev;
+    int post, do_rm, plus;
+    int* nonfinite;
+};
+
+// Tile engine plan of one player (tiled.cu): DPs below the split level are
+// renumbered tile-major (tile, level, root-first, original order) so every
+// tile is a contiguous block of DPs and of sequences.
+struct TileShape {  // one (tile, level) block, or one top level
+    int j_lo, s_lo, un, cn, c_lo, pc, p_lo, nroot;
+};
+struct TilePlayer {
+    int ls = 0;           // split level: levels [0, ls) are the top, [ls, L) are tiled
+    int Jtop = 0, Stop = 0;  // top DPs [0, Jtop), top sequences [0, Stop) (ids unchanged)
+    int ntiles = 0, nlev = 0;
+    int max_dps = 0, max_seqs = 0;  // largest tile (shared-memory sizing)
+    int maxa = 1;                   // widest DP below the split
+    std::vector<int> top_lvl;       // [ls+1] level starts of the top
+    std::vector<TileShape> top_shape;
+    unsigned top_warp = 0;          // top levels run warp-per-DP (fat)
+    std::vector<int> h_off;         // [ntiles][nlev+1] device DP offsets of the level blocks
+    std::vector<TileShape> h_shape; // [ntiles][nlev]
+    DevBuf<int> seq_ptr, dp_parent, off, sperm, dperm;
+    DevBuf<int2> child;
+    DevBuf<TileShape> shape;
+    DevBuf<unsigned> ticket;  // [B] last-CTA tickets
+    DevBuf<double> gat;       // original-order scratch for reads
+    // algorithmic bytes of one pass (host accounting)
+    double bytes_obs = 0, bytes_obs_rm = 0, bytes_pred = 0, bytes_td_avg = 0, bytes_td = 0,
+           bytes_cur = 0, bytes_spmv = 0;
+};
+
 }  // namespace scfr
 
 struct scfr_handle {
@@ -187,6 +228,7 @@ struct scfr_handle {
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
+    bool wave_ctas_env = false;
     int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;
     scfr::PersistentPlan plan;
@@ -194,6 +236,16 @@ struct scfr_handle {
     // (ncclComm_t) over `world` ranks, this handle being `rank`.
     void* comm = nullptr;
     int world = 1, rank = 0;
+    // Tile engine (SCFR_ENGINE_TILED): per-player plans and the payoff rows
+    // in the tile numbering (rows of U for player 1, of Uᵀ for player 2).
+    scfr::TilePlayer tp[2];
+    scfr::DevCsr tM[2];
+    int tile_threads = 256, tile_grid_up = 0, tile_grid_down = 0;
+    int tile_vwin = 0;       // doubles of the up pass's V window (largest tile)
+    int tile_dwin = 0;       // doubles of the down pass's x window (top + largest tile)
+    int tile_staged = 1;     // SCFR_TILE_STAGE=0: no shared-memory staging (A/B)
+    size_t tile_smem_up = 0, tile_smem_down = 0;
+    std::vector<std::pair<const void*, int>> tile_occ;  // resident CTAs per SM, per tile kernel
     ~scfr_handle() {
         if (exec) cudaGraphExecDestroy(exec);
         if (ev0) cudaEventDestroy(ev0);
@@ -203,6 +255,72 @@ struct scfr_handle {
 };
 
 namespace scfr {
+
+// Generic launch plumbing shared by the engines: optional per-launch CUDA
+// events (scfr_profile_step) and Programmatic Dependent Launch.
+struct LaunchBase {
+    scfr_handle* h;
+    int64_t count = 0;
+    std::vector<KernelRecord>* prof = nullptr;  // per-launch events when profiling
+
+    template <class F>
+    void launch(int kind, double bytes, F&& f) {
+        if (prof) {
+            KernelRecord r;
+            r.kind = kind;
+            r.bytes = bytes * h->B;
+            CUDA_OK(cudaEventCreate(&r.e0));
+            CUDA_OK(cudaEventCreate(&r.e1));
+            CUDA_OK(cudaEventRecord(r.e0, h->stream));
+            f();
+            CUDA_OK(cudaEventRecord(r.e1, h->stream));
+            prof->push_back(r);
+        } else {
+            f();
+        }
+        ++count;
+    }
+
+    // Kernel launch with Programmatic Dependent Launch allowed (the kernels
+    // call griddepcontrol.launch_dependents / .wait), so the next kernel's
+    // grid is set up while this one drains.  SCFR_NO_PDL=1 turns it off.
+    template <class... KArgs, class... Args>
+    void run_ex(void (*kern)(KArgs...), dim3 grid, int threads, size_t smem, Args... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = h->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args...));
+    }
+    template <class... KArgs, class... Args>
+    void run_threads(void (*kern)(KArgs...), dim3 grid, int threads, Args... args) {
+        run_ex(kern, grid, threads, 0, args...);
+    }
+    template <class... KArgs, class... Args>
+    void run(void (*kern)(KArgs...), dim3 grid, Args... args) {
+        run_ex(kern, grid, TPB, 0, args...);
+    }
+    template <class... KArgs, class... Args>
+    void run1(void (*kern)(KArgs...), dim3 grid, Args... args) {
+        run_ex(kern, grid, 1, 0, args...);
+    }
+    KParams kparams(bool do_rm) const;
+};
+
+// Tile engine (tiled.cu).
+bool prepare_tiled(scfr_handle* h, const scfr_csr* U, const scfr_csr* UT, bool required);
+void tiled_iteration(LaunchBase& L);
+// Device pointer to `buf` (a [B][S] vector of `player` in the engine's
+// numbering) for `solve`, in the reference's sequence order.
+const double* orig_order(scfr_handle* h, int player, const double* buf, int solve);
+__global__ void k_tick(long long* tdev);
+
 int choose_engine(scfr_handle* h);
 void prepare_persistent(scfr_handle* h);
 // Enqueues n iterations; returns the number of kernel launches issued.

@@ -63,16 +63,6 @@ struct Task {
     int fu_sx; // per-solve stride of fu.x
 };
 
-struct KParams {
-    const double* wsched;
-    const double* pfsched;
-    const double* nfsched;
-    int cap;
-    const long long* tdev;
-    int post, do_rm, plus;
-    int* nonfinite;
-};
-
 enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
 
 // The task's blocks stride over its DPs (grid-stride): a launch is capped at
@@ -94,24 +84,25 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
     }
     FuseU fu = t.fu;
     if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
-    for (int item = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
-         item < t.n; item += stride) {  // warp-uniform in warp mode
+    const int first = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
+    if (KIND == LK_TD_AVG && first == 0 && t.lo == 0 && t.n > 0) {  // the reference axpy also covers the empty sequence (x[0] = 1)
+        double* avg = t.avg + so;
+        avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
+    }
+    if (KIND == LK_OBS && fu.ip && first == 0 && lane == 0 && t.lo == 0 && t.n > 0) {  // the empty sequence's row: u[0] (next prediction)
+        bool bad = false;
+        fused_u<LdL1>(fu, const_cast<double*>(t.u) + so, 0, bad);
+        if (bad) atomicOr(kp.nonfinite, 1);
+    }
+    for (int item = first; item < t.n; item += stride) {  // warp-uniform in warp mode
         const int j = t.lo + item;
         if constexpr (KIND == LK_TD_AVG) {
-            double* avg = t.avg + so;
-            // the reference axpy also covers the empty sequence (x[0] = 1)
-            if (j == 0) avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
-            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w);
+            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w);
         } else if constexpr (KIND == LK_TD) {
             td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, 0.0);
         } else if constexpr (KIND == LK_CUR) {
             cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
-            if (fu.ip && j == 0 && lane == 0) {  // the empty sequence's row: u[0] (next prediction)
-                bool bad = false;
-                fused_u<LdL1>(fu, const_cast<double*>(t.u) + so, 0, bad);
-                if (bad) atomicOr(kp.nonfinite, 1);
-            }
             if constexpr (WARP)
                 obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
                                   kp.do_rm != 0, kp.nonfinite, lane, fu);
@@ -129,7 +120,10 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
 
 // Narrow variants (<= 2 actions in registers: the deep, bandwidth-bound
 // levels) are held to 40 registers so 12 CTAs fit per SM (more loads in
-// flight); wide / warp variants keep the default budget.
+// flight); wide / warp variants keep the default budget.  (A batched variant
+// with 4 DPs' loads in flight per thread measured no faster: these levels
+// already run within ~10% of a bare fp64 stream of the same size on B200,
+// scripts/micro/stream_probe.cu.)
 template <int KIND, int MAXA, bool WARP>
 __global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : 1) k_level(const __grid_constant__ Task t0,
                                                const __grid_constant__ Task t1,
@@ -385,7 +379,9 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     }
     k_init_root<<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
     CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaStreamSynchronize(s));  // host staging vectors die at return
+    CUDA_OK(cudaStreamSynchronize(s));
+    P.h_seq_ptr = std::move(seq_ptr);  // kept for the tile planner
+    P.h_dp_parent = std::move(dp_parent);
 }
 
 // Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
@@ -527,60 +523,15 @@ struct LevelBytes {
     }
 };
 
-struct Launcher {
-    scfr_handle* h;
-    int64_t count = 0;
-    std::vector<KernelRecord>* prof = nullptr;  // per-launch events when profiling
+KParams LaunchBase::kparams(bool do_rm) const {
+    return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
+                   post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
+                   h->nonfinite.p};
+}
 
-    template <class F>
-    void launch(int kind, double bytes, F&& f) {
-        if (prof) {
-            KernelRecord r;
-            r.kind = kind;
-            r.bytes = bytes * h->B;
-            CUDA_OK(cudaEventCreate(&r.e0));
-            CUDA_OK(cudaEventCreate(&r.e1));
-            CUDA_OK(cudaEventRecord(r.e0, h->stream));
-            f();
-            CUDA_OK(cudaEventRecord(r.e1, h->stream));
-            prof->push_back(r);
-        } else {
-            f();
-        }
-        ++count;
-    }
+struct Launcher : LaunchBase {
+    explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
 
-    // Kernel launch with Programmatic Dependent Launch allowed (the kernels
-    // call griddepcontrol.launch_dependents / .wait), so the next level's grid
-    // is set up while this one drains.  SCFR_NO_PDL=1 turns it off.
-    template <class... KArgs, class... Args>
-    void run_threads(void (*kern)(KArgs...), dim3 grid, int threads, Args... args) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = 0;
-        cfg.stream = h->stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args...));
-    }
-    template <class... KArgs, class... Args>
-    void run(void (*kern)(KArgs...), dim3 grid, Args... args) {
-        run_threads(kern, grid, TPB, args...);
-    }
-    template <class... KArgs, class... Args>
-    void run1(void (*kern)(KArgs...), dim3 grid, Args... args) {
-        run_threads(kern, grid, 1, args...);
-    }
-
-    KParams kparams(bool do_rm) const {
-        return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
-                       post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
-                       h->nonfinite.p};
-    }
 
     // Task for level l of player P (l outside [0, L) -> empty task).
     static Task task(Player& P, int l, const double* u, double* x) {
@@ -600,6 +551,20 @@ struct Launcher {
         }
         return t;
     }
+    // Resident CTAs of a level kernel on the whole GPU (cached per handle),
+    // or num_sms * SCFR_WAVE_CTAS when that is set.
+    int resident_ctas(LevelKernel kern) const {
+        if (h->wave_ctas_env) return h->num_sms * h->wave_ctas;
+        const void* key = reinterpret_cast<const void*>(kern);
+        for (const auto& e : h->tile_occ)
+            if (e.first == key) return e.second * h->num_sms;
+        int occ = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, 0));
+        occ = std::max(occ, 1);
+        h->tile_occ.emplace_back(key, occ);
+        return occ * h->num_sms;
+    }
+
     // SpMV fused into OBS unless a player has no decision points (then no
     // OBS level would produce its u) or SCFR_NO_FUSE=1.
     bool fuse_spmv() const { return h->fuse && h->P[0].J > 0 && h->P[1].J > 0; }
@@ -653,6 +618,10 @@ struct Launcher {
             }
         }
         const LevelKernel kern = pick_level_kernel(lk, maxa, warp);
+        // grid-stride tasks: cap each at one resident wave of this kernel
+        const int wave = resident_ctas(kern);
+        t0.nblk = std::min(t0.nblk, wave);
+        t1.nblk = std::min(t1.nblk, wave);
         const KParams kp = kparams(do_rm);
         launch(kk, bytes, [&] {
             run(kern, dim3(t0.nblk + t1.nblk, h->B), t0, t1, kp);
@@ -671,6 +640,10 @@ struct Launcher {
     }
 
     void iteration() {
+        if (h->engine == SCFR_ENGINE_TILED) {
+            tiled_iteration(*this);
+            return;
+        }
         Player& A = h->P[0];
         Player& Bp = h->P[1];
         const bool pr = predictive(h->variant);
@@ -758,7 +731,7 @@ static void ensure_schedule(scfr_handle* h, int64_t upto) {
 
 static void build_graph(scfr_handle* h) {
     cudaGraph_t graph;
-    Launcher L{h};
+    Launcher L(h);
     CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     L.iteration();
     CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
@@ -814,10 +787,10 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
 // (written into xbar) or the last emitted strategy.
 static const double* profile(scfr_handle* h, int player, int solve, int which) {
     Player& P = h->P[player - 1];
-    const size_t o = (size_t)solve * P.S;
-    if (which == 1) return P.x.p + o;
+    if (which == 1) return orig_order(h, player, P.x.p, solve);
     if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
-    k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(P.avg.p + o, h->avg_weight[solve], P.xbar.p, P.S);
+    const double* avg = orig_order(h, player, P.avg.p, solve);
+    k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
     CUDA_OK(cudaGetLastError());
     return P.xbar.p;
 }
@@ -843,7 +816,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
         if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
         if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
-        if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_PERSISTENT_GRID) fail(SCFR_EINVAL, "unknown engine");
+        if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_TILED) fail(SCFR_EINVAL, "unknown engine");
         if (cfg->engine == SCFR_ENGINE_PERSISTENT_GRID && cfg->batch != 1)
             fail(SCFR_EINVAL, "the grid-persistent engine runs a single solve (batch 1)");
         int ndev = 0;
@@ -928,11 +901,21 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->pdl = !(np && np[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
         h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
-        if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) h->wave_ctas = std::max(1, std::atoi(wc));
+        if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) {
+            h->wave_ctas = std::max(1, std::atoi(wc));
+            h->wave_ctas_env = true;
+        }
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
         if (eng && h->engine == SCFR_ENGINE_AUTO && !h->comm) h->engine = std::atoi(eng);
-        if (h->engine == SCFR_ENGINE_AUTO) h->engine = h->comm ? SCFR_ENGINE_LEVELS : choose_engine(h.get());
-        if (h->engine >= SCFR_ENGINE_PERSISTENT) prepare_persistent(h.get());
+        if (h->engine == SCFR_ENGINE_AUTO) {
+            // the tile engine is opt-in: bit-exact, but not yet faster than
+            // PDL-chained level kernels on the config games
+            h->engine = h->comm ? SCFR_ENGINE_LEVELS : choose_engine(h.get());
+        } else if (h->engine == SCFR_ENGINE_TILED) {
+            prepare_tiled(h.get(), U, UT, true);
+        }
+        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID)
+            prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
         stage("engine");
         *out = h.release();
@@ -977,14 +960,14 @@ int scfr_step(scfr_handle* h, int64_t n) {
         set_device(h);
         add_weights(h, n);
         CUDA_OK(cudaEventRecord(h->ev0, h->stream));
-        if (h->engine >= SCFR_ENGINE_PERSISTENT) {
+        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID) {
             h->launches += launch_persistent(h, n);
         } else if (h->use_graph) {
             if (!h->exec) build_graph(h);
             for (int64_t i = 0; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->exec, h->stream));
             h->launches += n * h->nodes_per_iter;
         } else {
-            Launcher L{h};
+            Launcher L(h);
             for (int64_t i = 0; i < n; ++i) L.iteration();
             CUDA_OK(cudaGetLastError());
             h->launches += L.count;
@@ -1003,7 +986,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
         add_weights(h, n);
         std::vector<KernelRecord> recs;
         int64_t issued = 0;
-        if (h->engine >= SCFR_ENGINE_PERSISTENT) {
+        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID) {
             KernelRecord r;
             r.kind = KK_PERSIST;
             r.bytes = persistent_bytes_per_iter(h) * (double)n;
@@ -1014,7 +997,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
             CUDA_OK(cudaEventRecord(r.e1, h->stream));
             recs.push_back(r);
         } else {
-            Launcher L{h};
+            Launcher L(h);
             L.prof = &recs;
             for (int64_t i = 0; i < n; ++i) L.iteration();
             issued = L.count;
@@ -1072,7 +1055,6 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
         set_device(h);
         Player& P = h->P[player - 1];
-        const size_t o = (size_t)solve * P.S;
         const double* src = nullptr;
         size_t off = 0, cnt = P.S;
         switch (which) {
@@ -1084,7 +1066,8 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
             case SCFR_STATE_UTILITY: src = P.u.p; break;
             default: fail(SCFR_EINVAL, "unknown state selector");
         }
-        if (cnt) CUDA_OK(copy_async(host_out, src + o + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        src = orig_order(h, player, src, solve);
+        if (cnt) CUDA_OK(copy_async(host_out, src + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
     });
 }
@@ -1096,7 +1079,7 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
         set_device(h);
         Player& P = h->P[player - 1];
-        CUDA_OK(copy_async(host_out, P.avg.p + (size_t)solve * P.S, P.S * sizeof(double),
+        CUDA_OK(copy_async(host_out, orig_order(h, player, P.avg.p, solve), P.S * sizeof(double),
                            cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         const double w = h->avg_weight[solve];
@@ -1111,7 +1094,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
         if (h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
         set_device(h);
         Player& P = h->P[player - 1];
-        CUDA_OK(copy_async(host_out, P.x.p + (size_t)solve * P.S, P.S * sizeof(double),
+        CUDA_OK(copy_async(host_out, orig_order(h, player, P.x.p, solve), P.S * sizeof(double),
                            cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
     });
@@ -1209,7 +1192,11 @@ int scfr_device_bytes(const scfr_handle* h, int64_t* out) {
             for (const DevBuf<double>* b : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V, &P.g, &P.W, &P.xbar})
                 s += b->bytes();
         }
-        for (const DevCsr* m : {&h->U, &h->UT}) s += m->indptr.bytes() + m->indices.bytes() + m->data.bytes();
+        for (const DevCsr* m : {&h->U, &h->UT, &h->tM[0], &h->tM[1]})
+            s += m->indptr.bytes() + m->indices.bytes() + m->data.bytes();
+        for (const TilePlayer& tp : h->tp)
+            s += tp.seq_ptr.bytes() + tp.dp_parent.bytes() + tp.off.bytes() + tp.sperm.bytes() +
+                 tp.child.bytes() + tp.shape.bytes() + tp.ticket.bytes() + tp.gat.bytes();
         s += h->wsched.bytes() + h->pfsched.bytes() + h->nfsched.bytes();
         *out = s;
     });

@@ -205,3 +205,47 @@ def test_row_sharded_mode_world1_bit_exact(gpu, key):
     for k in ("avg1", "avg2", "r1", "r2", "u1", "u2"):
         assert digest(st[k]) == rec["digests"][k], (key, k)
     assert s.exploitability("average")[0] == rec["expl"]
+
+
+def _tiled_or_skip(b, cfg, gpu, **kw):
+    try:
+        return Solver(b, cfg, device=gpu, engine="tiled", **kw)
+    except ValueError as e:  # the tree has no tile plan (e.g. a one-level player)
+        if "tile" in str(e):
+            pytest.skip(str(e))
+        raise
+
+
+@pytest.mark.parametrize("key", CASES)
+def test_tiled_engine_bit_exact(gpu, key):
+    """The tile engine (renumbered subtrees, one launch per pass) against the
+    reference on every lockstep case whose trees tile; reads come back in the
+    reference's order."""
+    rec = golden_meta()["lockstep"][key]
+    s = _tiled_or_skip(bundle(rec["game"]), _cfg(rec), gpu)
+    assert s.engine == "tiled"
+    done = 0
+    for chunk in (1, 3):
+        if done + chunk <= rec["iters"]:
+            s.step(chunk)
+            done += chunk
+    s.step(rec["iters"] - done)
+    for k, v in _state(s).items():
+        assert digest(v) == rec["digests"][k], (key, k)
+    e, br = s.exploitability("average")
+    assert e == rec["expl"] and list(br) == rec["br_avg"]
+    assert s.exploitability("current")[0] == rec["expl_current"]
+    s.check_finite()
+
+
+def test_tiled_graph_free_and_profiled_paths_agree(gpu, monkeypatch):
+    rec = golden_meta()["lockstep"]["goof4.pcfr+.alt.10"]
+    a = _tiled_or_skip(bundle(rec["game"]), _cfg(rec), gpu)
+    a.step(rec["iters"])
+    monkeypatch.setenv("SCFR_NO_GRAPH", "1")
+    b = _tiled_or_skip(bundle(rec["game"]), _cfg(rec), gpu)
+    b.step(rec["iters"] - 2)
+    prof = b.profile(2)
+    assert set(prof) >= {"td_avg", "tick"}
+    for k in ("avg1", "avg2", "r1", "u2"):
+        np.testing.assert_array_equal(_state(a)[k], _state(b)[k])
