@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <utility>
 #include <cstdint>
@@ -103,7 +104,10 @@ struct Player {
     std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
     std::vector<int> lvl_s0;                     // per level: first sequence
     std::vector<DevTree> lvl_shape;              // per level: affine shape (pointers unset)
-    std::vector<int> h_seq_ptr, h_dp_parent;    // host copies (tile planning)
+    // int32 host structure, valid only while scfr_create runs (host scratch
+    // reused across creates, see HostScratch in host_par.h): the tile planner
+    const std::vector<int>* h_seq_ptr = nullptr;
+    const std::vector<int>* h_dp_parent = nullptr;
     DevBuf<int> seq_ptr, dp_parent;
     DevBuf<int2> child;
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
@@ -115,7 +119,14 @@ struct Player {
 struct DevCsr {
     int rows = 0, cols = 0, nnz = 0;  // rows / nnz held on this device (a shard if sharded)
     int full_rows = 0, row0 = 0, chunk = 0;  // global rows; first local row; rows per rank
-    std::vector<int> h_indptr;  // host copy (per-level byte accounting)
+    // indptr at selected global rows (the players' level boundaries), for the
+    // per-launch byte accounting of the fused SpMV
+    std::vector<int> h_rows;
+    std::vector<int64_t> h_ptr;
+    int64_t ptr_at(int row) const {
+        const auto it = std::lower_bound(h_rows.begin(), h_rows.end(), row);
+        return it != h_rows.end() && *it == row ? h_ptr[it - h_rows.begin()] : 0;
+    }
     DevBuf<int> indptr, indices;
     DevBuf<double> data;
 };

@@ -17,7 +17,9 @@
 // graph serves every iteration.
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +30,7 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the library is dlopen'ed by the sharded mode
 
+#include "host_par.h"
 #include "runtime.h"
 
 namespace scfr {
@@ -259,49 +262,113 @@ __global__ void k_init_root(int S, int B, double* __restrict__ x, double* __rest
     xpost[(size_t)k * S] = 1.0;
 }
 
+// SCFR_TRACE=1: create-time breakdown on stderr.
+static void trace_stage(const char* what) {
+    static const bool on = [] {
+        const char* e = std::getenv("SCFR_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!on) return;
+    static auto prev = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[scfr_create]   %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - prev).count());
+    prev = now;
+}
+
 // Validates the reference DecisionProcess arrays, builds the int32 device
 // structure (seq_ptr, dp_parent on the host: O(J); child ranges and the
 // initial behaviour on the device: O(S)) and the per-level bookkeeping.
-static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s) {
+static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s, int slot) {
     if (!p || p->num_seqs < 1 || p->num_decisions < 0 || p->num_nodes < 1)
         fail(SCFR_EINVAL, "bad tfsdp sizes");
     if (p->num_seqs >= (1ll << 31) / 2) fail(SCFR_EINVAL, "tfsdp too large for int32 indexing");
     if (!p->depth || !p->dp_node || !p->dp_first_seq || !p->dp_num_actions || !p->dp_parent_seq)
         fail(SCFR_EINVAL, "tfsdp has a NULL array");
+    trace_stage("upload_player begin");
     const int S = (int)p->num_seqs, J = (int)p->num_decisions;
     P.S = S;
     P.J = J;
     P.max_actions = 0;
-    std::vector<int> seq_ptr(J + 1), dp_parent(std::max(J, 1));
-    std::vector<uint64_t> seen((S + 63) / 64, 0);  // parent sequences already grouped
-    int64_t next = 1;
-    int64_t prev_depth = -1;
-    P.lvl.clear();
-    for (int j = 0; j < J; ++j) {
-        if (p->dp_first_seq[j] != next) fail(SCFR_EINVAL, "dp_first_seq is not contiguous in j");
-        const int64_t n = p->dp_num_actions[j];
-        if (n < 1) fail(SCFR_EINVAL, "decision point without actions");
-        P.max_actions = std::max<int>(P.max_actions, (int)n);
-        seq_ptr[j] = (int)next;
-        const int64_t ps = p->dp_parent_seq[j];
-        if (ps < 0 || ps >= next) fail(SCFR_EINVAL, "dp_parent_seq out of range or after its decision point");
-        dp_parent[j] = (int)ps;
-        if (j == 0 || dp_parent[j - 1] != ps) {
-            if (seen[ps >> 6] >> (ps & 63) & 1)
-                fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
-            seen[ps >> 6] |= 1ull << (ps & 63);
+    constexpr int64_t kGrain = 1 << 16;
+    HostScratch& hs = host_scratch();  // create_impl holds the arena lock
+    std::vector<int>& seq_ptr = hs.sp[slot];
+    std::vector<int>& dp_parent = hs.par[slot];
+    std::vector<int64_t>& dpd = hs.dpd;  // depth of each DP's node
+    seq_ptr.resize(J + 1);
+    dp_parent.resize(std::max(J, 1));
+    dpd.resize(std::max(J, 1));
+    // Pass 1 (parallel over j): per-DP checks, int32 conversion.  Each chunk
+    // keeps its first offending j; the smallest one is reported.
+    struct Bad {
+        int64_t j = INT64_MAX;
+        int code = 0;
+    };
+    const int T = host_threads();
+    std::vector<Bad> bad(T);
+    std::vector<int> maxa_c(T, 0);
+    parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
+        Bad bd;
+        int ma = 0;
+        for (int64_t j = lo; j < hi; ++j) {
+            const int64_t fs = p->dp_first_seq[j];
+            const int64_t expect = j == 0 ? 1 : p->dp_first_seq[j - 1] + p->dp_num_actions[j - 1];
+            const int64_t n = p->dp_num_actions[j], ps = p->dp_parent_seq[j], node = p->dp_node[j];
+            const int code = fs != expect ? 1 : n < 1 ? 2 : (ps < 0 || ps >= fs) ? 3
+                           : (node < 0 || node >= p->num_nodes) ? 4 : 0;
+            if (code) {
+                bd.j = j;
+                bd.code = code;
+                break;
+            }
+            ma = std::max(ma, (int)n);
+            seq_ptr[j] = (int)fs;
+            dp_parent[j] = (int)ps;
+            dpd[j] = p->depth[node];
         }
-        next += n;
-        const int64_t node = p->dp_node[j];
-        if (node < 0 || node >= p->num_nodes) fail(SCFR_EINVAL, "dp_node out of range");
-        const int64_t d = p->depth[node];
-        if (d < prev_depth) fail(SCFR_EINVAL, "decision points are not ordered by depth");
-        if (d != prev_depth) P.lvl.push_back(j);
-        prev_depth = d;
+        bad[c] = bd;
+        maxa_c[c] = ma;
+    });
+    {
+        Bad first;
+        for (const Bad& bd : bad)
+            if (bd.j < first.j) first = bd;
+        static const char* msg[] = {"", "dp_first_seq is not contiguous in j", "decision point without actions",
+                                    "dp_parent_seq out of range or after its decision point",
+                                    "dp_node out of range"};
+        if (first.code) fail(SCFR_EINVAL, "%s", msg[first.code]);
+        for (int m : maxa_c) P.max_actions = std::max(P.max_actions, m);
+        const int64_t next = J ? p->dp_first_seq[J - 1] + p->dp_num_actions[J - 1] : 1;
+        if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     }
-    P.lvl.push_back(J);
-    if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     seq_ptr[J] = S;
+    // Pass 2 (parallel): depth order, level starts, and each parent sequence's
+    // child DPs forming one contiguous group (a group start may not repeat).
+    {
+        const size_t W = ((size_t)S + 63) / 64;
+        std::unique_ptr<std::atomic<uint64_t>[]> seen(new std::atomic<uint64_t>[W]());
+        std::vector<std::vector<int>> starts(T);
+        std::vector<int> order_bad(T, 0), group_bad(T, 0);
+        parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
+            for (int64_t j = lo; j < hi; ++j) {
+                if (j > 0 && dpd[j] < dpd[j - 1]) order_bad[c] = 1;
+                if (j == 0 || dpd[j] != dpd[j - 1]) starts[c].push_back((int)j);
+                const int ps = dp_parent[j];
+                if (j == 0 || dp_parent[j - 1] != ps) {
+                    const uint64_t bit = 1ull << (ps & 63);
+                    if (seen[ps >> 6].fetch_or(bit, std::memory_order_relaxed) & bit) group_bad[c] = 1;
+                }
+            }
+        });
+        for (int c = 0; c < T; ++c) {
+            if (group_bad[c]) fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
+            if (order_bad[c]) fail(SCFR_EINVAL, "decision points are not ordered by depth");
+        }
+        P.lvl.clear();
+        for (auto& v : starts) P.lvl.insert(P.lvl.end(), v.begin(), v.end());
+        P.lvl.push_back(J);
+    }
+    trace_stage("validate+seq_ptr");
     const int L = (int)P.lvl.size() - 1;
     P.lvl_ns.assign(L, 0);
     P.lvl_nj.assign(L, 0);
@@ -313,48 +380,95 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
         P.lvl_s0[l] = seq_ptr[j0];
         P.lvl_ns[l] = seq_ptr[j1] - seq_ptr[j0];
         P.lvl_nj[l] = j1 - j0;
-        int ma = 0;
-        for (int j = j0; j < j1; ++j) ma = std::max(ma, seq_ptr[j + 1] - seq_ptr[j]);
-        P.lvl_maxa[l] = ma;
     }
-    for (int j = 0; j < J; ++j) {  // child-DP references per level = DPs whose parent lies in it
-        const int ps = dp_parent[j];
-        if (ps == 0) continue;
-        const int l = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), ps) - P.lvl_s0.begin()) - 1;
-        if (l >= 0) P.lvl_nc[l] += 1;
+    // Per-level statistics and exact affine shapes (kernels then compute
+    // indices instead of loading them), parallel over j and over sequences.
+    std::vector<int>& ccnt = hs.ccnt;  // child-DP group of each sequence
+    std::vector<int>& cfirst = hs.cfirst;
+    ccnt.resize(S);
+    cfirst.resize(S);
+    parallel_chunks(S, kGrain, [&](int, int64_t lo, int64_t hi) {
+        std::fill(ccnt.begin() + lo, ccnt.begin() + hi, 0);
+        std::fill(cfirst.begin() + lo, cfirst.begin() + hi, -1);
+    });
+    std::vector<int> pc(L, 1);
+    for (int l = 0; l < L; ++l) {
+        const int j0 = P.lvl[l], j1 = P.lvl[l + 1];
+        while (j0 + pc[l] < j1 && dp_parent[j0 + pc[l]] == dp_parent[j0]) ++pc[l];
     }
-    // Affine level shapes (exact; kernels then compute indices instead of loading them).
-    {
-        std::vector<int> ccnt(S, 0), cfirst(S, -1);
-        for (int j = 0; j < J; ++j) {
-            if (cfirst[dp_parent[j]] < 0) cfirst[dp_parent[j]] = j;
-            ccnt[dp_parent[j]]++;
+    auto level_of_j = [&](int64_t j) {
+        return (int)(std::upper_bound(P.lvl.begin(), P.lvl.end(), (int)j) - P.lvl.begin()) - 1;
+    };
+    std::vector<std::vector<int>> cmax(T, std::vector<int>(L, 0)), cmin(T, std::vector<int>(L, INT32_MAX)),
+        cpar(T, std::vector<int>(L, 1));
+    std::vector<std::vector<double>> cnc(T, std::vector<double>(L, 0.0));
+    parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
+        // chunk-local accumulators (written back once: no false sharing)
+        std::vector<int> mx(L, 0), mn(L, INT32_MAX), pr(L, 1);
+        std::vector<double> nc(L, 0.0);
+        int l = lo < hi ? level_of_j(lo) : 0;
+        for (int64_t j = lo; j < hi; ++j) {
+            while (j >= P.lvl[l + 1]) ++l;
+            const int a = seq_ptr[j + 1] - seq_ptr[j];
+            mx[l] = std::max(mx[l], a);
+            mn[l] = std::min(mn[l], a);
+            const int ps = dp_parent[j];
+            const int j0 = P.lvl[l];
+            if (ps != dp_parent[j0] + (int)((j - j0) / pc[l])) pr[l] = 0;
+            if (ps != 0) {  // child-DP references per level = DPs whose parent lies in it
+                const int lp = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), ps) - P.lvl_s0.begin()) - 1;
+                if (lp >= 0) nc[lp] += 1;
+            }
+            if (j == 0 || dp_parent[j - 1] != ps) {  // group start: record the group
+                int64_t e = j + 1;
+                while (e < J && dp_parent[e] == ps) ++e;
+                cfirst[ps] = (int)j;
+                ccnt[ps] = (int)(e - j);
+            }
         }
-        P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
-        for (int l = 0; l < L; ++l) {
-            DevTree& sh = P.lvl_shape[l];
-            const int j0 = P.lvl[l], j1 = P.lvl[l + 1], s0 = seq_ptr[j0], s1 = seq_ptr[j1];
-            sh.j_lo = j0;
-            sh.s_lo = s0;
-            const int n0 = seq_ptr[j0 + 1] - seq_ptr[j0];
-            bool uni = true;
-            for (int j = j0; j < j1 && uni; ++j) uni = seq_ptr[j + 1] - seq_ptr[j] == n0;
-            sh.un = uni ? n0 : 0;
-            const int c0 = ccnt[s0];
-            bool aff = true;
-            for (int q = s0; q < s1 && aff; ++q)
-                aff = ccnt[q] == c0 && (c0 == 0 || cfirst[q] == cfirst[s0] + (q - s0) * c0);
-            sh.cn = aff ? c0 : -1;
-            sh.c_lo = aff && c0 > 0 ? cfirst[s0] : 0;
-            int pc = 1;
-            while (j0 + pc < j1 && dp_parent[j0 + pc] == dp_parent[j0]) ++pc;
-            bool par = true;
-            for (int j = j0; j < j1 && par; ++j) par = dp_parent[j] == dp_parent[j0] + (j - j0) / pc;
-            sh.pc = par ? pc : 0;
-            sh.p_lo = dp_parent[j0];
+        cmax[c] = std::move(mx);
+        cmin[c] = std::move(mn);
+        cpar[c] = std::move(pr);
+        cnc[c] = std::move(nc);
+    });
+    std::vector<std::vector<int>> caff(T, std::vector<int>(L, 1));
+    parallel_chunks(S > 1 ? S - 1 : 0, kGrain, [&](int c, int64_t lo, int64_t hi) {
+        if (lo >= hi) return;
+        std::vector<int> af(L, 1);
+        int l = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), (int)(lo + 1)) - P.lvl_s0.begin()) - 1;
+        for (int64_t q1 = lo; q1 < hi; ++q1) {
+            const int q = (int)q1 + 1;  // sequences 1..S-1, level by level
+            while (l + 1 < L && q >= P.lvl_s0[l + 1]) ++l;
+            const int s0 = P.lvl_s0[l], c0 = ccnt[s0];
+            if (!(ccnt[q] == c0 && (c0 == 0 || cfirst[q] == cfirst[s0] + (q - s0) * c0))) af[l] = 0;
         }
+        caff[c] = std::move(af);
+    });
+    P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
+    for (int l = 0; l < L; ++l) {
+        int mx = 0, mn = INT32_MAX, par = 1, aff = 1;
+        double nc = 0;
+        for (int c = 0; c < T; ++c) {
+            mx = std::max(mx, cmax[c][l]);
+            mn = std::min(mn, cmin[c][l]);
+            par &= cpar[c][l];
+            aff &= caff[c][l];
+            nc += cnc[c][l];
+        }
+        P.lvl_maxa[l] = mx;
+        P.lvl_nc[l] = nc;
+        DevTree& sh = P.lvl_shape[l];
+        const int j0 = P.lvl[l], s0 = seq_ptr[j0];
+        sh.j_lo = j0;
+        sh.s_lo = s0;
+        sh.un = mn == mx ? mx : 0;
+        const int c0 = ccnt[s0];
+        sh.cn = aff ? c0 : -1;
+        sh.c_lo = aff && c0 > 0 ? cfirst[s0] : 0;
+        sh.pc = par ? pc[l] : 0;
+        sh.p_lo = dp_parent[j0];
     }
-
+    trace_stage("affine shapes");
     P.seq_ptr.alloc(J + 1);
     P.dp_parent.alloc(std::max(J, 1));
     P.child.alloc(S);
@@ -373,6 +487,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     P.W.alloc(std::max(J, 1));
     P.xbar.alloc(S);
     for (auto* buf : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
+    trace_stage("copies+allocs");
     if (J) {
         k_derive_child<<<grid_for(J), TPB, 0, s>>>(J, P.dp_parent.p, P.child.p);
         k_derive_uniform<<<grid_for(J), TPB, 0, s>>>(J, S, B, P.seq_ptr.p, P.b.p);
@@ -380,13 +495,15 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s)
     k_init_root<<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(s));
-    P.h_seq_ptr = std::move(seq_ptr);  // kept for the tile planner
-    P.h_dp_parent = std::move(dp_parent);
+    trace_stage("derive+sync");
+    P.h_seq_ptr = &seq_ptr;  // for the tile planner, during this create only
+    P.h_dp_parent = &dp_parent;
 }
 
 // Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
 // last shard may hold fewer), re-based so local row i is global row0 + i.
-static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, int world = 1, int rank = 0) {
+static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Player& rowP, int world = 1,
+                       int rank = 0) {
     if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
     if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
     if (m->indptr[0] != 0 || m->indptr[m->rows] != m->nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
@@ -400,22 +517,58 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, int world =
     D.cols = (int)m->cols;
     const int64_t k0 = m->indptr[r0], k1 = m->indptr[r1];
     D.nnz = (int)(k1 - k0);
-    std::vector<int> ip(D.rows + 1), ix(D.nnz);
-    for (int64_t i = 0; i <= D.rows; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
-    for (int64_t k = k0; k < k1; ++k) {
-        if (m->indices[k] < 0 || m->indices[k] >= m->cols) fail(SCFR_EINVAL, "column index out of range");
-        ix[k - k0] = (int)m->indices[k];
+    trace_stage("upload_csr begin");
+    // int32 conversion straight into pinned staging (parallel over rows and
+    // nnz), then DMA; pageable host vectors if pinning is unavailable.
+    PinnedArena& pa = pinned_arena();  // create_impl holds pa.lock
+    pa.reset();
+    int* ip = static_cast<int*>(pa.take((size_t)(D.rows + 1) * sizeof(int)));
+    int* ix = static_cast<int*>(pa.take((size_t)std::max(D.nnz, 1) * sizeof(int)));
+    double* dv = static_cast<double*>(pa.take((size_t)std::max(D.nnz, 1) * sizeof(double)));
+    std::vector<int> ipv, ixv;
+    const bool pinned = ip && ix && dv;
+    if (!pinned) {
+        ipv.resize(D.rows + 1);
+        ixv.resize(std::max(D.nnz, 1));
+        ip = ipv.data();
+        ix = ixv.data();
+        dv = nullptr;
     }
-    D.h_indptr.assign(m->indptr, m->indptr + m->rows + 1);  // global (per-level accounting)
+    D.h_rows.clear();  // level boundaries of the row player (global rows)
+    D.h_ptr.clear();
+    for (int l = 0; l <= rowP.levels(); ++l) {
+        const int r = l < rowP.levels() ? rowP.lvl_s0[l] : rowP.S;
+        if (r >= 0 && r <= m->rows && (D.h_rows.empty() || D.h_rows.back() < r)) {
+            D.h_rows.push_back(r);
+            D.h_ptr.push_back(m->indptr[r]);
+        }
+    }
+    parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
+    });
+    std::vector<int> badcol(host_threads(), 0);
+    parallel_chunks(D.nnz, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) {
+            const int64_t col = m->indices[k0 + k];
+            if (col < 0 || col >= m->cols) badcol[c] = 1;
+            ix[k] = (int)col;
+        }
+        if (dv) std::memcpy(dv + lo, m->data + k0 + lo, (hi - lo) * sizeof(double));
+    });
+    for (int b : badcol)
+        if (b) fail(SCFR_EINVAL, "column index out of range");
+    trace_stage("csr convert");
     D.indptr.alloc(D.rows + 1);
     D.indices.alloc(std::max(D.nnz, 1));
     D.data.alloc(std::max(D.nnz, 1));
-    CUDA_OK(copy_async(D.indptr.p, ip.data(), ip.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_OK(copy_async(D.indptr.p, ip, (size_t)(D.rows + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
     if (D.nnz) {
-        CUDA_OK(copy_async(D.indices.p, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-        CUDA_OK(copy_async(D.data.p, m->data + k0, D.nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        CUDA_OK(copy_async(D.indices.p, ix, (size_t)D.nnz * sizeof(int), cudaMemcpyHostToDevice, s));
+        CUDA_OK(copy_async(D.data.p, dv ? dv : m->data + k0, (size_t)D.nnz * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
+    trace_stage("csr copies+sync");
 }
 
 // --- NCCL (loaded at run time; only the row-sharded mode needs it) -------
@@ -613,7 +766,7 @@ struct Launcher : LaunchBase {
             if (fused) {  // this level's payoff rows; u is written instead of read
                 const DevCsr& M = k == 0 ? h->U : h->UT;
                 const int s0 = P->lvl_s0[l], s1 = s0 + (int)P->lvl_ns[l];
-                const double nnz = M.h_indptr[s1] - M.h_indptr[s0];
+                const double nnz = (double)(M.ptr_at(s1) - M.ptr_at(s0));
                 bytes += 4.0 * (s1 - s0 + 1) + 12.0 * nnz + 8.0 * nnz;
             }
         }
@@ -742,6 +895,28 @@ static void build_graph(scfr_handle* h) {
 
 static void set_device(const scfr_handle* h) { CUDA_OK(cudaSetDevice(h->device)); }
 
+// Device -> caller memory for large state reads: DMA into the pinned arena,
+// then a parallel copy out (pageable DMA of a Goofspiel-5 vector is ~3 ms).
+static void read_to_host(scfr_handle* h, double* host_out, const double* dev, size_t count) {
+    if (!count) return;
+    const size_t bytes = count * sizeof(double);
+    PinnedArena& pa = pinned_arena();
+    std::lock_guard<std::mutex> guard(pa.lock);
+    pa.reset();
+    double* stage = bytes >= (1u << 20) && pa.reserve(std::max(bytes, pa.cap)) ? static_cast<double*>(pa.take(bytes))
+                                                                               : nullptr;
+    if (!stage) {
+        CUDA_OK(copy_async(host_out, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        return;
+    }
+    CUDA_OK(copy_async(stage, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    parallel_chunks((int64_t)count, 1 << 16, [&](int, int64_t lo, int64_t hi) {
+        std::memcpy(host_out + lo, stage + lo, (hi - lo) * sizeof(double));
+    });
+}
+
 static void check_player(const scfr_handle* h, int player, int solve) {
     if (!h) fail(SCFR_EINVAL, "handle is NULL");
     if (player != 1 && player != 2) fail(SCFR_EINVAL, "player must be 1 or 2");
@@ -824,12 +999,17 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (e != cudaSuccess || ndev == 0) fail(SCFR_ECUDA, "no CUDA device available: %s", cudaGetErrorString(e));
         if (device < 0 || device >= ndev) fail(SCFR_EINVAL, "device index out of range");
         CUDA_OK(cudaSetDevice(device));
-        cudaDeviceProp prop;
-        CUDA_OK(cudaGetDeviceProperties(&prop, device));
-        if (prop.major < 10) fail(SCFR_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+        int major = 0, nsm = 0;  // (cudaGetDeviceProperties costs milliseconds)
+        CUDA_OK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        if (major < 10) {
+            int minor = 0;
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+            fail(SCFR_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, major, minor);
+        }
         std::unique_ptr<scfr_handle> h(new scfr_handle());
         h->device = device;
-        h->num_sms = prop.multiProcessorCount;
+        h->num_sms = nsm;
         h->B = cfg->batch;
         h->variant = cfg->variant;
         h->mode = cfg->mode;
@@ -862,13 +1042,16 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         CUDA_OK(cudaEventCreate(&h->ev0));
         CUDA_OK(cudaEventCreate(&h->ev1));
         stage("stream");
-        upload_player(p1, h->P[0], h->B, h->stream);
+        PinnedArena& pa = pinned_arena();
+        std::lock_guard<std::mutex> pin_guard(pa.lock);
+        pa.reserve((size_t)std::max(U->rows, UT->rows) * 4 + (size_t)std::max<int64_t>(U->nnz, 1) * 12 + 4096);
+        upload_player(p1, h->P[0], h->B, h->stream, 0);
         stage("player1");
-        upload_player(p2, h->P[1], h->B, h->stream);
+        upload_player(p2, h->P[1], h->B, h->stream, 1);
         stage("player2");
         const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
-        upload_csr(U, h->U, h->stream, w, rk);
-        upload_csr(UT, h->UT, h->stream, w, rk);
+        upload_csr(U, h->U, h->stream, h->P[0], w, rk);
+        upload_csr(UT, h->UT, h->stream, h->P[1], w, rk);
         if (nccl_id) {
             // u and the BR gradient are gathered as world x chunk (padded) vectors
             for (int k = 0; k < 2; ++k) {
@@ -917,6 +1100,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID)
             prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
+        for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
         stage("engine");
         *out = h.release();
     }
@@ -1067,8 +1251,7 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
             default: fail(SCFR_EINVAL, "unknown state selector");
         }
         src = orig_order(h, player, src, solve);
-        if (cnt) CUDA_OK(copy_async(host_out, src + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CUDA_OK(cudaStreamSynchronize(h->stream));
+        read_to_host(h, host_out, src + off, cnt);
     });
 }
 
@@ -1079,11 +1262,11 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
         set_device(h);
         Player& P = h->P[player - 1];
-        CUDA_OK(copy_async(host_out, orig_order(h, player, P.avg.p, solve), P.S * sizeof(double),
-                           cudaMemcpyDeviceToHost, h->stream));
-        CUDA_OK(cudaStreamSynchronize(h->stream));
-        const double w = h->avg_weight[solve];
-        for (int i = 0; i < P.S; ++i) host_out[i] = host_out[i] / w;
+        // avg_accum / avg_weight (IEEE division, as the reference's numpy divide)
+        const double* avg = orig_order(h, player, P.avg.p, solve);
+        k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
+        CUDA_OK(cudaGetLastError());
+        read_to_host(h, host_out, P.xbar.p, P.S);
     });
 }
 
@@ -1094,9 +1277,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
         if (h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
         set_device(h);
         Player& P = h->P[player - 1];
-        CUDA_OK(copy_async(host_out, orig_order(h, player, P.x.p, solve), P.S * sizeof(double),
-                           cudaMemcpyDeviceToHost, h->stream));
-        CUDA_OK(cudaStreamSynchronize(h->stream));
+        read_to_host(h, host_out, orig_order(h, player, P.x.p, solve), P.S);
     });
 }
 

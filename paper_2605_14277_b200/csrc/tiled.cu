@@ -538,8 +538,9 @@ struct PlayerPlan {
 static bool plan_player(const scfr_handle* h, const Player& P, TilePlayer& tp, PlayerPlan& pp) {
     const int J = P.J, S = P.S, L = P.levels();
     if (J == 0 || L < 2) return false;
-    const std::vector<int>& sp = P.h_seq_ptr;
-    const std::vector<int>& par = P.h_dp_parent;
+    if (!P.h_seq_ptr || !P.h_dp_parent) return false;
+    const std::vector<int>& sp = *P.h_seq_ptr;
+    const std::vector<int>& par = *P.h_dp_parent;
     std::vector<int> seq_dp(S, -1), lev(J);
     for (int j = 0; j < J; ++j)
         for (int s = sp[j]; s < sp[j + 1]; ++s) seq_dp[s] = j;
@@ -779,7 +780,6 @@ bool prepare_tiled(scfr_handle* h, const scfr_csr* U, const scfr_csr* UT, bool r
             }
             ip[i + 1] = q;
         }
-        D.h_indptr.assign(ip.begin(), ip.end());
         D.indptr.alloc(ip.size());
         D.indices.alloc(ix.size());
         D.data.alloc(dv.size());
