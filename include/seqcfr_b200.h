@@ -73,6 +73,7 @@ extern "C" {
 #define SCFR_ENGINE_PERSISTENT 2      /* whole iterations in one kernel, one CTA per solve */
 #define SCFR_ENGINE_PERSISTENT_GRID 3 /* whole iterations in one cooperative grid (batch 1) */
 #define SCFR_ENGINE_TILED 4           /* one kernel per pass: CTAs own whole subtrees below a split level */
+#define SCFR_ENGINE_PERSISTENT_CLUSTER 5 /* whole iterations in one kernel, one 16-CTA cluster per solve */
 
 const char* scfr_last_error(void);
 int scfr_abi_version(void);

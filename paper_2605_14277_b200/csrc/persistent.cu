@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "runtime.h"
 
 namespace scfr {
@@ -85,7 +87,20 @@ template <int MAXA, class Ld>
 __device__ __noinline__ void phase_dps(int kind, DevTree T, int lo, int n, int begin, int stride,
                                        const double* u, double* r, double* b, double* x,
                                        double* xpost, double* avg, double* V, double w, int post,
-                                       double pf, double nf, int pred, int plus, int* nonfinite) {
+                                       double pf, double nf, int pred, int plus, int* nonfinite,
+                                       bool warp) {
+    if (warp && (kind == PH_OBS || kind == PH_PRED)) {
+        // warp-per-DP (fat / wide levels): begin and stride count warps
+        const int lane = threadIdx.x & 31;
+        for (int i = begin; i < n; i += stride) {
+            const int j = lo + i;
+            if (kind == PH_OBS)
+                obs_dp_warp<Ld>(T, j, u, r, b, V, post, pf, nf, pred == 0, nonfinite, lane);
+            else
+                pred_dp_warp<Ld>(T, j, u, r, b, V, plus != 0, lane);
+        }
+        return;
+    }
     for (int i = begin; i < n; i += stride) {
         const int j = lo + i;
         switch (kind) {
@@ -126,21 +141,37 @@ __device__ __noinline__ void phase_spmv(const int* ip, const int* ix, const doub
 template <int K, int MAXA, class Ld>
 __device__ __forceinline__ void player_phase(const PArgs& a, const Phase& ph, int lo, int n,
                                              int begin, int stride, int solve, double w,
-                                             double pf, double nf) {
+                                             double pf, double nf, bool warp) {
     if (n <= 0) return;
     const size_t o = (size_t)solve * a.S[K];
     phase_dps<MAXA, Ld>(ph.kind, a.T[K], lo, n, begin, stride, a.u[K] + o, a.r[K] + o,
                         a.b[K] + o, a.x[K] + o, a.xpost[K] + o, a.avg[K] + o,
                         a.V[K] + (size_t)solve * (a.J[K] > 0 ? a.J[K] : 1), w, a.post, pf, nf,
-                        a.pred, a.plus, a.nonfinite);
+                        a.pred, a.plus, a.nonfinite, warp);
 }
 
-template <bool GRID, int MAXA, int THREADS>
+// MODE: PM_CTA (one CTA per solve, __syncthreads), PM_GRID (one solve over
+// a cooperative grid, atomic grid barrier), PM_CLUSTER (one solve per
+// thread-block cluster of up to 16 SMs, hardware cluster barrier; a batch is
+// one cluster per solve).  Grid and cluster modes read mutable state from L2
+// (ld.global.cg): the producers are other SMs.
+enum : int { PM_CTA = 0, PM_GRID = 1, PM_CLUSTER = 2 };
+
+template <int MODE, int MAXA, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_persistent(const __grid_constant__ PArgs a) {
-    using Ld = std::conditional_t<GRID, LdL2, LdL1>;
-    const int solve = GRID ? 0 : blockIdx.x;
-    const int rank = GRID ? blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
-    const int size = GRID ? gridDim.x * blockDim.x : blockDim.x;
+    constexpr bool GRID = MODE == PM_GRID;
+    using Ld = std::conditional_t<MODE != PM_CTA, LdL2, LdL1>;
+    int solve = 0, rank = 0, size = 0;
+    if constexpr (MODE == PM_CLUSTER) {
+        const cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        solve = blockIdx.x / (int)cl.num_blocks();
+        rank = (int)cl.block_rank() * blockDim.x + threadIdx.x;
+        size = (int)cl.num_blocks() * blockDim.x;
+    } else {
+        solve = GRID ? 0 : blockIdx.x;
+        rank = GRID ? blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
+        size = GRID ? gridDim.x * blockDim.x : blockDim.x;
+    }
     const size_t o1 = (size_t)solve * a.S[0], o2 = (size_t)solve * a.S[1];
     for (int it = 0; it < a.n_iter; ++it) {
         const size_t si = (size_t)solve * a.cap + (size_t)(a.t0 + it);
@@ -150,10 +181,16 @@ __global__ void __launch_bounds__(THREADS) k_persistent(const __grid_constant__ 
         for (int p = 0; p < a.nphase; ++p) {
             const Phase ph = a.prog[p];
             if (ph.kind < PH_SPMV_U) {
-                // items [0,n1) are player-1 DPs, [n1,n1+n2) player-2 DPs
-                player_phase<0, MAXA, Ld>(a, ph, ph.lo1, ph.n1, rank, size, solve, w, pf, nf);
-                const int b2 = ((rank - ph.n1) % size + size) % size;
-                player_phase<1, MAXA, Ld>(a, ph, ph.lo2, ph.n2, b2, size, solve, w, pf, nf);
+                // items [0,n1) are player-1 DPs, [n1,n1+n2) player-2 DPs; in
+                // warp mode an item is a warp (lanes = actions)
+                const int wr = rank >> 5, ws = size >> 5;
+                const bool w1 = ph.warp1 && ws > 0, w2 = ph.warp2 && ws > 0;
+                player_phase<0, MAXA, Ld>(a, ph, ph.lo1, ph.n1, w1 ? wr : rank, w1 ? ws : size, solve,
+                                          w, pf, nf, w1);
+                const int r2 = w2 ? wr : rank, s2 = w2 ? ws : size;
+                const int n1u = w1 == w2 ? ph.n1 : 0;  // continue after player 1's items
+                const int b2 = ((r2 - n1u) % s2 + s2) % s2;
+                player_phase<1, MAXA, Ld>(a, ph, ph.lo2, ph.n2, b2, s2, solve, w, pf, nf, w2);
             } else {
                 // payoff SpMV: rows of U (-> u1), then rows of Uᵀ (-> u2 = -Uᵀ x1)
                 const double* x1 = (a.alt ? a.xpost[0] : a.x[0]) + o1;
@@ -171,11 +208,12 @@ __global__ void __launch_bounds__(THREADS) k_persistent(const __grid_constant__ 
                 if (a.J[0] == 0) a.avg[0][o1] = dadd(dmul(w, Ld::ld(a.x[0] + o1)), Ld::ld(a.avg[0] + o1));
                 if (a.J[1] == 0) a.avg[1][o2] = dadd(dmul(w, Ld::ld(a.x[1] + o2)), Ld::ld(a.avg[1] + o2));
             }
-            if (GRID) grid_sync(a.barrier);
+            if constexpr (MODE == PM_CLUSTER) cooperative_groups::this_cluster().sync();
+            else if constexpr (GRID) grid_sync(a.barrier);
             else __syncthreads();
         }
     }
-    if (rank == 0 && (GRID || blockIdx.x == 0)) *a.tdev = a.t0 + a.n_iter;
+    if (rank == 0 && (GRID || (MODE == PM_CLUSTER ? solve == 0 : blockIdx.x == 0))) *a.tdev = a.t0 + a.n_iter;
 }
 
 // ---------------------------------------------------------------------------
@@ -354,8 +392,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
 
 // CTA mode: 256 threads, 4 actions in registers; grid mode: 128 threads x
 // all SMs, 8 actions in registers (Liar's dice has up to 12-way DPs).
-static constexpr auto kCta = k_persistent<false, 4, 256>;
-static constexpr auto kGrid = k_persistent<true, 8, 128>;
+static constexpr auto kCta = k_persistent<PM_CTA, 4, 256>;
+static constexpr auto kGrid = k_persistent<PM_GRID, 8, 128>;
+// Cluster mode: 16 CTAs (the non-portable maximum) x 256 threads per solve.
+static constexpr int kClusterThreads = 256;
+static constexpr auto kClu = k_persistent<PM_CLUSTER, 8, kClusterThreads>;
 static constexpr int kSmallThreads = 256;
 static constexpr auto kSmall = k_small<2, kSmallThreads>;
 static constexpr int kSmemLimit = 220 * 1024;
@@ -390,7 +431,8 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
 
 // Same rule as the level engine: few DPs, >= 8 child-DP references per DP.
 static bool fat_level(const Player& P, int l) {
-    return P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l];
+    return (P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l]) ||
+           (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
 static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, const Player* B,
@@ -453,8 +495,32 @@ void prepare_persistent(scfr_handle* h) {
     PersistentPlan& pl = h->plan;
     pl.host_program = build_program(h);
     pl.grid = h->engine == SCFR_ENGINE_PERSISTENT_GRID;
-    pl.threads = pl.grid ? 128 : 256;  // must match kGrid / kCta
-    if (pl.grid) {
+    pl.cluster = h->engine == SCFR_ENGINE_PERSISTENT_CLUSTER;
+    pl.threads = pl.grid ? 128 : 256;  // must match kGrid / kCta / kClu
+    if (pl.cluster) {
+        int want = 16;
+        if (const char* e = std::getenv("SCFR_CLUSTER_SIZE")) want = std::max(1, std::min(16, std::atoi(e)));
+        CUDA_OK(cudaFuncSetAttribute(kClu, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (; want >= 1; want /= 2) {  // largest cluster the device can co-schedule
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(want * h->B);
+            cfg.blockDim = dim3(kClusterThreads);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = want;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, kClu, &cfg) == cudaSuccess && nclusters >= 1) break;
+            cudaGetLastError();
+        }
+        if (want < 1) fail(SCFR_ECUDA, "cluster-persistent kernel cannot be scheduled");
+        pl.csize = want;
+        pl.ctas = want * h->B;
+        pl.threads = kClusterThreads;
+    } else if (pl.grid) {
         int occ = 0;
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kGrid, pl.threads, 0));
         if (occ < 1) fail(SCFR_ECUDA, "persistent kernel cannot be resident");
@@ -532,7 +598,20 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
     for (int64_t done = 0; done < n; done += chunk) {
         a.t0 = h->t + done;
         a.n_iter = (int)std::min<int64_t>(chunk, n - done);
-        if (pl.grid) {
+        if (pl.cluster) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(pl.ctas);
+            cfg.blockDim = dim3(pl.threads);
+            cfg.stream = h->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = pl.csize;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CUDA_OK(cudaLaunchKernelEx(&cfg, kClu, a));
+        } else if (pl.grid) {
             void* args[] = {&a};
             CUDA_OK(cudaLaunchCooperativeKernel((const void*)kGrid, dim3(pl.ctas),
                                                 dim3(pl.threads), args, 0, h->stream));

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <utility>
 #include <cstdint>
 #include <vector>
@@ -154,6 +155,8 @@ struct SmemPlan {
 
 struct PersistentPlan {
     bool grid = false;   // true: one solve over a cooperative grid; false: one CTA per solve
+    bool cluster = false;  // one solve per thread-block cluster of csize CTAs
+    int csize = 0;
     bool small = false;  // CTA mode with state + structure resident in shared memory
     SmemPlan smem{};
     int ctas = 0, threads = 0;
@@ -171,7 +174,17 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 bool predictive(int v);
 int post_of(int v);
+inline bool is_persistent(int engine) {
+    return engine == SCFR_ENGINE_PERSISTENT || engine == SCFR_ENGINE_PERSISTENT_GRID ||
+           engine == SCFR_ENGINE_PERSISTENT_CLUSTER;
+}
 inline int grid_for(int n) { return n <= 0 ? 1 : (n + TPB - 1) / TPB; }
+// Levels whose widest DP has at least this many actions run warp-per-DP
+// (SCFR_WIDE_ACTIONS overrides; large values disable).
+inline const int kWideActions = [] {
+    const char* e = std::getenv("SCFR_WIDE_ACTIONS");
+    return e ? std::atoi(e) : 5;
+}();
 
 // Per-iteration parameters shared by every pass kernel: host-computed
 // schedules indexed by the device iteration counter, the variant's post-op.

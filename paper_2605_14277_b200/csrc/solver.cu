@@ -144,8 +144,12 @@ using LevelKernel = void (*)(Task, Task, KParams);
 // references per DP (long serial chains in a single thread).  Measured on
 // Goofspiel-5: the 5- and 500-DP top levels drop from 8-16 µs to ~5 µs;
 // warp mode on the 24K/432K-DP levels is 2-20x slower than thread mode.
+// Wide levels (>= 5 actions somewhere) also go warp-per-DP: the thread path
+// walks a wide DP's actions as a serial chain of L2 round trips (Liar's dice:
+// 12-way bids, ~15 µs per level launch).
 static bool warp_level(const Player& P, int l) {
-    return P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l];
+    return (P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l]) ||
+           (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
 static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
@@ -991,7 +995,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
         if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
         if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
-        if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_TILED) fail(SCFR_EINVAL, "unknown engine");
+        if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_PERSISTENT_CLUSTER)
+            fail(SCFR_EINVAL, "unknown engine");
         if (cfg->engine == SCFR_ENGINE_PERSISTENT_GRID && cfg->batch != 1)
             fail(SCFR_EINVAL, "the grid-persistent engine runs a single solve (batch 1)");
         int ndev = 0;
@@ -1097,7 +1102,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         } else if (h->engine == SCFR_ENGINE_TILED) {
             prepare_tiled(h.get(), U, UT, true);
         }
-        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID)
+        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID ||
+            h->engine == SCFR_ENGINE_PERSISTENT_CLUSTER)
             prepare_persistent(h.get());
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
@@ -1144,7 +1150,7 @@ int scfr_step(scfr_handle* h, int64_t n) {
         set_device(h);
         add_weights(h, n);
         CUDA_OK(cudaEventRecord(h->ev0, h->stream));
-        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID) {
+        if (is_persistent(h->engine)) {
             h->launches += launch_persistent(h, n);
         } else if (h->use_graph) {
             if (!h->exec) build_graph(h);
@@ -1170,7 +1176,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
         add_weights(h, n);
         std::vector<KernelRecord> recs;
         int64_t issued = 0;
-        if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID) {
+        if (is_persistent(h->engine)) {
             KernelRecord r;
             r.kind = KK_PERSIST;
             r.bytes = persistent_bytes_per_iter(h) * (double)n;

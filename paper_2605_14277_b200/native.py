@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(HERE, "_lib", "libseqcfr_b200.so")
 OK, EINVAL, EGAME, ENONFINITE, ECUDA, ENOMEM, ENCCL = 0, -1, -2, -3, -4, -5, -6
 VARIANT_CODE = {"cfr": 0, "cfr+": 1, "dcfr": 2, "pcfr": 3, "pcfr+": 4}
 MODE_CODE = {"sim": 0, "alt": 1}
-ENGINE_CODE = {"auto": 0, "levels": 1, "persistent": 2, "persistent_grid": 3, "tiled": 4}
+ENGINE_CODE = {"auto": 0, "levels": 1, "persistent": 2, "persistent_grid": 3, "tiled": 4,
+               "persistent_cluster": 5}
 ENGINE_NAME = {v: k for k, v in ENGINE_CODE.items()}
 STATE_CODE = {"regrets": 0, "behavior": 1, "accum": 2, "utility": 3}
 

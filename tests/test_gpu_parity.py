@@ -145,7 +145,7 @@ def test_goofspiel5_full_size_against_oracle(gpu):
         np.testing.assert_allclose(sums, x[p.dp_parent_seq], rtol=0, atol=1e-11)
 
 
-ENGINES = ["levels", "persistent", "persistent_grid"]
+ENGINES = ["levels", "persistent", "persistent_grid", "persistent_cluster"]
 ENGINE_CASES = ["kuhn.cfr.sim.200", "leduc.cfr+.alt.100", "leduc.pcfr+.alt.100",
                 "random6.dcfr.sim.200", "random7.pcfr.alt.40", "liars3.dcfr.alt.60",
                 "goof3.pcfr+.sim.60", "mp.cfr+.alt.50", "liars6.dcfr.alt.30.a1.5.b0.0.g2.0"]
