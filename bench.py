@@ -116,10 +116,10 @@ class ClockSampler:
 
 
 def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: float | None,
-                    threads: int):
+                    threads: int, dtype: str = "f64"):
     """The oracle port on the host cores: iterations/sec over a bounded sample."""
     from oracle.oracle import OracleSolver
-    o = OracleSolver(bundle, variant, threads=threads)
+    o = OracleSolver(bundle, variant, threads=threads, dtype=dtype)
     if warmup:
         o.step(warmup)
     if budget_s is not None:
@@ -234,7 +234,7 @@ def run_ours(args):
         if sharded:  # config 4: one solve, payoff SpMV rows split over the ranks
             from paper_2605_14277_b200.distributed import sharded_solver
             return sharded_solver(bundle, cfg, device=device)
-        return Solver(bundle, cfg, device=device)
+        return Solver(bundle, cfg, device=device, dtype=args.dtype)
 
     # process-level warm-up (CUDA context, lazy module load) outside any timing
     torch.cuda.synchronize(device)
@@ -322,7 +322,7 @@ def run_ours(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated game tree)",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (generated game tree)",
         "config": {"workload": desc, "variant": variant, "mode": cfg.mode, "gamma": cfg.gamma,
                    "seqs_per_player": [p.num_seqs for p in bundle.procs],
                    "nnz_U": bundle.payoff.nnz, "parallelism": (f"row-sharded payoff SpMV + NCCL all-gather x{ws}" if sharded
@@ -350,7 +350,7 @@ def run_ours(args):
     }
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rate, steps, dt = cpu_oracle_rate(bundle, variant, 50, 1, args.cpu_budget, threads)
+        rate, steps, dt = cpu_oracle_rate(bundle, variant, 50, 1, args.cpu_budget, threads, args.dtype)
         line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": threads,
                                 "kind": "port",
                                 "sample": f"{steps} {args.workload} iterations after 1 warm-up, "
@@ -371,6 +371,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="goofspiel5")
+    ap.add_argument("--dtype", choices=("f64", "f32"), default="f64",
+                    help="f64 (default; bit-exact with the reference) or the optional fp32 mode")
     ap.add_argument("--profile-iters", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.0)
     ap.add_argument("--cpu-budget", type=float, default=15.0)

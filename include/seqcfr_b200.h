@@ -62,6 +62,10 @@ extern "C" {
 #define SCFR_MODE_SIM 0
 #define SCFR_MODE_ALT 1
 
+/* Arithmetic of the iteration state (scfr_config.dtype). */
+#define SCFR_DTYPE_F64 0
+#define SCFR_DTYPE_F32 1
+
 /* Node kinds of the input game (pkg/games.py:23-25). */
 #define SCFR_NODE_CHANCE 0
 #define SCFR_NODE_DECISION 1
@@ -155,7 +159,13 @@ typedef struct scfr_config {
     const double* batch_beta;
     const double* batch_gamma;
     int32_t engine;  /* SCFR_ENGINE_* */
-    int32_t reserved[7];
+    /* SCFR_DTYPE_F64 (default; bit-exact with the reference) or
+     * SCFR_DTYPE_F32: iteration state and payoff values in fp32, the same
+     * operation order rounded to fp32 at every step (level engine only).
+     * Reads widen to fp64; exploitability runs in fp64 on the widened
+     * profile. */
+    int32_t dtype;
+    int32_t reserved[6];
 } scfr_config;
 
 typedef struct scfr_handle scfr_handle;
@@ -193,7 +203,11 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out);
 /* The sequence-form strategy emitted by the last iteration (x1/x2 of _step). */
 int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out);
 #define SCFR_STATE_REGRETS 0  /* [num_seqs-1]  RegretState.regrets   */
-#define SCFR_STATE_BEHAVIOR 1 /* [num_seqs-1]  RegretState.behavior  */
+#define SCFR_STATE_BEHAVIOR 1 /* [num_seqs-1]  RegretState.behavior; for non-predictive
+                               * variants the behaviour the NEXT iteration plays (regret
+                               * matching of the current regrets, fused into the observe
+                               * pass; the reference computes the same b at the start of
+                               * the next next_strategy) */
 #define SCFR_STATE_ACCUM 2    /* [num_seqs]    RegretState.avg_accum */
 #define SCFR_STATE_UTILITY 3  /* [num_seqs]    u of the last iteration (the next prediction) */
 int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* host_out);

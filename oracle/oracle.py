@@ -17,8 +17,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "libseqcfr_oracle.so")
+LIB_PATH_F32 = os.path.join(HERE, "_build", "libseqcfr_oracle_f32.so")  # -DREAL=float build
 VARIANTS = {"cfr": 0, "cfr+": 1, "dcfr": 2, "pcfr": 3, "pcfr+": 4}
-_lib = None
+_libs = {}
 
 
 def build() -> str:
@@ -26,12 +27,14 @@ def build() -> str:
     return LIB_PATH
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+def lib(dtype: str = "f64"):
+    """The fp64 restatement, or (dtype "f32") the same source built with
+    float state: the checker of the fp32 mode."""
+    path = LIB_PATH_F32 if dtype in ("f32", "float32") else LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
             build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         P = C.POINTER
         i64p = P(C.c_int64)
         f64p = P(C.c_double)
@@ -48,8 +51,8 @@ def lib():
         L.oc_best_response.restype = C.c_double
         L.oc_spmv.argtypes = [C.c_void_p, C.c_int, f64p, f64p, C.c_int]
         L.oc_free.argtypes = [C.c_void_p]
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 def _i64(a):
@@ -62,7 +65,7 @@ def _ptr(a, t):
 
 class OracleSolver:
     def __init__(self, bundle, variant="cfr", mode=None, alpha=1.5, beta=0.0, gamma=None,
-                 threads: int = 1):
+                 threads: int = 1, dtype: str = "f64"):
         defaults = {"cfr": (0.0, "sim"), "cfr+": (1.0, "alt"), "dcfr": (2.0, "alt"),
                     "pcfr": (0.0, "sim"), "pcfr+": (2.0, "alt")}
         g0, m0 = defaults[variant]
@@ -70,7 +73,8 @@ class OracleSolver:
         self.mode = m0 if mode is None else mode
         self.variant = variant
         self.threads = threads
-        L = lib()
+        self.dtype = dtype
+        L = self._L = lib(dtype)
         p1, p2 = bundle.procs
         keep = []
         arr = lambda *xs: (C.POINTER(C.c_int64) * 2)(*[_ptr(x, C.c_int64) for x in xs])  # noqa: E731
@@ -98,15 +102,15 @@ class OracleSolver:
         self.sizes = (p1.num_seqs, p2.num_seqs)
 
     def step(self, n: int = 1) -> None:
-        lib().oc_step(self._st, int(n))
+        self._L.oc_step(self._st, int(n))
 
     @property
     def t(self) -> int:
-        return int(lib().oc_t(self._st))
+        return int(self._L.oc_t(self._st))
 
     def _read(self, player, which):
         out = np.empty(self.sizes[player - 1])
-        w = lib().oc_read(self._st, player, which, _ptr(out, C.c_double))
+        w = self._L.oc_read(self._st, player, which, _ptr(out, C.c_double))
         return out, w
 
     def regrets(self, player):
@@ -130,7 +134,7 @@ class OracleSolver:
 
     def best_response(self, player, x_opp):
         x = np.ascontiguousarray(x_opp, dtype=np.float64)
-        return float(lib().oc_best_response(self._st, player, _ptr(x, C.c_double)))
+        return float(self._L.oc_best_response(self._st, player, _ptr(x, C.c_double)))
 
     def exploitability(self, x1, x2):
         b1 = self.best_response(1, x2)
@@ -139,5 +143,5 @@ class OracleSolver:
 
     def __del__(self):
         if getattr(self, "_st", None):
-            lib().oc_free(self._st)
+            self._L.oc_free(self._st)
             self._st = None

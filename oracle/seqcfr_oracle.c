@@ -18,6 +18,12 @@
  *   scalar_best_response     pkg/oracle.py:186-221
  * with the exact association order of the reference's matrix/vector path
  * (SURVEY.md §8(a)): compile with -ffp-contract=off; sums are sequential.
+ *
+ * REAL selects the arithmetic of the iteration state: double (default; the
+ * reference's) or float (-DREAL=float, libseqcfr_oracle_f32.so: the fp32
+ * mode's checker: the same operation order with every operation rounded to
+ * fp32, payoffs rounded once to fp32, schedules from fp64 libm pow rounded
+ * once, avg_weight summed in fp64).  Interfaces stay fp64 (widened reads).
  * Thread parallelism (pthreads) is over independent DPs of one depth level
  * and independent SpMV rows (each output written by exactly one thread, like
  * the reference's prange backend), so results are bitwise independent of the
@@ -29,19 +35,25 @@
 #include <string.h>
 #include <pthread.h>
 
+#ifndef REAL
+#define REAL double
+#endif
+typedef REAL real;
+#define RL(v) ((real)(v))
+
 typedef struct {
     int64_t S, J, L;          /* |Σ| (incl. empty), |J|, number of DP levels */
     int64_t *first, *parent;  /* [J+1] action ranges, [J] parent sequence */
     int64_t *clo, *ccnt;      /* [S] child-DP range per sequence */
     int64_t *lvl;             /* [L+1] DP level starts (by process depth) */
-    double *r, *b, *x, *xpost, *avg, *u, *V, *W, *g;
+    real *r, *b, *x, *xpost, *avg, *u, *V, *W, *g;
     double avg_weight;
 } oc_player;
 
 typedef struct {
     int64_t rows, nnz;
     int64_t *indptr, *indices;
-    double* data;
+    real* data;
 } oc_csr;
 
 typedef struct {
@@ -110,19 +122,19 @@ static int build_player(oc_player* P, int64_t num_nodes, int64_t S, int64_t J, c
     P->first[J] = J ? first[J - 1] + nact[J - 1] : 1;
     P->lvl[L] = J;
     P->L = L;
-    P->r = xcalloc(S, 8);
-    P->b = xcalloc(S, 8);
-    P->x = xcalloc(S, 8);
-    P->xpost = xcalloc(S, 8);
-    P->avg = xcalloc(S, 8);
-    P->u = xcalloc(S, 8);
-    P->V = xcalloc(J, 8);
-    P->W = xcalloc(J, 8);
-    P->g = xcalloc(S, 8);
+    P->r = xcalloc(S, sizeof(real));
+    P->b = xcalloc(S, sizeof(real));
+    P->x = xcalloc(S, sizeof(real));
+    P->xpost = xcalloc(S, sizeof(real));
+    P->avg = xcalloc(S, sizeof(real));
+    P->u = xcalloc(S, sizeof(real));
+    P->V = xcalloc(J, sizeof(real));
+    P->W = xcalloc(J, sizeof(real));
+    P->g = xcalloc(S, sizeof(real));
     for (int64_t j = 0; j < J; ++j)
-        for (int64_t s = first[j]; s < first[j] + nact[j]; ++s) P->b[s] = 1.0 / (double)nact[j];
-    P->x[0] = 1.0;
-    P->xpost[0] = 1.0;
+        for (int64_t s = first[j]; s < first[j] + nact[j]; ++s) P->b[s] = RL(1.0) / (real)nact[j];
+    P->x[0] = RL(1.0);
+    P->xpost[0] = RL(1.0);
     P->avg_weight = 0.0;
     return 0;
 }
@@ -133,110 +145,111 @@ static void copy_csr(oc_csr* M, int64_t rows, int64_t nnz, const int64_t* ip, co
     M->nnz = nnz;
     M->indptr = xcalloc(rows + 1, 8);
     M->indices = xcalloc(nnz, 8);
-    M->data = xcalloc(nnz, 8);
+    M->data = xcalloc(nnz, sizeof(real));
     memcpy(M->indptr, ip, (rows + 1) * 8);
     if (nnz) {
         memcpy(M->indices, ix, nnz * 8);
-        memcpy(M->data, d, nnz * 8);
+        for (int64_t k = 0; k < nnz; ++k) M->data[k] = (real)d[k]; /* rounded once */
     }
 }
 
 /* pkg/kernels.py:148-154 (+ backend.scale(-1.0, .) when neg). */
-typedef struct { const oc_csr* M; const double* x; double* out; int neg; } spmv_ctx;
+typedef struct { const oc_csr* M; const real* x; real* out; int neg; } spmv_ctx;
 static void spmv_rows(void* p, int64_t lo, int64_t hi) {
     const spmv_ctx* c = (const spmv_ctx*)p;
     const oc_csr* M = c->M;
     for (int64_t i = lo; i < hi; ++i) {
-        double acc = 0.0;
+        real acc = RL(0.0);
         for (int64_t k = M->indptr[i]; k < M->indptr[i + 1]; ++k) acc += M->data[k] * c->x[M->indices[k]];
-        c->out[i] = c->neg ? -1.0 * acc : acc;
+        c->out[i] = c->neg ? RL(-1.0) * acc : acc;
     }
 }
-static void spmv(const oc_csr* M, const double* x, double* out, int neg, int threads) {
+static void spmv(const oc_csr* M, const real* x, real* out, int neg, int threads) {
     spmv_ctx c = {M, x, out, neg};
     parfor(0, M->rows, threads, 1 << 14, spmv_rows, &c);
 }
 
-static double child_sum(const oc_player* P, int64_t s, const double* V) {
+static real child_sum(const oc_player* P, int64_t s, const real* V) {
     const int64_t c = P->ccnt[s], lo = P->clo[s];
-    if (c == 0) return 0.0;
+    if (c == 0) return RL(0.0);
     if (c == 1) return V[lo];
-    double acc = 0.0;
+    real acc = RL(0.0);
     for (int64_t k = 0; k < c; ++k) acc += V[lo + k];
     return acc;
 }
 
-static double qval(const oc_player* P, const double* u, int64_t s) {
-    return (0.0 + u[s]) + child_sum(P, s, P->V);
+static real qval(const oc_player* P, const real* u, int64_t s) {
+    return (RL(0.0) + u[s]) + child_sum(P, s, P->V);
 }
 
 /* observe (pkg/solvers.py:178-207) + floor (:210-214) / discount (:217-224). */
-typedef struct { oc_player* P; const double* u; int post; double pf, nf; } obs_ctx;
+typedef struct { oc_player* P; const real* u; int post; real pf, nf; } obs_ctx;
 static void observe_range(void* p, int64_t lo, int64_t hi) {
     const obs_ctx* c = (const obs_ctx*)p;
     oc_player* P = c->P;
-    const double* u = c->u;
+    const real* u = c->u;
     const int post = c->post;
-    const double pf = c->pf, nf = c->nf;
+    const real pf = c->pf, nf = c->nf;
     {
         for (int64_t j = lo; j < hi; ++j) {
             const int64_t s0 = P->first[j], s1 = P->first[j + 1];
-            double E = 0.0;
+            real E = RL(0.0);
             for (int64_t s = s0; s < s1; ++s) E += P->b[s] * qval(P, u, s);
             P->V[j] = E;
-            const double negE = -1.0 * (0.0 + E);
+            const real negE = RL(-1.0) * (RL(0.0) + E);
             for (int64_t s = s0; s < s1; ++s) {
-                double rv = P->r[s] + (negE + qval(P, u, s));
-                if (post == 1) rv = rv > 0.0 ? rv : 0.0;
-                else if (post == 2) rv = rv > 0.0 ? rv * pf : (rv < 0.0 ? rv * nf : rv);
+                real rv = P->r[s] + (negE + qval(P, u, s));
+                if (post == 1) rv = rv > RL(0.0) ? rv : RL(0.0);
+                else if (post == 2) rv = rv > RL(0.0) ? rv * pf : (rv < RL(0.0) ? rv * nf : rv);
                 P->r[s] = rv;
             }
         }
     }
 }
-static void observe(oc_player* P, const double* u, int post, double pf, double nf, int threads) {
-    obs_ctx c = {P, u, post, pf, nf};
+static void observe(oc_player* P, const real* u, int post, double pf, double nf, int threads) {
+    obs_ctx c = {P, u, post, (real)pf, (real)nf}; /* schedule factors rounded once */
     for (int64_t l = P->L - 1; l >= 0; --l) parfor(P->lvl[l], P->lvl[l + 1], threads, 1 << 13, observe_range, &c);
 }
 
-static void regret_match(const double* r, double* b, int64_t s0, int64_t s1) {
-    double S = 0.0;
-    for (int64_t s = s0; s < s1; ++s) S += r[s] > 0.0 ? r[s] : 0.0;
+static void regret_match(const real* r, real* b, int64_t s0, int64_t s1) {
+    real S = RL(0.0);
+    for (int64_t s = s0; s < s1; ++s) S += r[s] > RL(0.0) ? r[s] : RL(0.0);
     for (int64_t s = s0; s < s1; ++s) {
-        const double p = r[s] > 0.0 ? r[s] : 0.0;
-        b[s] = S != 0.0 ? p / S : 1.0 / (double)(s1 - s0);
+        const real p = r[s] > RL(0.0) ? r[s] : RL(0.0);
+        b[s] = S != RL(0.0) ? p / S : RL(1.0) / (real)(s1 - s0);
     }
 }
 
 /* next_strategy (pkg/solvers.py:143-175): RM into b, TD into x, avg += w x.
  * current_strategy (:270-291) when b_out is a scratch and w < 0 (no avg). */
-typedef struct { oc_player* P; const double* r; double* b_out; double* x; double w; } next_ctx;
+typedef struct { oc_player* P; const real* r; real* b_out; real* x; real w; int avg; } next_ctx;
 static void next_range(void* p, int64_t lo, int64_t hi) {
     const next_ctx* c = (const next_ctx*)p;
     oc_player* P = c->P;
-    const double* r = c->r;
-    double* b_out = c->b_out;
-    double* x = c->x;
-    const double w = c->w;
+    const real* r = c->r;
+    real* b_out = c->b_out;
+    real* x = c->x;
+    const real w = c->w;
     {
         for (int64_t j = lo; j < hi; ++j) {
             const int64_t s0 = P->first[j], s1 = P->first[j + 1];
             regret_match(r, b_out, s0, s1);
-            const double xp = x[P->parent[j]];
+            const real xp = x[P->parent[j]];
             for (int64_t s = s0; s < s1; ++s) {
-                const double xa = b_out[s] * xp;
+                const real xa = b_out[s] * xp;
                 x[s] = xa;
-                if (w >= 0.0) P->avg[s] = w * xa + P->avg[s];
+                if (c->avg) P->avg[s] = w * xa + P->avg[s];
             }
         }
     }
 }
-static void next_strategy(oc_player* P, const double* r, double* b_out, double* x, double w,
+/* w < 0: no average (current_strategy).  avg_weight sums the fp64 w. */
+static void next_strategy(oc_player* P, const real* r, real* b_out, real* x, double w,
                           int threads) {
-    next_ctx c = {P, r, b_out, x, w};
+    next_ctx c = {P, r, b_out, x, (real)w, w >= 0.0};
     for (int64_t l = 0; l < P->L; ++l) parfor(P->lvl[l], P->lvl[l + 1], threads, 1 << 13, next_range, &c);
     if (w >= 0.0) {
-        P->avg[0] = w * x[0] + P->avg[0]; /* the axpy covers the empty sequence too */
+        P->avg[0] = (real)w * x[0] + P->avg[0]; /* the axpy covers the empty sequence too */
         P->avg_weight += w;
     }
 }
@@ -247,7 +260,7 @@ static double factor(int64_t t, double e) {
     return p / (p + 1.0);
 }
 
-static void variant_observe(oc_state* st, oc_player* P, const double* u) {
+static void variant_observe(oc_state* st, oc_player* P, const real* u) {
     int post = 0;
     double pf = 1.0, nf = 1.0;
     if (st->variant == 1 || st->variant == 4) post = 1;
@@ -261,11 +274,11 @@ static void variant_observe(oc_state* st, oc_player* P, const double* u) {
 
 /* variant_next (pkg/solvers.py:248-256); predictive = snapshot / observe(m)
  * with the previous behaviour / next_strategy / restore (:227-245). */
-static void variant_next(oc_state* st, oc_player* P, double* scratch_r) {
+static void variant_next(oc_state* st, oc_player* P, real* scratch_r) {
     const double w = pow((double)st->t, st->gamma);
     if (st->variant == 3 || st->variant == 4) {
-        memcpy(scratch_r, P->r, P->S * 8);
-        double* keep = P->r;
+        memcpy(scratch_r, P->r, P->S * sizeof(real));
+        real* keep = P->r;
         P->r = scratch_r;
         observe(P, P->u, st->variant == 4 ? 1 : 0, 1.0, 1.0, st->threads);
         next_strategy(P, P->r, P->b, P->x, w, st->threads);
@@ -305,8 +318,8 @@ oc_state* oc_create(const int64_t* nn, const int64_t* ns, const int64_t* nj,
 void oc_step(oc_state* st, int64_t n) {
     oc_player *A = &st->p[0], *B = &st->p[1];
     int64_t smax = A->S > B->S ? A->S : B->S;
-    double* scratch = xcalloc(smax, 8);
-    double* peek = xcalloc(A->S, 8);
+    real* scratch = xcalloc(smax, sizeof(real));
+    real* peek = xcalloc(A->S, sizeof(real));
     for (int64_t it = 0; it < n; ++it) {
         variant_next(st, A, scratch);
         variant_next(st, B, scratch);
@@ -330,9 +343,9 @@ void oc_step(oc_state* st, int64_t n) {
  * 5 xpost.  Returns the avg weight. */
 double oc_read(const oc_state* st, int player, int which, double* out) {
     const oc_player* P = &st->p[player - 1];
-    const double* src = which == 0 ? P->r : which == 1 ? P->b : which == 2 ? P->avg
-                      : which == 3 ? P->u : which == 4 ? P->x : P->xpost;
-    memcpy(out, src, P->S * 8);
+    const real* src = which == 0 ? P->r : which == 1 ? P->b : which == 2 ? P->avg
+                    : which == 3 ? P->u : which == 4 ? P->x : P->xpost;
+    for (int64_t s = 0; s < P->S; ++s) out[s] = (double)src[s]; /* exact widening */
     return P->avg_weight;
 }
 
@@ -340,14 +353,22 @@ int64_t oc_t(const oc_state* st) { return st->t; }
 
 /* g = U x (player 1) or -Uᵀ x (player 2), then scalar_best_response
  * (pkg/oracle.py:186-221) per DP, deepest level first. */
+static real* to_real(const double* x, int64_t n) {
+    real* r = xcalloc(n, sizeof(real));
+    for (int64_t i = 0; i < n; ++i) r[i] = (real)x[i];
+    return r;
+}
+
 double oc_best_response(oc_state* st, int player, const double* x_opp) {
     oc_player* P = &st->p[player - 1];
-    spmv(player == 1 ? &st->U : &st->UT, x_opp, P->g, player == 2, st->threads);
+    real* xo = to_real(x_opp, st->p[2 - player].S);
+    spmv(player == 1 ? &st->U : &st->UT, xo, P->g, player == 2, st->threads);
+    free(xo);
     for (int64_t l = P->L - 1; l >= 0; --l)
         for (int64_t j = P->lvl[l]; j < P->lvl[l + 1]; ++j) {
-            double best = -INFINITY;
+            real best = -INFINITY;
             for (int64_t s = P->first[j]; s < P->first[j + 1]; ++s) {
-                const double v = P->g[s] + child_sum(P, s, P->W);
+                const real v = P->g[s] + child_sum(P, s, P->W);
                 if (v > best) best = v;
             }
             P->W[j] = best;
@@ -356,7 +377,13 @@ double oc_best_response(oc_state* st, int player, const double* x_opp) {
 }
 
 void oc_spmv(oc_state* st, int transposed, const double* x, double* out, int neg) {
-    spmv(transposed ? &st->UT : &st->U, x, out, neg, st->threads);
+    const oc_csr* M = transposed ? &st->UT : &st->U;
+    real* xr = to_real(x, transposed ? st->p[0].S : st->p[1].S);
+    real* o = xcalloc(M->rows, sizeof(real));
+    spmv(M, xr, o, neg, st->threads);
+    for (int64_t i = 0; i < M->rows; ++i) out[i] = (double)o[i];
+    free(xr);
+    free(o);
 }
 
 void oc_free(oc_state* st) {

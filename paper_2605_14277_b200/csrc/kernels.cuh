@@ -44,18 +44,25 @@ struct DevTree {
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// fp32 mode: the same operation sequence, every operation rounded to fp32
+// (no FMA contraction either way; the fp32 oracle restates it op for op).
+__device__ __forceinline__ float dadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float dmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float ddiv(float a, float b) { return __fdiv_rn(a, b); }
 
 // kChunk: child loads a lane keeps in flight in the warp-per-DP variants
 // (deep for HBM/L2 latency, shallow for shared memory).
 struct LdL1 {
     static constexpr int kChunk = 32;
-    static __device__ __forceinline__ double ld(const double* p) { return *p; }
+    template <class V>
+    static __device__ __forceinline__ V ld(const V* p) { return *p; }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
 struct LdL2 {
     static constexpr int kChunk = 32;
-    static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+    template <class V>
+    static __device__ __forceinline__ V ld(const V* p) { return __ldcg(p); }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
@@ -63,19 +70,27 @@ struct LdL2 {
 // shares a kernel (and so a register budget) with the tile walk.
 struct LdL2s {
     static constexpr int kChunk = 8;
-    static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+    template <class V>
+    static __device__ __forceinline__ V ld(const V* p) { return __ldcg(p); }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
 // Shared-memory resident state and structure (CTA-resident small-game engine).
 struct LdS {
     static constexpr int kChunk = 8;
-    static __device__ __forceinline__ double ld(const double* p) { return *p; }
+    template <class V>
+    static __device__ __forceinline__ V ld(const V* p) { return *p; }
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return *p; }
 };
 
 enum : int { POST_NONE = 0, POST_PLUS = 1, POST_DCFR = 2 };
+
+// Non-deduced context: scalars and optional pointers take the state's type.
+template <class T>
+struct nd {
+    using type = T;
+};
 
 template <class Ld>
 __device__ __forceinline__ void dp_range(const DevTree& T, int j, int& s0, int& n) {
@@ -103,38 +118,38 @@ __device__ __forceinline__ int parent_of(const DevTree& T, int j) {
 //   end node: 0.0 (the zero-initialised v); one DP: V of that DP;
 //   observation point: ((0.0 + V_lo) + V_lo+1) + ... in j order
 // (pkg/solvers.py:195-199, pkg/oracle.py:91-95).
-template <class Ld>
-__device__ __forceinline__ double child_value(int2 c, double v0, const double* __restrict__ V) {
-    if (c.y == 0) return 0.0;
+template <class Ld, class R>
+__device__ __forceinline__ R child_value(int2 c, R v0, const R* __restrict__ V) {
+    if (c.y == 0) return R(0);
     if (c.y == 1) return v0;
-    double acc = dadd(0.0, v0);
+    R acc = dadd(R(0), v0);
     int k = 1;
     for (; k + 4 <= c.y; k += 4) {  // loads first, adds in order
-        const double a0 = Ld::ld(V + c.x + k), a1 = Ld::ld(V + c.x + k + 1);
-        const double a2 = Ld::ld(V + c.x + k + 2), a3 = Ld::ld(V + c.x + k + 3);
+        const R a0 = Ld::ld(V + c.x + k), a1 = Ld::ld(V + c.x + k + 1);
+        const R a2 = Ld::ld(V + c.x + k + 2), a3 = Ld::ld(V + c.x + k + 3);
         acc = dadd(dadd(dadd(dadd(acc, a0), a1), a2), a3);
     }
     for (; k < c.y; ++k) acc = dadd(acc, Ld::ld(V + c.x + k));
     return acc;
 }
 
-template <class Ld>
-__device__ __forceinline__ double child_sum(int2 c, const double* __restrict__ V) {
-    return child_value<Ld>(c, c.y > 0 ? Ld::ld(V + c.x) : 0.0, V);
+template <class Ld, class R>
+__device__ __forceinline__ R child_sum(int2 c, const R* __restrict__ V) {
+    return child_value<Ld>(c, c.y > 0 ? Ld::ld(V + c.x) : R(0), V);
 }
 
 // Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
-template <class Ld>
-__device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,
+template <class Ld, class R>
+__device__ __forceinline__ R spmv_row(const int* __restrict__ indptr,
                                            const int* __restrict__ indices,
-                                           const double* __restrict__ data,
-                                           const double* __restrict__ x, int row) {
+                                           const R* __restrict__ data,
+                                           const R* __restrict__ x, int row) {
     const int k0 = __ldg(indptr + row), k1 = __ldg(indptr + row + 1);
-    double acc = 0.0;
+    R acc = R(0);
     int k = k0;
     for (; k + 2 <= k1; k += 2) {
-        const double d0 = __ldg(data + k), d1 = __ldg(data + k + 1);
-        const double x0 = Ld::ld(x + __ldg(indices + k)), x1 = Ld::ld(x + __ldg(indices + k + 1));
+        const R d0 = __ldg(data + k), d1 = __ldg(data + k + 1);
+        const R x0 = Ld::ld(x + __ldg(indices + k)), x1 = Ld::ld(x + __ldg(indices + k + 1));
         acc = dadd(dadd(acc, dmul(d0, x0)), dmul(d1, x1));
     }
     if (k < k1) acc = dadd(acc, dmul(__ldg(data + k), Ld::ld(x + __ldg(indices + k))));
@@ -145,18 +160,20 @@ __device__ __forceinline__ double spmv_row(const int* __restrict__ indptr,
 // the utility of sequence s is computed here as row s of M applied to the
 // opponent's strategy x (scaled by -1 for player 2, pkg/solvers.py:359,368),
 // stored to u[s] (it is the next iteration's prediction), and used directly.
-struct FuseU {
+template <class R>
+struct FuseUT {
     const int* ip;
     const int* ix;
-    const double* d;
-    const double* x;
+    const R* d;
+    const R* x;
     int neg;
 };
+using FuseU = FuseUT<double>;
 
-template <class Ld>
-__device__ __forceinline__ double fused_u(const FuseU& f, double* u, int s, bool& bad) {
-    double v = spmv_row<Ld>(f.ip, f.ix, f.d, f.x, s);
-    if (f.neg) v = dmul(-1.0, v);
+template <class Ld, class R>
+__device__ __forceinline__ R fused_u(const FuseUT<R>& f, R* u, int s, bool& bad) {
+    R v = spmv_row<Ld>(f.ip, f.ix, f.d, f.x, s);
+    if (f.neg) v = dmul(R(-1), v);
     bad |= !isfinite(v);
     u[s] = v;
     return v;
@@ -165,44 +182,46 @@ __device__ __forceinline__ double fused_u(const FuseU& f, double* u, int s, bool
 // q[a] = (0.0 + u[s0+a]) + C_{s0+a} for a < n <= MAXA, all loads issued
 // before the dependent adds ((w + v)[node(s)] read back through Bᵀ,
 // pkg/solvers.py:192-202).
-template <int MAXA, class Ld>
-__device__ __forceinline__ void load_q(const DevTree& T, const double* __restrict__ u,
-                                       const double* __restrict__ V, int s0, int n,
-                                       double (&q)[MAXA], const FuseU f = FuseU{},
+template <int MAXA, class Ld, class R>
+__device__ __forceinline__ void load_q(const DevTree& T, const R* __restrict__ u,
+                                       const R* __restrict__ V, int s0, int n,
+                                       R (&q)[MAXA], const FuseUT<R> f = FuseUT<R>{},
                                        bool* bad = nullptr) {
     int2 c[MAXA];
-    double uu[MAXA], v0[MAXA];
+    R uu[MAXA], v0[MAXA];
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
         if (a < n) {
             c[a] = child_of<Ld>(T, s0 + a);
-            uu[a] = f.ip ? fused_u<Ld>(f, const_cast<double*>(u), s0 + a, *bad) : Ld::ld(u + s0 + a);
+            uu[a] = f.ip ? fused_u<Ld>(f, const_cast<R*>(u), s0 + a, *bad) : Ld::ld(u + s0 + a);
         }
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
-        if (a < n) v0[a] = c[a].y > 0 ? Ld::ld(V + c[a].x) : 0.0;
+        if (a < n) v0[a] = c[a].y > 0 ? Ld::ld(V + c[a].x) : R(0);
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
-        if (a < n) q[a] = dadd(dadd(0.0, uu[a]), child_value<Ld>(c[a], v0[a], V));
+        if (a < n) q[a] = dadd(dadd(R(0), uu[a]), child_value<Ld>(c[a], v0[a], V));
 }
 
-template <class Ld>
-__device__ __forceinline__ double qval(const DevTree& T, const double* __restrict__ u,
-                                       const double* __restrict__ V, int s) {
-    return dadd(dadd(0.0, Ld::ld(u + s)), child_sum<Ld>(child_of<Ld>(T, s), V));
+template <class Ld, class R>
+__device__ __forceinline__ R qval(const DevTree& T, const R* __restrict__ u,
+                                       const R* __restrict__ V, int s) {
+    return dadd(dadd(R(0), Ld::ld(u + s)), child_sum<Ld>(child_of<Ld>(T, s), V));
 }
 
-__device__ __forceinline__ double post_op(double rv, int post, double pf, double nf) {
-    if (post == POST_PLUS) return rv > 0.0 ? rv : 0.0;
-    if (post == POST_DCFR) return rv > 0.0 ? dmul(rv, pf) : (rv < 0.0 ? dmul(rv, nf) : rv);
+template <class R>
+__device__ __forceinline__ R post_op(R rv, int post, R pf, R nf) {
+    if (post == POST_PLUS) return rv > R(0) ? rv : R(0);
+    if (post == POST_DCFR) return rv > R(0) ? dmul(rv, pf) : (rv < R(0) ? dmul(rv, nf) : rv);
     return rv;
 }
 
 // Regret matching of one block (pkg/solvers.py:156-160): positive part,
 // sequential sum from 0.0, IEEE division, uniform 1.0/n fallback.
-__device__ __forceinline__ double rm_prob(double rv, double S, int n) {
-    const double p = rv > 0.0 ? rv : 0.0;
-    return S != 0.0 ? ddiv(p, S) : ddiv(1.0, (double)n);
+template <class R>
+__device__ __forceinline__ R rm_prob(R rv, R S, int n) {
+    const R p = rv > R(0) ? rv : R(0);
+    return S != R(0) ? ddiv(p, S) : ddiv(R(1), R(n));
 }
 
 
@@ -221,24 +240,24 @@ __device__ __forceinline__ double rm_prob(double rv, double S, int n) {
 // matching of the updated regrets into b for the next iteration).
 // pkg/solvers.py:178-224 and :143-160, fused per decision point.
 // MAXA: actions held in registers; wider DPs take the generic (recompute) path.
-template <int MAXA, class Ld>
-__device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __restrict__ u,
-                                       double* __restrict__ r, double* __restrict__ b,
-                                       double* __restrict__ V, int post, double pf, double nf,
-                                       bool do_rm, int* nonfinite, FuseU fuse = FuseU{}) {
+template <int MAXA, class Ld, class R>
+__device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restrict__ u,
+                                       R* __restrict__ r, R* __restrict__ b,
+                                       R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
+                                       bool do_rm, int* nonfinite, FuseUT<R> fuse = FuseUT<R>{}) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     bool bad = false;
     if (T.un == 1) {  // single-action level: r and b are constants (see single_action_note)
-        const double uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<double*>(u), s0, bad) : Ld::ld(u + s0);
-        const double q = dadd(dadd(0.0, uu), child_sum<Ld>(child_of<Ld>(T, s0), V));
-        V[j] = dadd(0.0, dmul(1.0, q));
+        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s0, bad) : Ld::ld(u + s0);
+        const R q = dadd(dadd(R(0), uu), child_sum<Ld>(child_of<Ld>(T, s0), V));
+        V[j] = dadd(R(0), dmul(R(1), q));
         bad |= !isfinite(q);
         if (bad) atomicOr(nonfinite, 1);
         return;
     }
     if (n <= MAXA) {
-        double q[MAXA], bb[MAXA], rr[MAXA];
+        R q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, u, V, s0, n, q, fuse, &bad);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
@@ -246,22 +265,22 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
                 bb[a] = Ld::ld(b + s0 + a);
                 rr[a] = Ld::ld(r + s0 + a);
             }
-        double E = 0.0;
+        R E = R(0);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) E = dadd(E, dmul(bb[a], q[a]));
         V[j] = E;
-        const double negE = dmul(-1.0, dadd(0.0, E));
-        double S = 0.0;
+        const R negE = dmul(R(-1), dadd(R(0), E));
+        R S = R(0);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) {
                 bad |= !isfinite(q[a]);
-                const double rv = post_op(dadd(rr[a], dadd(negE, q[a])), post, pf, nf);
+                const R rv = post_op(dadd(rr[a], dadd(negE, q[a])), post, pf, nf);
                 bad |= !isfinite(rv);
                 rr[a] = rv;
                 r[s0 + a] = rv;
-                S = dadd(S, rv > 0.0 ? rv : 0.0);
+                S = dadd(S, rv > R(0) ? rv : R(0));
             }
         if (do_rm) {
 #pragma unroll
@@ -270,19 +289,19 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
         }
     } else {
         if (fuse.ip)  // wide DP: materialise u first, then the generic path re-reads it
-            for (int s = s0; s < s0 + n; ++s) fused_u<Ld>(fuse, const_cast<double*>(u), s, bad);
-        double E = 0.0;
+            for (int s = s0; s < s0 + n; ++s) fused_u<Ld>(fuse, const_cast<R*>(u), s, bad);
+        R E = R(0);
         for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, u, V, s)));
         V[j] = E;
-        const double negE = dmul(-1.0, dadd(0.0, E));
-        double S = 0.0;
+        const R negE = dmul(R(-1), dadd(R(0), E));
+        R S = R(0);
         for (int s = s0; s < s0 + n; ++s) {
-            const double q = qval<Ld>(T, u, V, s);
+            const R q = qval<Ld>(T, u, V, s);
             bad |= !isfinite(q);
-            const double rv = post_op(dadd(Ld::ld(r + s), dadd(negE, q)), post, pf, nf);
+            const R rv = post_op(dadd(Ld::ld(r + s), dadd(negE, q)), post, pf, nf);
             bad |= !isfinite(rv);
             r[s] = rv;
-            S = dadd(S, rv > 0.0 ? rv : 0.0);
+            S = dadd(S, rv > R(0) ? rv : R(0));
         }
         if (do_rm)
             for (int s = s0; s < s0 + n; ++s) b[s] = rm_prob(Ld::ld(r + s), S, n);
@@ -294,19 +313,19 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const double* __
 // plus, regret-match the predicted regrets into b; r itself is untouched
 // (the snapshot/restore of pkg/solvers.py:227-245 without the copy).
 // MAXA: actions held in registers; wider DPs take the generic (recompute) path.
-template <int MAXA, class Ld>
-__device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* __restrict__ m,
-                                        const double* __restrict__ r, double* __restrict__ b,
-                                        double* __restrict__ V, bool plus) {
+template <int MAXA, class Ld, class R>
+__device__ __forceinline__ void pred_dp(const DevTree& T, int j, const R* __restrict__ m,
+                                        const R* __restrict__ r, R* __restrict__ b,
+                                        R* __restrict__ V, bool plus) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
-    if (T.un == 1) {  // single-action level: b stays 1.0 (see single_action_note)
-        const double q = dadd(dadd(0.0, Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), V));
-        V[j] = dadd(0.0, dmul(1.0, q));
+    if (T.un == 1) {  // single-action level: b stays R(1) (see single_action_note)
+        const R q = dadd(dadd(R(0), Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), V));
+        V[j] = dadd(R(0), dmul(R(1), q));
         return;
     }
     if (n <= MAXA) {
-        double q[MAXA], bb[MAXA], rr[MAXA];
+        R q[MAXA], bb[MAXA], rr[MAXA];
         load_q<MAXA, Ld>(T, m, V, s0, n, q);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
@@ -314,38 +333,38 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* _
                 bb[a] = Ld::ld(b + s0 + a);
                 rr[a] = Ld::ld(r + s0 + a);
             }
-        double E = 0.0;
+        R E = R(0);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) E = dadd(E, dmul(bb[a], q[a]));
         V[j] = E;
-        const double negE = dmul(-1.0, dadd(0.0, E));
-        double S = 0.0;
+        const R negE = dmul(R(-1), dadd(R(0), E));
+        R S = R(0);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) {
-                double rv = dadd(rr[a], dadd(negE, q[a]));
-                if (plus) rv = rv > 0.0 ? rv : 0.0;
+                R rv = dadd(rr[a], dadd(negE, q[a]));
+                if (plus) rv = rv > R(0) ? rv : R(0);
                 rr[a] = rv;
-                S = dadd(S, rv > 0.0 ? rv : 0.0);
+                S = dadd(S, rv > R(0) ? rv : R(0));
             }
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
     } else {
-        double E = 0.0;
+        R E = R(0);
         for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, m, V, s)));
         V[j] = E;
-        const double negE = dmul(-1.0, dadd(0.0, E));
-        double S = 0.0;
+        const R negE = dmul(R(-1), dadd(R(0), E));
+        R S = R(0);
         for (int s = s0; s < s0 + n; ++s) {
-            double rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
-            if (plus) rv = rv > 0.0 ? rv : 0.0;
-            S = dadd(S, rv > 0.0 ? rv : 0.0);
+            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            if (plus) rv = rv > R(0) ? rv : R(0);
+            S = dadd(S, rv > R(0) ? rv : R(0));
         }
         for (int s = s0; s < s0 + n; ++s) {
-            double rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
-            if (plus) rv = rv > 0.0 ? rv : 0.0;
+            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            if (plus) rv = rv > R(0) ? rv : R(0);
             b[s] = rm_prob(rv, S, n);
         }
     }
@@ -353,22 +372,22 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const double* _
 
 // TD: x[(j,a)] = b[(j,a)] * x[parent(j)] (pkg/solvers.py:163-170), with the
 // fused average update avg = w*x + avg (pkg/solvers.py:172-174).
-template <class Ld>
-__device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __restrict__ b,
-                                      double* __restrict__ x, double* __restrict__ avg,
-                                      double w) {
+template <class Ld, class R>
+__device__ __forceinline__ void td_dp(const DevTree& T, int j, const R* __restrict__ b,
+                                      R* __restrict__ x, typename nd<R>::type* __restrict__ avg,
+                                      typename nd<R>::type w) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     const int s1 = s0 + n;
-    const double xp = Ld::ld(x + parent_of<Ld>(T, j));
-    if (T.un == 1) {  // single-action level: b == 1.0, so x = 1.0 * xp (single_action_note)
-        const double xa = dmul(1.0, xp);
+    const R xp = Ld::ld(x + parent_of<Ld>(T, j));
+    if (T.un == 1) {  // single-action level: b == R(1), so x = R(1) * xp (single_action_note)
+        const R xa = dmul(R(1), xp);
         x[s0] = xa;
         if (avg) avg[s0] = dadd(dmul(w, xa), Ld::ld(avg + s0));
         return;
     }
     for (int s = s0; s < s1; ++s) {
-        const double xa = dmul(Ld::ld(b + s), xp);
+        const R xa = dmul(Ld::ld(b + s), xp);
         x[s] = xa;
         if (avg) avg[s] = dadd(dmul(w, xa), Ld::ld(avg + s));
     }
@@ -377,33 +396,33 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const double* __r
 // CUR: side-effect-free current strategy (pkg/solvers.py:270-291): regret
 // matching on the fly, then the top-down product into x.
 // MAXA: actions held in registers; wider DPs take the generic (recompute) path.
-template <int MAXA, class Ld>
-__device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __restrict__ r,
-                                       double* __restrict__ x) {
+template <int MAXA, class Ld, class R>
+__device__ __forceinline__ void cur_dp(const DevTree& T, int j, const R* __restrict__ r,
+                                       R* __restrict__ x) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
-    const double xp = Ld::ld(x + parent_of<Ld>(T, j));
-    if (T.un == 1) {  // single-action level: r == +0.0, RM gives 1.0 (single_action_note)
-        x[s0] = dmul(1.0, xp);
+    const R xp = Ld::ld(x + parent_of<Ld>(T, j));
+    if (T.un == 1) {  // single-action level: r == +R(0), RM gives R(1) (single_action_note)
+        x[s0] = dmul(R(1), xp);
         return;
     }
     if (n <= MAXA) {
-        double rr[MAXA];
+        R rr[MAXA];
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) rr[a] = Ld::ld(r + s0 + a);
-        double S = 0.0;
+        R S = R(0);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
-            if (a < n) S = dadd(S, rr[a] > 0.0 ? rr[a] : 0.0);
+            if (a < n) S = dadd(S, rr[a] > R(0) ? rr[a] : R(0));
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) x[s0 + a] = dmul(rm_prob(rr[a], S, n), xp);
     } else {
-        double S = 0.0;
+        R S = R(0);
         for (int s = s0; s < s0 + n; ++s) {
-            const double v = Ld::ld(r + s);
-            S = dadd(S, v > 0.0 ? v : 0.0);
+            const R v = Ld::ld(r + s);
+            S = dadd(S, v > R(0) ? v : R(0));
         }
         for (int s = s0; s < s0 + n; ++s) x[s] = dmul(rm_prob(Ld::ld(r + s), S, n), xp);
     }
@@ -411,15 +430,15 @@ __device__ __forceinline__ void cur_dp(const DevTree& T, int j, const double* __
 
 // BR: best response to gradient g (pkg/oracle.py:186-221): strict '>' from
 // -inf in action order; value g + C_s with C_s the child sum as above.
-template <class Ld>
-__device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __restrict__ g,
-                                      double* __restrict__ W) {
+template <class Ld, class R>
+__device__ __forceinline__ void br_dp(const DevTree& T, int j, const R* __restrict__ g,
+                                      R* __restrict__ W) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     const int s1 = s0 + n;
-    double best = -INFINITY;
+    R best = R(-INFINITY);
     for (int s = s0; s < s1; ++s) {
-        const double v = dadd(Ld::ld(g + s), child_sum<Ld>(child_of<Ld>(T, s), W));
+        const R v = dadd(Ld::ld(g + s), child_sum<Ld>(child_of<Ld>(T, s), W));
         if (v > best) best = v;
     }
     W[j] = best;
@@ -436,14 +455,14 @@ __device__ __forceinline__ void br_dp(const DevTree& T, int j, const double* __r
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
-template <class Ld>
-__device__ __forceinline__ double lane_child_value(int2 c, const double* __restrict__ V) {
-    if (c.y == 0) return 0.0;
+template <class Ld, class R>
+__device__ __forceinline__ R lane_child_value(int2 c, const R* __restrict__ V) {
+    if (c.y == 0) return R(0);
     if (c.y == 1) return Ld::ld(V + c.x);
     constexpr int CH = Ld::kChunk;
-    double acc = 0.0;
+    R acc = R(0);
     for (int base = 0; base < c.y; base += CH) {
-        double vv[CH];
+        R vv[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k)
             if (base + k < c.y) vv[k] = Ld::ld(V + c.x + base + k);
@@ -455,94 +474,95 @@ __device__ __forceinline__ double lane_child_value(int2 c, const double* __restr
 }
 
 // Sequential sum over lanes 0..n-1 of v: ((0.0 + v0) + v1) + ...
-__device__ __forceinline__ double lane_seq_sum(double v, int n) {
-    double acc = 0.0;
+template <class R>
+__device__ __forceinline__ R lane_seq_sum(R v, int n) {
+    R acc = R(0);
     for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, a));
     return acc;
 }
 
-template <class Ld>
-__device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const double* __restrict__ u,
-                                            double* __restrict__ r, double* __restrict__ b,
-                                            double* __restrict__ V, int post, double pf, double nf,
+template <class Ld, class R>
+__device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __restrict__ u,
+                                            R* __restrict__ r, R* __restrict__ b,
+                                            R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
                                             bool do_rm, int* nonfinite, int lane,
-                                            FuseU fuse = FuseU{}) {
+                                            FuseUT<R> fuse = FuseUT<R>{}) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {  // wider than a warp: single-lane generic path
         if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse);
         return;
     }
-    double q = 0.0, bb = 0.0, rr = 0.0;
+    R q = R(0), bb = R(0), rr = R(0);
     bool bad = false;
     if (lane < n) {
         const int s = s0 + lane;
         const int2 c = child_of<Ld>(T, s);
-        const double uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<double*>(u), s, bad) : Ld::ld(u + s);
+        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : Ld::ld(u + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
-        q = dadd(dadd(0.0, uu), lane_child_value<Ld>(c, V));
+        q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, V));
     }
-    const double E = lane_seq_sum(dmul(bb, q), n);
+    const R E = lane_seq_sum(dmul(bb, q), n);
     if (lane == 0) V[j] = E;
-    const double negE = dmul(-1.0, dadd(0.0, E));
-    double rv = 0.0;
+    const R negE = dmul(R(-1), dadd(R(0), E));
+    R rv = R(0);
     if (lane < n) {
         bad |= !isfinite(q);
         rv = post_op(dadd(rr, dadd(negE, q)), post, pf, nf);
         bad |= !isfinite(rv);
         r[s0 + lane] = rv;
     }
-    const double S = lane_seq_sum(rv > 0.0 ? rv : 0.0, n);
+    const R S = lane_seq_sum(rv > R(0) ? rv : R(0), n);
     if (do_rm && lane < n) b[s0 + lane] = rm_prob(rv, S, n);
     if (__any_sync(kFullMask, bad) && lane == 0) atomicOr(nonfinite, 1);
 }
 
-template <class Ld>
-__device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const double* __restrict__ m,
-                                             const double* __restrict__ r, double* __restrict__ b,
-                                             double* __restrict__ V, bool plus, int lane) {
+template <class Ld, class R>
+__device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const R* __restrict__ m,
+                                             const R* __restrict__ r, R* __restrict__ b,
+                                             R* __restrict__ V, bool plus, int lane) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
         if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus);
         return;
     }
-    double q = 0.0, bb = 0.0, rr = 0.0;
+    R q = R(0), bb = R(0), rr = R(0);
     if (lane < n) {
         const int s = s0 + lane;
         const int2 c = child_of<Ld>(T, s);
-        const double mm = Ld::ld(m + s);
+        const R mm = Ld::ld(m + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
-        q = dadd(dadd(0.0, mm), lane_child_value<Ld>(c, V));
+        q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, V));
     }
-    const double E = lane_seq_sum(dmul(bb, q), n);
+    const R E = lane_seq_sum(dmul(bb, q), n);
     if (lane == 0) V[j] = E;
-    const double negE = dmul(-1.0, dadd(0.0, E));
-    double rv = 0.0;
+    const R negE = dmul(R(-1), dadd(R(0), E));
+    R rv = R(0);
     if (lane < n) {
         rv = dadd(rr, dadd(negE, q));
-        if (plus) rv = rv > 0.0 ? rv : 0.0;
+        if (plus) rv = rv > R(0) ? rv : R(0);
     }
-    const double S = lane_seq_sum(rv > 0.0 ? rv : 0.0, n);
+    const R S = lane_seq_sum(rv > R(0) ? rv : R(0), n);
     if (lane < n) b[s0 + lane] = rm_prob(rv, S, n);
 }
 
-template <class Ld>
-__device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const double* __restrict__ g,
-                                           double* __restrict__ W, int lane) {
+template <class Ld, class R>
+__device__ __forceinline__ void br_dp_warp(const DevTree& T, int j, const R* __restrict__ g,
+                                           R* __restrict__ W, int lane) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
         if (lane == 0) br_dp<Ld>(T, j, g, W);
         return;
     }
-    double v = 0.0;
+    R v = R(0);
     if (lane < n) v = dadd(Ld::ld(g + s0 + lane), lane_child_value<Ld>(child_of<Ld>(T, s0 + lane), W));
-    double best = -INFINITY;
+    R best = R(-INFINITY);
     for (int a = 0; a < n; ++a) {
-        const double x = __shfl_sync(kFullMask, v, a);
+        const R x = __shfl_sync(kFullMask, v, a);
         if (x > best) best = x;
     }
     if (lane == 0) W[j] = best;

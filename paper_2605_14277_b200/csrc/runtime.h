@@ -97,6 +97,14 @@ struct DevBuf {
     ~DevBuf() { free(); }
 };
 
+// State vectors are DevBuf<double>; in the fp32 mode they hold floats
+// (allocated with half the doubles) and are accessed through vals<R>().
+template <class R>
+inline R* vals(const DevBuf<double>& b) {
+    return reinterpret_cast<R*>(b.p);
+}
+inline size_t val_slots(size_t count, bool f32) { return f32 ? (count + 1) / 2 : count; }
+
 struct Player {
     int S = 0, J = 0;
     int max_actions = 0;
@@ -113,6 +121,7 @@ struct Player {
     DevBuf<int2> child;
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
     DevBuf<double> g, W, xbar;                 // best-response scratch, one solve
+    DevBuf<double> wide;                       // fp32 mode: a widened read of one vector
     DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
     int levels() const { return (int)lvl.size() - 1; }
 };
@@ -130,6 +139,7 @@ struct DevCsr {
     }
     DevBuf<int> indptr, indices;
     DevBuf<double> data;
+    DevBuf<float> data32;  // fp32 mode: the values rounded once
 };
 
 // One phase of the persistent program: a DP level of one or both players
@@ -230,6 +240,7 @@ struct TilePlayer {
 struct scfr_handle {
     int device = 0;
     int B = 1;
+    bool f32 = false;  // SCFR_DTYPE_F32: iteration state in fp32
     int variant = 0, mode = 0;
     int engine = SCFR_ENGINE_LEVELS;
     int num_sms = 148;

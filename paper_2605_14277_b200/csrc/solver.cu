@@ -51,50 +51,53 @@ int post_of(int v) {
 // coherent.  Thread-per-DP for thin levels, warp-per-DP (lane = action) for
 // fat ones.
 
-struct Task {
+template <class R>  // value type: double, or float in the fp32 mode
+struct TaskT {
     DevTree T;
     int lo, n;   // DPs [lo, lo+n)
     int S, J;    // per-solve strides of seq- and dp-indexed state
     int nblk;    // blocks of the launch serving this task
-    const double* u;  // utility (OBS) / prediction (PRED)
-    double* r;
-    double* b;
-    double* x;
-    double* avg;
-    double* V;
-    FuseU fu;  // fu.ip set: OBS computes u from the payoff rows (fused SpMV)
-    int fu_sx; // per-solve stride of fu.x
+    const R* u;  // utility (OBS) / prediction (PRED)
+    R* r;
+    R* b;
+    R* x;
+    R* avg;
+    R* V;
+    FuseUT<R> fu;  // fu.ip set: OBS computes u from the payoff rows (fused SpMV)
+    int fu_sx;     // per-solve stride of fu.x
 };
+using Task = TaskT<double>;
 
 enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
 
 // The task's blocks stride over its DPs (grid-stride): a launch is capped at
 // about one resident wave, so the deep levels (10^6 DPs of a few loads each)
 // are not limited by CTA scheduling.
-template <int KIND, int MAXA, bool WARP>
-__device__ __forceinline__ void level_body(const Task& t, int blk, const KParams& kp) {
+template <int KIND, int MAXA, bool WARP, class R>
+__device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KParams& kp) {
     constexpr int kPerBlock = WARP ? TPB / 32 : TPB;
     const int stride = t.nblk * kPerBlock;
     const size_t so = (size_t)blockIdx.y * t.S;
-    double* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
+    R* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
     const int lane = threadIdx.x & 31;
-    double w = 0.0, pf = 1.0, nf = 1.0;
-    if (KIND == LK_TD_AVG) w = kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    // schedules are fp64 (host libm pow); the fp32 mode rounds them once
+    R w = R(0), pf = R(1), nf = R(1);
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
     if (KIND == LK_OBS && kp.post == POST_DCFR) {
         const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
-        pf = kp.pfsched[k];
-        nf = kp.nfsched[k];
+        pf = (R)kp.pfsched[k];
+        nf = (R)kp.nfsched[k];
     }
-    FuseU fu = t.fu;
+    FuseUT<R> fu = t.fu;
     if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
     const int first = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
     if (KIND == LK_TD_AVG && first == 0 && t.lo == 0 && t.n > 0) {  // the reference axpy also covers the empty sequence (x[0] = 1)
-        double* avg = t.avg + so;
+        R* avg = t.avg + so;
         avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
     }
     if (KIND == LK_OBS && fu.ip && first == 0 && lane == 0 && t.lo == 0 && t.n > 0) {  // the empty sequence's row: u[0] (next prediction)
         bool bad = false;
-        fused_u<LdL1>(fu, const_cast<double*>(t.u) + so, 0, bad);
+        fused_u<LdL1>(fu, const_cast<R*>(t.u) + so, 0, bad);
         if (bad) atomicOr(kp.nonfinite, 1);
     }
     for (int item = first; item < t.n; item += stride) {  // warp-uniform in warp mode
@@ -102,7 +105,7 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
         if constexpr (KIND == LK_TD_AVG) {
             td_dp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w);
         } else if constexpr (KIND == LK_TD) {
-            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, 0.0);
+            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0));
         } else if constexpr (KIND == LK_CUR) {
             cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
@@ -127,17 +130,19 @@ __device__ __forceinline__ void level_body(const Task& t, int blk, const KParams
 // with 4 DPs' loads in flight per thread measured no faster: these levels
 // already run within ~10% of a bare fp64 stream of the same size on B200,
 // scripts/micro/stream_probe.cu.)
-template <int KIND, int MAXA, bool WARP>
-__global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : 1) k_level(const __grid_constant__ Task t0,
-                                               const __grid_constant__ Task t1,
+template <int KIND, int MAXA, bool WARP, class R>
+__global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : 1) k_level(const __grid_constant__ TaskT<R> t0,
+                                               const __grid_constant__ TaskT<R> t1,
                                                const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
     pdl_wait();
-    if ((int)blockIdx.x < t0.nblk) level_body<KIND, MAXA, WARP>(t0, blockIdx.x, kp);
-    else level_body<KIND, MAXA, WARP>(t1, blockIdx.x - t0.nblk, kp);
+    if ((int)blockIdx.x < t0.nblk) level_body<KIND, MAXA, WARP, R>(t0, blockIdx.x, kp);
+    else level_body<KIND, MAXA, WARP, R>(t1, blockIdx.x - t0.nblk, kp);
 }
 
-using LevelKernel = void (*)(Task, Task, KParams);
+template <class R>
+using LevelKernelT = void (*)(TaskT<R>, TaskT<R>, KParams);
+using LevelKernel = LevelKernelT<double>;
 
 // Warp-per-DP only pays on small, fat levels: few DPs (parallelism is
 // scarce, so per-DP latency is the critical path) with >= 8 child-DP
@@ -152,31 +157,33 @@ static bool warp_level(const Player& P, int l) {
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
-static LevelKernel pick_level_kernel(int kind, int maxa, bool warp) {
+template <class R>
+static LevelKernelT<R> pick_level_kernel(int kind, int maxa, bool warp) {
     const int m = maxa <= 1 ? 0 : maxa <= 2 ? 1 : maxa <= 4 ? 2 : 3;
 #define SCFR_PICK(K) \
-    (m == 0 ? k_level<K, 1, false> : m == 1 ? k_level<K, 2, false> : m == 2 ? k_level<K, 4, false> : k_level<K, 8, false>)
+    (m == 0 ? k_level<K, 1, false, R> : m == 1 ? k_level<K, 2, false, R> : m == 2 ? k_level<K, 4, false, R> : k_level<K, 8, false, R>)
     switch (kind) {
-        case LK_TD_AVG: return k_level<LK_TD_AVG, 1, false>;
-        case LK_TD: return k_level<LK_TD, 1, false>;
+        case LK_TD_AVG: return k_level<LK_TD_AVG, 1, false, R>;
+        case LK_TD: return k_level<LK_TD, 1, false, R>;
         case LK_CUR: return SCFR_PICK(LK_CUR);
         case LK_OBS:
-            if (warp) return k_level<LK_OBS, 1, true>;
+            if (warp) return k_level<LK_OBS, 1, true, R>;
             return SCFR_PICK(LK_OBS);
         default:
-            if (warp) return k_level<LK_PRED, 1, true>;
+            if (warp) return k_level<LK_PRED, 1, true, R>;
             return SCFR_PICK(LK_PRED);
     }
 #undef SCFR_PICK
 }
 
 // avg[0] update for a player without decision points (no TD levels).
-__global__ void k_avg0(int S, const double* __restrict__ x, double* __restrict__ avg,
+template <class R>
+__global__ void k_avg0(int S, const R* __restrict__ x, R* __restrict__ avg,
                        const double* __restrict__ wsched, int cap, const long long* __restrict__ tdev) {
     pdl_launch_dependents();
     pdl_wait();
     const size_t o = (size_t)blockIdx.x * S;
-    const double w = wsched[(size_t)blockIdx.x * cap + *tdev];
+    const R w = (R)wsched[(size_t)blockIdx.x * cap + *tdev];
     avg[o] = dadd(dmul(w, x[o]), avg[o]);
 }
 
@@ -200,15 +207,16 @@ __global__ void k_br_root(DevTree T, const double* __restrict__ g, const double*
     *out = dadd(g[0], child_sum<LdL1>(T.child[0], W));
 }
 
+template <class R>
 __global__ void k_spmv(int rows, const int* __restrict__ indptr, const int* __restrict__ indices,
-                       const double* __restrict__ data, const double* __restrict__ x, int sx,
-                       double* __restrict__ out, int so, int negate, int* nonfinite) {
+                       const R* __restrict__ data, const R* __restrict__ x, int sx,
+                       R* __restrict__ out, int so, int negate, int* nonfinite) {
     pdl_launch_dependents();
     pdl_wait();
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
-    double acc = spmv_row<LdL1>(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
-    if (negate) acc = dmul(-1.0, acc);
+    R acc = spmv_row<LdL1>(indptr, indices, data, x + (size_t)blockIdx.y * sx, row);
+    if (negate) acc = dmul(R(-1), acc);
     if (nonfinite && !isfinite(acc)) atomicOr(nonfinite, 1);
     out[(size_t)blockIdx.y * so + row] = acc;
 }
@@ -248,23 +256,32 @@ __global__ void k_derive_child(int J, const int* __restrict__ dp_parent, int2* _
 
 // Uniform behaviour 1.0/n per DP block (pkg/decision_process.py:254-261),
 // the RegretState initial b, for every solve of the batch.
+template <class R>
 __global__ void k_derive_uniform(int J, int S, int B, const int* __restrict__ seq_ptr,
-                                 double* __restrict__ b) {
+                                 R* __restrict__ b) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= J) return;
     const int s0 = seq_ptr[j], n = seq_ptr[j + 1] - s0;
-    const double v = ddiv(1.0, (double)n);
+    const R v = ddiv(R(1), R(n));
     for (int k = 0; k < B; ++k)
         for (int a = 0; a < n; ++a) b[(size_t)k * S + s0 + a] = v;
 }
 
 // x[0] = xpost[0] = 1 (the empty sequence's mass) for every solve.
-__global__ void k_init_root(int S, int B, double* __restrict__ x, double* __restrict__ xpost) {
+template <class R>
+__global__ void k_init_root(int S, int B, R* __restrict__ x, R* __restrict__ xpost) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= B) return;
-    x[(size_t)k * S] = 1.0;
-    xpost[(size_t)k * S] = 1.0;
+    x[(size_t)k * S] = R(1);
+    xpost[(size_t)k * S] = R(1);
 }
+
+// fp32 mode: payoff values rounded to nearest fp32 once, at upload.
+__global__ void k_to_f32(int n, const double* __restrict__ d, float* __restrict__ f) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) f[i] = __double2float_rn(d[i]);
+}
+
 
 // SCFR_TRACE=1: create-time breakdown on stderr.
 static void trace_stage(const char* what) {
@@ -283,7 +300,7 @@ static void trace_stage(const char* what) {
 // Validates the reference DecisionProcess arrays, builds the int32 device
 // structure (seq_ptr, dp_parent on the host: O(J); child ranges and the
 // initial behaviour on the device: O(S)) and the per-level bookkeeping.
-static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s, int slot) {
+static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s, int slot, bool f32) {
     if (!p || p->num_seqs < 1 || p->num_decisions < 0 || p->num_nodes < 1)
         fail(SCFR_EINVAL, "bad tfsdp sizes");
     if (p->num_seqs >= (1ll << 31) / 2) fail(SCFR_EINVAL, "tfsdp too large for int32 indexing");
@@ -479,7 +496,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     CUDA_OK(copy_async(P.seq_ptr.p, seq_ptr.data(), (J + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
     if (J) CUDA_OK(copy_async(P.dp_parent.p, dp_parent.data(), J * sizeof(int), cudaMemcpyHostToDevice, s));
     P.child.zero(s);
-    const size_t SB = (size_t)S * B, JB = (size_t)std::max(J, 1) * B;
+    const size_t SB = val_slots((size_t)S * B, f32), JB = val_slots((size_t)std::max(J, 1) * B, f32);
     P.r.alloc(SB);
     P.b.alloc(SB);
     P.x.alloc(SB);
@@ -487,16 +504,19 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     P.avg.alloc(SB);
     P.u.alloc(SB);
     P.V.alloc(JB);
-    P.g.alloc(S);
+    P.g.alloc(S);  // best response / evaluation scratch: always fp64
     P.W.alloc(std::max(J, 1));
     P.xbar.alloc(S);
+    if (f32) P.wide.alloc(S);
     for (auto* buf : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V}) buf->zero(s);
     trace_stage("copies+allocs");
     if (J) {
         k_derive_child<<<grid_for(J), TPB, 0, s>>>(J, P.dp_parent.p, P.child.p);
-        k_derive_uniform<<<grid_for(J), TPB, 0, s>>>(J, S, B, P.seq_ptr.p, P.b.p);
+        if (f32) k_derive_uniform<float><<<grid_for(J), TPB, 0, s>>>(J, S, B, P.seq_ptr.p, vals<float>(P.b));
+        else k_derive_uniform<double><<<grid_for(J), TPB, 0, s>>>(J, S, B, P.seq_ptr.p, P.b.p);
     }
-    k_init_root<<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
+    if (f32) k_init_root<float><<<grid_for(B), TPB, 0, s>>>(S, B, vals<float>(P.x), vals<float>(P.xpost));
+    else k_init_root<double><<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(s));
     trace_stage("derive+sync");
@@ -506,8 +526,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
 
 // Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
 // last shard may hold fewer), re-based so local row i is global row0 + i.
-static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Player& rowP, int world = 1,
-                       int rank = 0) {
+static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Player& rowP, bool f32,
+                       int world = 1, int rank = 0) {
     if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
     if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
     if (m->indptr[0] != 0 || m->indptr[m->rows] != m->nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
@@ -570,6 +590,11 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Playe
         CUDA_OK(copy_async(D.indices.p, ix, (size_t)D.nnz * sizeof(int), cudaMemcpyHostToDevice, s));
         CUDA_OK(copy_async(D.data.p, dv ? dv : m->data + k0, (size_t)D.nnz * sizeof(double),
                            cudaMemcpyHostToDevice, s));
+    }
+    if (f32) {  // the iteration's copy, rounded once (the fp64 one serves best responses)
+        D.data32.alloc(std::max(D.nnz, 1));
+        if (D.nnz) k_to_f32<<<grid_for(D.nnz), TPB, 0, s>>>(D.nnz, D.data.p, D.data32.p);
+        CUDA_OK(cudaGetLastError());
     }
     CUDA_OK(cudaStreamSynchronize(s));
     trace_stage("csr copies+sync");
@@ -649,34 +674,33 @@ static DevTree shaped_tree(const Player& P, int l) {
 
 // Structure bytes are counted only where the kernel loads them: an affine
 // level (lvl_shape) computes seq_ptr / child / dp_parent arithmetically.
-struct LevelBytes {
+struct LevelBytes {  // v: bytes per value (8 fp64, 4 in the fp32 mode)
     static double seqptr(const Player& P, int l) { return P.lvl_shape[l].un > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
     static double child(const Player& P, int l) { return P.lvl_shape[l].cn >= 0 ? 0.0 : 8.0 * P.lvl_ns[l]; }
     static double parent(const Player& P, int l) { return P.lvl_shape[l].pc > 0 ? 0.0 : 4.0 * P.lvl_nj[l]; }
     // single-action levels touch no r / b (kernels.cuh single_action_note)
     static bool single(const Player& P, int l) { return P.lvl_shape[l].un == 1; }
-    static double obs(const Player& P, int l, bool rm) {
+    static double obs(const Player& P, int l, bool rm, double v = 8) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
         // u, b read; r RMW; [b write]; V write; child V reads; structure
-        const double rb = single(P, l) ? 0.0 : (8 + 16 + (rm ? 8 : 0)) * ns;
-        return 8 * ns + rb + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
+        const double rb = single(P, l) ? 0.0 : (3 + (rm ? 1 : 0)) * v * ns;
+        return v * ns + rb + v * nj + v * nc + seqptr(P, l) + child(P, l);
     }
-    static double pred(const Player& P, int l) {
+    static double pred(const Player& P, int l, double v = 8) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l], nc = P.lvl_nc[l];
         // m, b, r read; b write; V write; child V reads; structure
-        return (single(P, l) ? 8 : 32) * ns + 8 * nj + 8 * nc + seqptr(P, l) + child(P, l);
+        return (single(P, l) ? 1 : 4) * v * ns + v * nj + v * nc + seqptr(P, l) + child(P, l);
     }
-    static double td(const Player& P, int l, bool avg) {
+    static double td(const Player& P, int l, bool avg, double v = 8) {
         const double ns = P.lvl_ns[l], nj = P.lvl_nj[l];
         // b read, x write, [avg RMW]; parent x; structure
-        return ((single(P, l) ? 8 : 16) + (avg ? 16 : 0)) * ns + 8 * nj + seqptr(P, l) + parent(P, l);
+        return ((single(P, l) ? 1 : 2) + (avg ? 2 : 0)) * v * ns + v * nj + seqptr(P, l) + parent(P, l);
     }
-    static double cur(const Player& P, int l) {  // r read, x write; parent x; structure
-        return (single(P, l) ? 8.0 : 16.0) * P.lvl_ns[l] + 8.0 * P.lvl_nj[l] + seqptr(P, l) +
-               parent(P, l);
+    static double cur(const Player& P, int l, double v = 8) {  // r read, x write; parent x; structure
+        return (single(P, l) ? 1 : 2) * v * P.lvl_ns[l] + v * P.lvl_nj[l] + seqptr(P, l) + parent(P, l);
     }
-    static double spmv(const DevCsr& M) {
-        return 4.0 * (M.rows + 1) + 12.0 * M.nnz + 8.0 * M.cols + 8.0 * M.rows;
+    static double spmv(const DevCsr& M, double v = 8) {
+        return 4.0 * (M.rows + 1) + (4.0 + v) * M.nnz + v * M.cols + v * M.rows;
     }
 };
 
@@ -691,17 +715,18 @@ struct Launcher : LaunchBase {
 
 
     // Task for level l of player P (l outside [0, L) -> empty task).
-    static Task task(Player& P, int l, const double* u, double* x) {
-        Task t{};
+    template <class R>
+    static TaskT<R> task(Player& P, int l, const R* u, R* x) {
+        TaskT<R> t{};
         t.T = shaped_tree(P, l);
         t.S = P.S;
         t.J = P.J;
         t.u = u;
-        t.r = P.r.p;
-        t.b = P.b.p;
+        t.r = vals<R>(P.r);
+        t.b = vals<R>(P.b);
         t.x = x;
-        t.avg = P.avg.p;
-        t.V = P.V.p;
+        t.avg = vals<R>(P.avg);
+        t.V = vals<R>(P.V);
         if (l >= 0 && l < P.levels()) {
             t.lo = P.lvl[l];
             t.n = P.lvl[l + 1] - P.lvl[l];
@@ -710,7 +735,8 @@ struct Launcher : LaunchBase {
     }
     // Resident CTAs of a level kernel on the whole GPU (cached per handle),
     // or num_sms * SCFR_WAVE_CTAS when that is set.
-    int resident_ctas(LevelKernel kern) const {
+    template <class K>
+    int resident_ctas(K kern) const {
         if (h->wave_ctas_env) return h->num_sms * h->wave_ctas;
         const void* key = reinterpret_cast<const void*>(kern);
         for (const auto& e : h->tile_occ)
@@ -730,20 +756,28 @@ struct Launcher : LaunchBase {
         return l >= 0 && l < P.levels() && warp_level(P, l);
     }
 
+    // Payoff values in the handle's arithmetic (fp32 copy in the fp32 mode).
+    template <class R>
+    const R* payoff_data(const DevCsr& M) const {
+        if constexpr (sizeof(R) == 4) return M.data32.p;
+        else return M.data.p;
+    }
+
     // One launch over level la of A and level lb of Bp (either may be absent).
-    void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const double* ua,
-               const double* ub, double* xa, double* xb, bool do_rm) {
-        Task t0 = A ? task(*A, la, ua, xa) : Task{};
-        Task t1 = Bp ? task(*Bp, lb, ub, xb) : Task{};
+    template <class R>
+    void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
+               R* xa, R* xb, bool do_rm) {
+        TaskT<R> t0 = A ? task<R>(*A, la, ua, xa) : TaskT<R>{};
+        TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
         if (t0.n == 0 && t1.n == 0) return;
         const bool fused = lk == LK_OBS && fuse_spmv();
         if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
             Player& P1 = h->P[0];
             Player& P2 = h->P[1];
-            t0.fu = FuseU{h->U.indptr.p, h->U.indices.p, h->U.data.p, P2.x.p, 0};
+            t0.fu = FuseUT<R>{h->U.indptr.p, h->U.indices.p, payoff_data<R>(h->U), vals<R>(P2.x), 0};
             t0.fu_sx = P2.S;
-            t1.fu = FuseU{h->UT.indptr.p, h->UT.indices.p, h->UT.data.p,
-                          h->mode == SCFR_MODE_ALT ? P1.xpost.p : P1.x.p, 1};
+            t1.fu = FuseUT<R>{h->UT.indptr.p, h->UT.indices.p, payoff_data<R>(h->UT),
+                              h->mode == SCFR_MODE_ALT ? vals<R>(P1.xpost) : vals<R>(P1.x), 1};
             t1.fu_sx = P1.S;
         }
         const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
@@ -755,26 +789,27 @@ struct Launcher : LaunchBase {
         t1.nblk = std::min((t1.n + per - 1) / per, cap);
         int maxa = 1;
         double bytes = 0.0;
+        const double v = sizeof(R);
         for (int k = 0; k < 2; ++k) {
             Player* P = k == 0 ? A : Bp;
             const int l = k == 0 ? la : lb;
             if (!P || l < 0 || l >= P->levels()) continue;
             maxa = std::max(maxa, P->lvl_maxa[l]);
             switch (lk) {
-                case LK_TD_AVG: bytes += LevelBytes::td(*P, l, true); break;
-                case LK_TD: bytes += LevelBytes::td(*P, l, false); break;
-                case LK_CUR: bytes += LevelBytes::cur(*P, l); break;
-                case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm); break;
-                default: bytes += LevelBytes::pred(*P, l); break;
+                case LK_TD_AVG: bytes += LevelBytes::td(*P, l, true, v); break;
+                case LK_TD: bytes += LevelBytes::td(*P, l, false, v); break;
+                case LK_CUR: bytes += LevelBytes::cur(*P, l, v); break;
+                case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm, v); break;
+                default: bytes += LevelBytes::pred(*P, l, v); break;
             }
             if (fused) {  // this level's payoff rows; u is written instead of read
                 const DevCsr& M = k == 0 ? h->U : h->UT;
                 const int s0 = P->lvl_s0[l], s1 = s0 + (int)P->lvl_ns[l];
                 const double nnz = (double)(M.ptr_at(s1) - M.ptr_at(s0));
-                bytes += 4.0 * (s1 - s0 + 1) + 12.0 * nnz + 8.0 * nnz;
+                bytes += 4.0 * (s1 - s0 + 1) + (4.0 + v) * nnz + v * nnz;
             }
         }
-        const LevelKernel kern = pick_level_kernel(lk, maxa, warp);
+        const LevelKernelT<R> kern = pick_level_kernel<R>(lk, maxa, warp);
         // grid-stride tasks: cap each at one resident wave of this kernel
         const int wave = resident_ctas(kern);
         t0.nblk = std::min(t0.nblk, wave);
@@ -787,13 +822,15 @@ struct Launcher : LaunchBase {
 
     // out[row0 + i] = (±) row i of M applied to x (this rank's rows), then in
     // the row-sharded mode the slices are all-gathered into the full vector.
-    void spmv(const DevCsr& M, const double* x, int sx, double* out, int so, bool neg) {
-        launch(KK_SPMV, LevelBytes::spmv(M), [&] {
+    template <class R>
+    void spmv(const DevCsr& M, const R* x, int sx, R* out, int so, bool neg) {
+        launch(KK_SPMV, LevelBytes::spmv(M, sizeof(R)), [&] {
             dim3 grid(grid_for(M.rows), h->B);
-            run(k_spmv, grid, M.rows, (const int*)M.indptr.p, (const int*)M.indices.p,
-                (const double*)M.data.p, x, sx, out + M.row0, so, neg ? 1 : 0, h->nonfinite.p);
+            run(k_spmv<R>, grid, M.rows, (const int*)M.indptr.p, (const int*)M.indices.p,
+                payoff_data<R>(M), x, sx, out + M.row0, so, neg ? 1 : 0, h->nonfinite.p);
         });
-        if (h->comm) allgather_rows(h, out, M.chunk);
+        if constexpr (sizeof(R) == 8)
+            if (h->comm) allgather_rows(h, out, M.chunk);
     }
 
     void iteration() {
@@ -801,44 +838,51 @@ struct Launcher : LaunchBase {
             tiled_iteration(*this);
             return;
         }
+        if (h->f32) iteration_t<float>();
+        else iteration_t<double>();
+    }
+
+    template <class R>
+    void iteration_t() {
         Player& A = h->P[0];
         Player& Bp = h->P[1];
+        R *Au = vals<R>(A.u), *Bu = vals<R>(Bp.u), *Ax = vals<R>(A.x), *Bx = vals<R>(Bp.x);
+        R* Axp = vals<R>(A.xpost);
         const bool pr = predictive(h->variant);
         const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
         // next_strategy of both players (independent): PRED deep -> shallow,
         // then TD + average shallow -> deep, the two players sharing launches.
         if (pr)
             for (int k = 0; k < L; ++k)
-                level(LK_PRED, KK_PRED, &A, LA - 1 - k, &Bp, LB - 1 - k, A.u.p, Bp.u.p, A.x.p,
-                      Bp.x.p, false);
+                level<R>(LK_PRED, KK_PRED, &A, LA - 1 - k, &Bp, LB - 1 - k, Au, Bu, Ax, Bx, false);
         for (Player* P : {&A, &Bp})
             if (P->J == 0)
-                launch(KK_TD_AVG, 16.0, [&] {
-                    run1(k_avg0, dim3(h->B), P->S, (const double*)P->x.p, P->avg.p,
+                launch(KK_TD_AVG, 2.0 * sizeof(R), [&] {
+                    run1(k_avg0<R>, dim3(h->B), P->S, (const R*)vals<R>(P->x), vals<R>(P->avg),
                          (const double*)h->wsched.p, h->cap, (const long long*)h->tdev.p);
                 });
         for (int k = 0; k < L; ++k)
-            level(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, A.x.p, Bp.x.p, false);
+            level<R>(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, Ax, Bx, false);
         const bool fused = fuse_spmv();
-        if (!fused) spmv(h->U, Bp.x.p, Bp.S, A.u.p, A.S, false);  // u1 = U x2
+        if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
-            if (!fused) spmv(h->UT, A.x.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1
+            if (!fused) spmv<R>(h->UT, Ax, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1
             for (int k = 0; k < L; ++k)
-                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, A.u.p,
-                      Bp.u.p, A.x.p, Bp.x.p, !pr);
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, Au, Bu, Ax, Bx,
+                         !pr);
         } else {
             for (int k = 0; k < LA; ++k)
-                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, A.u.p, nullptr,
-                      A.x.p, nullptr, !pr);
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, Au, nullptr, Ax,
+                         nullptr, !pr);
             // current_strategy of player 1 into xpost: RM on the fly
             // (predictive) or TD of the b that OBS already regret-matched
             for (int k = 0; k < LA; ++k)
-                level(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, k, nullptr, -1, nullptr,
-                      nullptr, A.xpost.p, nullptr, false);
-            if (!fused) spmv(h->UT, A.xpost.p, A.S, Bp.u.p, Bp.S, true);  // u2 = -Uᵀ x1'
+                level<R>(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, k, nullptr, -1, nullptr, nullptr,
+                         Axp, nullptr, false);
+            if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
-                level(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr,
-                      Bp.u.p, nullptr, Bp.x.p, !pr);
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
+                         nullptr, Bx, !pr);
         }
         launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p); });
     }
@@ -993,6 +1037,12 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                 fail(SCFR_EINVAL, "the row-sharded mode runs on the level engine");
         }
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
+        if (cfg->dtype != SCFR_DTYPE_F64 && cfg->dtype != SCFR_DTYPE_F32) fail(SCFR_EINVAL, "unknown dtype");
+        if (cfg->dtype == SCFR_DTYPE_F32) {
+            if (nccl_id) fail(SCFR_EINVAL, "the fp32 mode does not run the row-sharded mode");
+            if (cfg->engine != SCFR_ENGINE_AUTO && cfg->engine != SCFR_ENGINE_LEVELS)
+                fail(SCFR_EINVAL, "the fp32 mode runs on the level engine");
+        }
         if (cfg->mode != SCFR_MODE_SIM && cfg->mode != SCFR_MODE_ALT) fail(SCFR_EINVAL, "mode must be sim or alt");
         if (cfg->batch < 1) fail(SCFR_EINVAL, "batch must be >= 1");
         if (cfg->engine < SCFR_ENGINE_AUTO || cfg->engine > SCFR_ENGINE_PERSISTENT_CLUSTER)
@@ -1016,6 +1066,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->device = device;
         h->num_sms = nsm;
         h->B = cfg->batch;
+        h->f32 = cfg->dtype == SCFR_DTYPE_F32;
         h->variant = cfg->variant;
         h->mode = cfg->mode;
         h->engine = cfg->engine;
@@ -1050,13 +1101,13 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         PinnedArena& pa = pinned_arena();
         std::lock_guard<std::mutex> pin_guard(pa.lock);
         pa.reserve((size_t)std::max(U->rows, UT->rows) * 4 + (size_t)std::max<int64_t>(U->nnz, 1) * 12 + 4096);
-        upload_player(p1, h->P[0], h->B, h->stream, 0);
+        upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32);
         stage("player1");
-        upload_player(p2, h->P[1], h->B, h->stream, 1);
+        upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32);
         stage("player2");
         const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
-        upload_csr(U, h->U, h->stream, h->P[0], w, rk);
-        upload_csr(UT, h->UT, h->stream, h->P[1], w, rk);
+        upload_csr(U, h->U, h->stream, h->P[0], h->f32, w, rk);
+        upload_csr(UT, h->UT, h->stream, h->P[1], h->f32, w, rk);
         if (nccl_id) {
             // u and the BR gradient are gathered as world x chunk (padded) vectors
             for (int k = 0; k < 2; ++k) {
@@ -1095,6 +1146,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         }
         const char* eng = std::getenv("SCFR_ENGINE");  // override for experiments / tests
         if (eng && h->engine == SCFR_ENGINE_AUTO && !h->comm) h->engine = std::atoi(eng);
+        if (h->f32) h->engine = SCFR_ENGINE_LEVELS;  // (validated above)
         if (h->engine == SCFR_ENGINE_AUTO) {
             // the tile engine is opt-in: bit-exact, but not yet faster than
             // PDL-chained level kernels on the config games

@@ -39,8 +39,9 @@
 namespace scfr {
 
 __global__ void k_derive_child(int J, const int* __restrict__ dp_parent, int2* __restrict__ child);
+template <class R>
 __global__ void k_derive_uniform(int J, int S, int B, const int* __restrict__ seq_ptr,
-                                 double* __restrict__ b);
+                                 R* __restrict__ b);
 
 constexpr int kTileThreads = 256;
 constexpr int kTileMinBlocks = 3;  // <= 80 registers; shared memory allows ~3 CTAs per SM anyway
@@ -944,8 +945,19 @@ __global__ void k_scatter_seq(int S, const int* __restrict__ sperm, const double
     if (i < S) dst[sperm[i]] = src[i];
 }
 
+__global__ void k_widen_f32(int n, const float* __restrict__ f, double* __restrict__ d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = (double)f[i];
+}
+
 const double* orig_order(scfr_handle* h, int player, const double* buf, int solve) {
     Player& P = h->P[player - 1];
+    if (h->f32) {  // fp32 state (level engine, reference order): widen exactly
+        const float* f = reinterpret_cast<const float*>(buf) + (size_t)solve * P.S;
+        k_widen_f32<<<grid_for(P.S), TPB, 0, h->stream>>>(P.S, f, P.wide.p);
+        CUDA_OK(cudaGetLastError());
+        return P.wide.p;
+    }
     const double* src = buf + (size_t)solve * P.S;
     if (h->engine != SCFR_ENGINE_TILED) return src;
     TilePlayer& tp = h->tp[player - 1];

@@ -21,6 +21,7 @@ MODE_CODE = {"sim": 0, "alt": 1}
 ENGINE_CODE = {"auto": 0, "levels": 1, "persistent": 2, "persistent_grid": 3, "tiled": 4,
                "persistent_cluster": 5}
 ENGINE_NAME = {v: k for k, v in ENGINE_CODE.items()}
+DTYPE_CODE = {"f64": 0, "float64": 0, "f32": 1, "float32": 1}
 STATE_CODE = {"regrets": 0, "behavior": 1, "accum": 2, "utility": 3}
 
 
@@ -74,7 +75,7 @@ class Config(C.Structure):
     _fields_ = [("variant", C.c_int32), ("mode", C.c_int32), ("alpha", C.c_double),
                 ("beta", C.c_double), ("gamma", C.c_double), ("batch", C.c_int32),
                 ("batch_alpha", f64p), ("batch_beta", f64p), ("batch_gamma", f64p),
-                ("engine", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("engine", C.c_int32), ("dtype", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 _lib = None

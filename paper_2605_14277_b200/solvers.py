@@ -107,9 +107,13 @@ class Solver:
     """
 
     def __init__(self, bundle: GameBundle, config: SolverConfig, device: int = 0,
-                 batch_params=None, engine: str = "auto", shard=None):
+                 batch_params=None, engine: str = "auto", shard=None, dtype: str = "f64"):
         """``shard=(nccl_unique_id, rank, world)`` selects the row-sharded
-        multi-GPU mode (see distributed.sharded_solver)."""
+        multi-GPU mode (see distributed.sharded_solver).  ``dtype="f32"``
+        runs the iteration in fp32 (same operation order, fp32 rounding;
+        level engine); reads and exploitability stay fp64."""
+        if dtype not in N.DTYPE_CODE:
+            raise ValueError(f"unknown dtype {dtype!r}")
         self.bundle = bundle
         self.config = config
         L = N.lib()
@@ -135,6 +139,8 @@ class Solver:
             cfg.batch = 1
             self.batch_params = [(float(config.alpha), float(config.beta), float(config.gamma))]
         cfg.engine = N.ENGINE_CODE[engine]
+        cfg.dtype = N.DTYPE_CODE[dtype]
+        self.dtype = "f32" if cfg.dtype == 1 else "f64"
         self.batch = int(cfg.batch)
         self.device = device
         h = C.c_void_p()
@@ -305,7 +311,8 @@ def _as_bundle(game) -> GameBundle:
 
 def run(game, config: SolverConfig, iterations: int | None = None,
         seconds: float | None = None, checkpoints=None, backend=None,
-        record_current: bool = True, device: int = 0, engine: str = "auto") -> RunResult:
+        record_current: bool = True, device: int = 0, engine: str = "auto",
+        dtype: str = "f64") -> RunResult:
     """Solve and record convergence (reference pkg/solvers.py:375-438).
 
     Iterates are bit-identical to the reference's.  Iterations between
@@ -321,7 +328,7 @@ def run(game, config: SolverConfig, iterations: int | None = None,
         raise ValueError("budget must be positive: seconds <= 0")
     del backend
     bundle = _as_bundle(game)
-    solver = Solver(bundle, config, device=device, engine=engine)
+    solver = Solver(bundle, config, device=device, engine=engine, dtype=dtype)
     schedule = sorted(set(int(c) for c in checkpoints)) if checkpoints else []
     wpi = work_per_iteration(bundle, config)
     peak = bundle.reference_nbytes() + bundle.reference_state_bytes()
@@ -379,7 +386,7 @@ class TargetResult:
 
 def solve_to_target(game, config: SolverConfig, target: float = 1e-4, check_every: int = 1,
                     max_iterations: int = 1_000_000, device: int = 0,
-                    engine: str = "auto") -> TargetResult:
+                    engine: str = "auto", dtype: str = "f64") -> TargetResult:
     """Iterate until the average profile's exploitability is <= target,
     checking every ``check_every`` iterations on the device (time-to-target
     metric of BASELINE.json; the reference computes the same quantity with a
@@ -387,7 +394,7 @@ def solve_to_target(game, config: SolverConfig, target: float = 1e-4, check_ever
     if target <= 0 or check_every < 1:
         raise ValueError("target must be > 0 and check_every >= 1")
     bundle = _as_bundle(game)
-    s = Solver(bundle, config, device=device, engine=engine)
+    s = Solver(bundle, config, device=device, engine=engine, dtype=dtype)
     t0 = time.perf_counter()
     solve_ms = 0.0
     t = checks = 0
@@ -429,13 +436,13 @@ class IterationBenchmark:
 
 def benchmark_iterations(bundle: GameBundle, config: SolverConfig, backend=None,
                          warmup: int = 2, measured: int = 8, device: int = 0,
-                         engine: str = "auto") -> IterationBenchmark:
+                         engine: str = "auto", dtype: str = "f64") -> IterationBenchmark:
     """Per-iteration device time (CUDA events around each step)
     (reference pkg/solvers.py:463-492)."""
     if measured < 1:
         raise ValueError("measured iterations must be >= 1")
     del backend
-    s = Solver(bundle, config, device=device, engine=engine)
+    s = Solver(bundle, config, device=device, engine=engine, dtype=dtype)
     if warmup:
         s.step(warmup)
     s.synchronize()
