@@ -135,15 +135,15 @@ def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: flo
 
 def per_game_suite(device: int, cpu: bool) -> dict:
     """BASELINE.json configs on one GPU: iterations/s and time to
-    exploitability 1e-4 (device-side best response after every iteration, or
-    every 10 for Liar's dice), the 256-solve Leduc DCFR sweep, and the CPU
+    exploitability 1e-4 (the exact first iteration, found by a coarse-to-fine
+    search over device-side snapshots), the 256-solve Leduc DCFR sweep, and the CPU
     oracle on the same small configs for context."""
     from paper_2605_14277_b200 import Solver, SolverConfig, solve_to_target
 
     out = {}
     for name, kind, variant, check in (("kuhn_cfr", "kuhn", "cfr", None),
                                         ("leduc_cfr+", "leduc", "cfr+", 1),
-                                        ("liars_dice_dcfr", "liars", "dcfr", 10)):
+                                        ("liars_dice_dcfr", "liars", "dcfr", 1)):
         b = make_bundle(kind)
         cfg = SolverConfig(variant)
         s = Solver(b, cfg, device=device)
@@ -157,7 +157,8 @@ def per_game_suite(device: int, cpu: bool) -> dict:
             r = solve_to_target(b, cfg, 1e-4, check_every=check, device=device)
             rec.update({"target": 1e-4, "reached": r.reached, "iterations": r.iterations,
                         "exploitability": r.exploitability, "seconds_wall": r.seconds,
-                        "seconds_solve_only": r.solve_seconds, "check_every": check})
+                        "seconds_solve_only": r.solve_seconds, "check_every": check,
+                        "search": "coarse-to-fine: snapshot, 16 iterations, check; replay on a hit"})
         else:
             s = Solver(b, cfg, device=device)
             s.step(1000)

@@ -196,6 +196,12 @@ int scfr_step(scfr_handle* h, int64_t n_iter);
 /* The engine the handle runs (SCFR_ENGINE_*; AUTO resolved at creation). */
 int scfr_engine(const scfr_handle* h, int* engine);
 int scfr_synchronize(scfr_handle* h);
+/* Saves (restore = 0) or restores (restore = 1) the whole iteration state of
+ * the handle (every solve, and the iteration counters) in device memory:
+ * a time-to-target search checks every K iterations and, on a hit, replays
+ * the last K from the snapshot to find the first iteration that meets the
+ * target (paper_2605_14277_b200.solve_to_target). */
+int scfr_snapshot(scfr_handle* h, int restore);
 /* Completed iterations (the reference's RegretState.t - 1). */
 int scfr_iterations(const scfr_handle* h, int64_t* out);
 /* Normalised average strategy avg_accum / avg_weight over Σ (player 1/2). */

@@ -237,6 +237,17 @@ struct TilePlayer {
 
 }  // namespace scfr
 
+namespace scfr {
+// scfr_snapshot: saved state vectors, device iteration counter, host counters.
+struct Snapshot {
+    bool valid = false;
+    DevBuf<double> buf[2][7];  // per player: r, b, x, xpost, avg, u, V
+    DevBuf<long long> tdev;
+    int64_t t = 0;
+    std::vector<double> avg_weight;
+};
+}  // namespace scfr
+
 struct scfr_handle {
     int device = 0;
     int B = 1;
@@ -267,6 +278,7 @@ struct scfr_handle {
     int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;
     scfr::PersistentPlan plan;
+    scfr::Snapshot snap;
     // Row-sharded payoff SpMV (scfr_create_sharded): NCCL communicator
     // (ncclComm_t) over `world` ranks, this handle being `rank`.
     void* comm = nullptr;

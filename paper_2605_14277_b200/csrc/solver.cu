@@ -1276,6 +1276,42 @@ int scfr_synchronize(scfr_handle* h) {
     });
 }
 
+// Device-side copy of the whole iteration state (every solve of the batch)
+// and of the host counters: a coarse-to-fine time-to-target search replays
+// from it instead of paying a best response after every iteration.
+int scfr_snapshot(scfr_handle* h, int restore) {
+    return guarded([&] {
+        if (!h) fail(SCFR_EINVAL, "handle is NULL");
+        if (restore != 0 && restore != 1) fail(SCFR_EINVAL, "restore must be 0 (save) or 1 (restore)");
+        set_device(h);
+        Snapshot& sn = h->snap;
+        if (restore && !sn.valid) fail(SCFR_EINVAL, "no snapshot saved");
+        AllocStream alloc_on(h->stream);
+        auto copy = [&](DevBuf<double>& live, DevBuf<double>& saved) {
+            if (!restore && saved.n != live.n) saved.alloc(live.n);
+            if (live.n)
+                CUDA_OK(cudaMemcpyAsync(restore ? live.p : saved.p, restore ? saved.p : live.p,
+                                        live.n * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        };
+        for (int k = 0; k < 2; ++k) {
+            Player& P = h->P[k];
+            DevBuf<double>* live[] = {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.V};
+            for (int a = 0; a < 7; ++a) copy(*live[a], sn.buf[k][a]);
+        }
+        if (!restore) {
+            if (!sn.tdev.n) sn.tdev.alloc(1);
+            CUDA_OK(cudaMemcpyAsync(sn.tdev.p, h->tdev.p, sizeof(long long), cudaMemcpyDeviceToDevice, h->stream));
+            sn.t = h->t;
+            sn.avg_weight = h->avg_weight;
+            sn.valid = true;
+        } else {
+            CUDA_OK(cudaMemcpyAsync(h->tdev.p, sn.tdev.p, sizeof(long long), cudaMemcpyDeviceToDevice, h->stream));
+            h->t = sn.t;
+            h->avg_weight = sn.avg_weight;
+        }
+    });
+}
+
 int scfr_iterations(const scfr_handle* h, int64_t* out) {
     return guarded([&] {
         if (!h || !out) fail(SCFR_EINVAL, "NULL argument");

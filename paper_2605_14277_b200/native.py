@@ -99,6 +99,7 @@ _SIGS = {
     "scfr_step": ([C.c_void_p, C.c_int64], C.c_int),
     "scfr_engine": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "scfr_synchronize": ([C.c_void_p], C.c_int),
+    "scfr_snapshot": ([C.c_void_p, C.c_int], C.c_int),
     "scfr_iterations": ([C.c_void_p, i64p], C.c_int),
     "scfr_read_average": ([C.c_void_p, C.c_int, C.c_int, f64p], C.c_int),
     "scfr_read_current": ([C.c_void_p, C.c_int, C.c_int, f64p], C.c_int),

@@ -166,6 +166,10 @@ class Solver:
     def synchronize(self) -> None:
         N.check(N.lib().scfr_synchronize(self._h))
 
+    def snapshot(self, restore: bool = False) -> None:
+        """Save (or restore) the whole iteration state in device memory."""
+        N.check(N.lib().scfr_snapshot(self._h, 1 if restore else 0))
+
     @property
     def iterations(self) -> int:
         v = C.c_int64()
@@ -386,28 +390,51 @@ class TargetResult:
 
 def solve_to_target(game, config: SolverConfig, target: float = 1e-4, check_every: int = 1,
                     max_iterations: int = 1_000_000, device: int = 0,
-                    engine: str = "auto", dtype: str = "f64") -> TargetResult:
+                    engine: str = "auto", dtype: str = "f64", stride: int = 16) -> TargetResult:
     """Iterate until the average profile's exploitability is <= target,
     checking every ``check_every`` iterations on the device (time-to-target
     metric of BASELINE.json; the reference computes the same quantity with a
-    checkpointed ``run``, pkg/solvers.py:406-432)."""
-    if target <= 0 or check_every < 1:
-        raise ValueError("target must be > 0 and check_every >= 1")
+    checkpointed ``run``, pkg/solvers.py:406-432).
+
+    With ``check_every=1`` the search is coarse-to-fine: the state is
+    snapshotted on the device, ``stride`` iterations run, one exploitability
+    check; on a hit the snapshot is restored and the last ``stride``
+    iterations replay with a check after each.  The iterates are
+    deterministic, so the result is the exact first iteration that meets
+    the target, with about 1/stride of the best-response checks on the
+    critical path."""
+    if target <= 0 or check_every < 1 or stride < 1:
+        raise ValueError("target must be > 0, check_every >= 1 and stride >= 1")
     bundle = _as_bundle(game)
     s = Solver(bundle, config, device=device, engine=engine, dtype=dtype)
     t0 = time.perf_counter()
     solve_ms = 0.0
     t = checks = 0
     e = math.inf
-    while t < max_iterations:
-        n = min(check_every, max_iterations - t)
+
+    def advance(n):
+        nonlocal solve_ms, t, e, checks
         s.step(n)
         solve_ms += s.last_step_ms()
         t += n
         e = s.exploitability("average")[0]
         checks += 1
-        if e <= target:
-            break
+
+    coarse = check_every == 1 and stride > 1
+    while t < max_iterations and e > target:
+        if not coarse:
+            advance(min(check_every, max_iterations - t))
+            continue
+        k = min(stride, max_iterations - t)
+        s.snapshot()
+        t_start = t
+        advance(k)
+        if e <= target and k > 1:  # the first hit lies in (t_start, t]: replay one by one
+            s.snapshot(restore=True)
+            t = t_start
+            e = math.inf
+            while e > target:
+                advance(1)
     s.check_finite()
     out = TargetResult(e <= target, t, e, time.perf_counter() - t0, solve_ms / 1e3, checks)
     s.close()

@@ -249,3 +249,31 @@ def test_tiled_graph_free_and_profiled_paths_agree(gpu, monkeypatch):
     assert set(prof) >= {"td_avg", "tick"}
     for k in ("avg1", "avg2", "r1", "u2"):
         np.testing.assert_array_equal(_state(a)[k], _state(b)[k])
+
+
+def test_solve_to_target_coarse_to_fine_is_exact(gpu):
+    """Snapshot / replay search finds the same first iteration <= 1e-4 as a
+    check after every iteration: Leduc CFR+ @1592 (reference golden run)."""
+    from paper_2605_14277_b200 import solve_to_target
+    want = golden_meta()["runs"]["leduc.cfr+.1592"]["records"][-1]
+    r = solve_to_target(bundle("leduc"), SolverConfig("cfr+"), 1e-4, check_every=1, stride=16)
+    assert r.reached and r.iterations == 1592 and r.exploitability == want["exploitability"]
+    assert r.checks < 1592 // 4
+    r1 = solve_to_target(bundle("leduc"), SolverConfig("cfr+"), 1e-4, check_every=1, stride=1)
+    assert (r1.iterations, r1.exploitability) == (r.iterations, r.exploitability)
+
+
+@pytest.mark.parametrize("engine", ["levels", "persistent", "tiled"])
+def test_snapshot_restore_replays_bit_exact(gpu, engine):
+    rec = golden_meta()["lockstep"]["goof3.pcfr+.alt.60"]
+    s = Solver(bundle(rec["game"]), _cfg(rec), device=gpu, engine=engine)
+    s.step(20)
+    s.snapshot()
+    s.step(rec["iters"] - 20)
+    first = _state(s)
+    s.snapshot(restore=True)
+    assert s.iterations == 20
+    s.step(rec["iters"] - 20)
+    for k, v in _state(s).items():
+        np.testing.assert_array_equal(v, first[k])
+        assert digest(v) == rec["digests"][k], k
