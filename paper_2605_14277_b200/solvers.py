@@ -216,6 +216,8 @@ class Solver:
 
     # -- reads -----------------------------------------------------------------
     def _nseq(self, player: int) -> int:
+        if player not in (1, 2):
+            raise ValueError("player must be 1 or 2")
         return self.bundle.procs[player - 1].num_seqs
 
     def average(self, player: int, solve: int = 0) -> np.ndarray:

@@ -1,0 +1,118 @@
+"""Error behaviour of the C-ABI through the host mirror: the reference's
+exception classes (ValueError for bad arguments, FloatingPointError for
+non-finite values; pkg/solvers.py:62-75, :154-155) and loud failures instead
+of silent fallbacks."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import bundle
+from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, native
+
+pytestmark = pytest.mark.gpu
+
+
+def _raw_create(b, cfg, p1=None, p2=None, U=None, UT=None):
+    L = native.lib()
+    c1, c2, cu, cut = b._c
+    h = C.c_void_p()
+    return L.scfr_create(C.byref(p1 or c1), C.byref(p2 or c2), C.byref(U or cu), C.byref(UT or cut),
+                         C.byref(cfg), 0, C.byref(h)), h
+
+
+def _cfg(**kw):
+    cfg = native.Config()
+    cfg.variant, cfg.mode, cfg.batch = 0, 0, 1
+    cfg.alpha, cfg.beta, cfg.gamma = 1.5, 0.0, 0.0
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+def test_bad_config_values(gpu):
+    b = bundle("kuhn")
+    for kw in ({"variant": 9}, {"mode": 3}, {"batch": 0}, {"engine": 42}, {"dtype": 7}, {"gamma": -1.0},
+               {"alpha": float("nan")}):
+        rc, _ = _raw_create(b, _cfg(**kw))
+        assert rc == native.EINVAL, kw
+        assert native.lib().scfr_last_error()
+
+
+def test_dimension_mismatch(gpu):
+    kuhn, leduc = bundle("kuhn"), bundle("leduc")
+    rc, _ = _raw_create(kuhn, _cfg(), U=leduc._c[2])
+    assert rc == native.EINVAL
+    assert b"dimension" in native.lib().scfr_last_error()
+
+
+def test_corrupt_decision_process_rejected(gpu):
+    b = bundle("leduc")
+    p = b.procs[0]
+    bad = np.array(p.dp_first_seq, dtype=np.int64)
+    bad[5] += 1  # not contiguous in j
+    t = p.as_c()
+    t.dp_first_seq = bad.ctypes.data_as(C.POINTER(C.c_int64))
+    rc, _ = _raw_create(b, _cfg(), p1=t)
+    assert rc == native.EINVAL
+    assert b"contiguous" in native.lib().scfr_last_error()
+    par = np.array(p.dp_parent_seq, dtype=np.int64)
+    par[7] = p.num_seqs + 3  # parent after its decision point
+    t = p.as_c()
+    t.dp_parent_seq = par.ctypes.data_as(C.POINTER(C.c_int64))
+    rc, _ = _raw_create(b, _cfg(), p1=t)
+    assert rc == native.EINVAL
+
+
+def test_bad_column_index_rejected(gpu):
+    b = bundle("kuhn")
+    U = b.payoff
+    ix = np.array(U.indices, dtype=np.int64)
+    ix[0] = U.cols + 5
+    cu = U.as_c()
+    cu.indices = ix.ctypes.data_as(C.POINTER(C.c_int64))
+    rc, _ = _raw_create(b, _cfg(), U=cu)
+    assert rc == native.EINVAL
+    assert b"column" in native.lib().scfr_last_error()
+
+
+def test_engine_constraints(gpu):
+    b = bundle("leduc")
+    with pytest.raises(ValueError):
+        Solver(b, SolverConfig("cfr"), device=gpu, batch_params=[(1.5, 0, 2)] * 2, engine="persistent_grid")
+    with pytest.raises(ValueError):
+        Solver(bundle("kuhn"), SolverConfig("cfr"), device=gpu, engine="tiled")  # player 2 has one level
+    with pytest.raises(ValueError):
+        Solver(b, SolverConfig("cfr"), device=10_000)
+
+
+def test_read_arguments(gpu):
+    s = Solver(bundle("kuhn"), SolverConfig("cfr"), device=gpu)
+    with pytest.raises(ValueError):
+        s.average(1)  # nothing accumulated yet (the reference divides by zero weight)
+    s.step(3)
+    with pytest.raises(ValueError):
+        s.average(3)
+    with pytest.raises(ValueError):
+        s.average(1, solve=1)
+    with pytest.raises(ValueError):
+        s.best_response_values(np.zeros(4), np.zeros(13))
+    with pytest.raises(ValueError):
+        s.snapshot(restore=True)  # none saved
+    assert s.exploitability()[0] > 0
+
+
+def test_nonfinite_payoffs_raise_floating_point_error(gpu):
+    from paper_2605_14277_b200 import games as G
+    g = G.GameBuilder("inf")
+    top = g.decision(None, None, 1, "p1")
+    for a in ("H", "T"):
+        sub = g.decision(top, a, 2, "p2")
+        for b_ in ("H", "T"):
+            g.terminal(sub, b_, 1.7e308 if a == "H" else -1.7e308)
+    for dtype in ("f64", "f32"):  # fp32 overflows at once: the payoffs round to inf
+        s = Solver(GameBundle(g.build()), SolverConfig("cfr"), device=gpu, dtype=dtype)
+        s.step(8)
+        with pytest.raises(FloatingPointError):
+            s.check_finite()
