@@ -115,6 +115,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def size_matched_copy(device: int, bytes_per_launch: float, achieved_gbs: float) -> dict:
+    """What a bare fp64 device copy moving the dominant kernel's average
+    bytes per launch achieves on this GPU (cold L2, CUDA events, best of 10):
+    the attainable bandwidth at that launch size, reported beside the
+    roofline.  Peak stays MEASURED_PEAKS' 1 GiB copy."""
+    import torch
+    n = max(1, int(bytes_per_launch / 16))  # read + write 8 B each
+    src = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
+    dst = torch.empty_like(src)
+    flush = torch.empty(64 << 20, dtype=torch.float64, device=f"cuda:{device}")  # 512 MB > L2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(10):
+        flush.fill_(1.0)
+        e0.record()
+        dst.copy_(src)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    gbs = 16.0 * n / (best / 1e3) / 1e9
+    del src, dst, flush
+    return {"bytes_per_launch": 16.0 * n, "gbs": gbs, "kernel_frac_of_copy": achieved_gbs / gbs,
+            "how": "torch fp64 copy of the same bytes per launch, L2 flushed, best of 10"}
+
+
 def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: float | None,
                     threads: int, dtype: str = "f64"):
     """The oracle port on the host cores: iterations/sec over a bounded sample."""
@@ -316,6 +341,8 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    copy_ref = size_matched_copy(device, d["bytes"] / max(1, d["launches"]), achieved)
+
     solves = 1 if sharded else ws  # sharded: all ranks advance ONE solve
     value = solves * args.steps / (ms_max / 1e3)
     line = {
@@ -339,6 +366,7 @@ def run_ours(args):
                             f"median of {E2E_REPS} repetitions",
                 "parts": e2e_parts},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                     "size_matched_copy": copy_ref,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,
                      "step": {"algorithmic_bytes": step_bytes, "profiled_ms": prof_ms,
