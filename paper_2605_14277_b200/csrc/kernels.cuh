@@ -235,6 +235,13 @@ __device__ __forceinline__ R rm_prob(R rv, R S, int n) {
 // A non-finite q still raises the FloatingPointError flag; the run aborts
 // there exactly as the reference would.
 
+// leaf_note — a level of single-action DPs whose sequences end the tree
+// (no child DPs) gives, in the PRED pass, V_j = 0.0 + 1.0*((0.0 + m_s) + 0.0)
+// = m_s with -0.0 turned into +0.0.  A parent reads child values either as
+// the lone child (added to 0.0 + u, which is never -0.0) or through a sum
+// that starts from 0.0, so +0.0 and -0.0 give the same bits: the parent can
+// read m_s directly and that PRED level need not run.
+
 // ---------------------------------------------------------------------------
 // OBS: counterfactual values + regret update (+ variant post-op) (+ regret
 // matching of the updated regrets into b for the next iteration).
@@ -316,17 +323,22 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
 template <int MAXA, class Ld, class R>
 __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const R* __restrict__ m,
                                         const R* __restrict__ r, R* __restrict__ b,
-                                        R* __restrict__ V, bool plus) {
+                                        R* __restrict__ V, bool plus, const R* Vc = nullptr) {
+    // Vc: where the child DPs' values are read (default V).  The level engine
+    // points it at the prediction itself when the child level is all
+    // forced moves into end nodes: their V would be exactly 0.0 + m, and a
+    // parent's child sum cannot tell that from m (see leaf_note).
+    const R* Vr = Vc ? Vc : V;
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (T.un == 1) {  // single-action level: b stays R(1) (see single_action_note)
-        const R q = dadd(dadd(R(0), Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), V));
+        const R q = dadd(dadd(R(0), Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), Vr));
         V[j] = dadd(R(0), dmul(R(1), q));
         return;
     }
     if (n <= MAXA) {
         R q[MAXA], bb[MAXA], rr[MAXA];
-        load_q<MAXA, Ld>(T, m, V, s0, n, q);
+        load_q<MAXA, Ld>(T, m, Vr, s0, n, q);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) {
@@ -353,17 +365,17 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const R* __rest
             if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
     } else {
         R E = R(0);
-        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, m, V, s)));
+        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, m, Vr, s)));
         V[j] = E;
         const R negE = dmul(R(-1), dadd(R(0), E));
         R S = R(0);
         for (int s = s0; s < s0 + n; ++s) {
-            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, Vr, s)));
             if (plus) rv = rv > R(0) ? rv : R(0);
             S = dadd(S, rv > R(0) ? rv : R(0));
         }
         for (int s = s0; s < s0 + n; ++s) {
-            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, V, s)));
+            R rv = dadd(Ld::ld(r + s), dadd(negE, qval<Ld>(T, m, Vr, s)));
             if (plus) rv = rv > R(0) ? rv : R(0);
             b[s] = rm_prob(rv, S, n);
         }
@@ -521,11 +533,13 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
 template <class Ld, class R>
 __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const R* __restrict__ m,
                                              const R* __restrict__ r, R* __restrict__ b,
-                                             R* __restrict__ V, bool plus, int lane) {
+                                             R* __restrict__ V, bool plus, int lane,
+                                             const R* Vc = nullptr) {
+    const R* Vr = Vc ? Vc : V;
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
-        if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus);
+        if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus, Vc);
         return;
     }
     R q = R(0), bb = R(0), rr = R(0);
@@ -535,7 +549,7 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const R* _
         const R mm = Ld::ld(m + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
-        q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, V));
+        q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, Vr));
     }
     const R E = lane_seq_sum(dmul(bb, q), n);
     if (lane == 0) V[j] = E;

@@ -274,6 +274,7 @@ struct scfr_handle {
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
+    bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)
     bool wave_ctas_env = false;
     int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;

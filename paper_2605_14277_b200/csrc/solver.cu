@@ -65,6 +65,7 @@ struct TaskT {
     R* V;
     FuseUT<R> fu;  // fu.ip set: OBS computes u from the payoff rows (fused SpMV)
     int fu_sx;     // per-solve stride of fu.x
+    const R* Vc;   // PRED: child values read from here (the prediction; kernels.cuh leaf_note), per-solve stride S
 };
 using Task = TaskT<double>;
 
@@ -116,10 +117,11 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
                 obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
                                    kp.do_rm != 0, kp.nonfinite, fu);
         } else {
+            const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
-                pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane);
+                pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane, Vc);
             else
-                pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0);
+                pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, Vc);
         }
     }
 }
@@ -748,6 +750,15 @@ struct Launcher : LaunchBase {
         return occ * h->num_sms;
     }
 
+    // The deepest level is single-action DPs into end nodes (affine, no child
+    // DPs) and all its DPs hang under the level above (kernels.cuh leaf_note).
+    bool leaf_single(const Player& P) const {
+        const int L = P.levels();
+        if (!h->leaf_skip || L < 2) return false;
+        const DevTree& sh = P.lvl_shape[L - 1];
+        return sh.un == 1 && sh.cn == 0 && P.lvl_nc[L - 2] == P.lvl_nj[L - 1];
+    }
+
     // SpMV fused into OBS unless a player has no decision points (then no
     // OBS level would produce its u) or SCFR_NO_FUSE=1.
     bool fuse_spmv() const { return h->fuse && h->P[0].J > 0 && h->P[1].J > 0; }
@@ -766,9 +777,11 @@ struct Launcher : LaunchBase {
     // One launch over level la of A and level lb of Bp (either may be absent).
     template <class R>
     void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
-               R* xa, R* xb, bool do_rm) {
+               R* xa, R* xb, bool do_rm, const R* vca = nullptr, const R* vcb = nullptr) {
         TaskT<R> t0 = A ? task<R>(*A, la, ua, xa) : TaskT<R>{};
         TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
+        t0.Vc = vca;
+        t1.Vc = vcb;
         if (t0.n == 0 && t1.n == 0) return;
         const bool fused = lk == LK_OBS && fuse_spmv();
         if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
@@ -852,9 +865,21 @@ struct Launcher : LaunchBase {
         const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
         // next_strategy of both players (independent): PRED deep -> shallow,
         // then TD + average shallow -> deep, the two players sharing launches.
-        if (pr)
-            for (int k = 0; k < L; ++k)
-                level<R>(LK_PRED, KK_PRED, &A, LA - 1 - k, &Bp, LB - 1 - k, Au, Bu, Ax, Bx, false);
+        if (pr) {
+            // a deepest level of forced moves into end nodes needs no PRED
+            // launch: its parent level reads the prediction itself (leaf_note)
+            const bool sa = leaf_single(A), sb = leaf_single(Bp);
+            auto vc = [](const Player& P, const R* u) {  // u shifted to index by the leaf level's DP id
+                const DevTree& sh = P.lvl_shape[P.levels() - 1];
+                return u + (sh.s_lo - sh.j_lo);
+            };
+            for (int k = 0; k < L; ++k) {
+                const int la = LA - 1 - k, lb = LB - 1 - k;
+                level<R>(LK_PRED, KK_PRED, &A, sa && la == LA - 1 ? -1 : la, &Bp, sb && lb == LB - 1 ? -1 : lb,
+                         Au, Bu, Ax, Bx, false, sa && la == LA - 2 ? vc(A, Au) : nullptr,
+                         sb && lb == LB - 2 ? vc(Bp, Bu) : nullptr);
+            }
+        }
         for (Player* P : {&A, &Bp})
             if (P->J == 0)
                 launch(KK_TD_AVG, 2.0 * sizeof(R), [&] {
@@ -1138,6 +1163,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->use_graph = !(ng && ng[0] == '1');
         const char* np = std::getenv("SCFR_NO_PDL");
         h->pdl = !(np && np[0] == '1');
+        const char* nls = std::getenv("SCFR_NO_LEAF_SKIP");
+        h->leaf_skip = !(nls && nls[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
         h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
         if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) {
