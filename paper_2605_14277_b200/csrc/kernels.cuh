@@ -251,21 +251,26 @@ template <int MAXA, class Ld, class R>
 __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restrict__ u,
                                        R* __restrict__ r, R* __restrict__ b,
                                        R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
-                                       bool do_rm, int* nonfinite, FuseUT<R> fuse = FuseUT<R>{}) {
+                                       bool do_rm, int* nonfinite, FuseUT<R> fuse = FuseUT<R>{},
+                                       const R* Vc = nullptr, bool skip_v = false) {
+    // Vc: where child values are read (default V; the level engine points it
+    // at u when the child level is a forced leaf level, kernels.cuh
+    // leaf_note).  skip_v: that leaf level itself, whose V nobody reads.
+    const R* Vr = Vc ? Vc : V;
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     bool bad = false;
     if (T.un == 1) {  // single-action level: r and b are constants (see single_action_note)
         const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s0, bad) : Ld::ld(u + s0);
-        const R q = dadd(dadd(R(0), uu), child_sum<Ld>(child_of<Ld>(T, s0), V));
-        V[j] = dadd(R(0), dmul(R(1), q));
+        const R q = dadd(dadd(R(0), uu), child_sum<Ld>(child_of<Ld>(T, s0), Vr));
+        if (!skip_v) V[j] = dadd(R(0), dmul(R(1), q));
         bad |= !isfinite(q);
         if (bad) atomicOr(nonfinite, 1);
         return;
     }
     if (n <= MAXA) {
         R q[MAXA], bb[MAXA], rr[MAXA];
-        load_q<MAXA, Ld>(T, u, V, s0, n, q, fuse, &bad);
+        load_q<MAXA, Ld>(T, u, Vr, s0, n, q, fuse, &bad);
 #pragma unroll
         for (int a = 0; a < MAXA; ++a)
             if (a < n) {
@@ -298,12 +303,12 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
         if (fuse.ip)  // wide DP: materialise u first, then the generic path re-reads it
             for (int s = s0; s < s0 + n; ++s) fused_u<Ld>(fuse, const_cast<R*>(u), s, bad);
         R E = R(0);
-        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, u, V, s)));
+        for (int s = s0; s < s0 + n; ++s) E = dadd(E, dmul(Ld::ld(b + s), qval<Ld>(T, u, Vr, s)));
         V[j] = E;
         const R negE = dmul(R(-1), dadd(R(0), E));
         R S = R(0);
         for (int s = s0; s < s0 + n; ++s) {
-            const R q = qval<Ld>(T, u, V, s);
+            const R q = qval<Ld>(T, u, Vr, s);
             bad |= !isfinite(q);
             const R rv = post_op(dadd(Ld::ld(r + s), dadd(negE, q)), post, pf, nf);
             bad |= !isfinite(rv);
@@ -498,11 +503,12 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
                                             R* __restrict__ r, R* __restrict__ b,
                                             R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
                                             bool do_rm, int* nonfinite, int lane,
-                                            FuseUT<R> fuse = FuseUT<R>{}) {
+                                            FuseUT<R> fuse = FuseUT<R>{}, const R* Vc = nullptr) {
+    const R* Vr = Vc ? Vc : V;
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {  // wider than a warp: single-lane generic path
-        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse);
+        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
         return;
     }
     R q = R(0), bb = R(0), rr = R(0);
@@ -513,7 +519,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
         const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : Ld::ld(u + s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
-        q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, V));
+        q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, Vr));
     }
     const R E = lane_seq_sum(dmul(bb, q), n);
     if (lane == 0) V[j] = E;

@@ -65,7 +65,8 @@ struct TaskT {
     R* V;
     FuseUT<R> fu;  // fu.ip set: OBS computes u from the payoff rows (fused SpMV)
     int fu_sx;     // per-solve stride of fu.x
-    const R* Vc;   // PRED: child values read from here (the prediction; kernels.cuh leaf_note), per-solve stride S
+    const R* Vc;   // OBS / PRED: child values read from here (u / the prediction; kernels.cuh leaf_note), per-solve stride S
+    int skip_v;    // OBS on a forced leaf level whose V nobody reads
 };
 using Task = TaskT<double>;
 
@@ -110,12 +111,13 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
         } else if constexpr (KIND == LK_CUR) {
             cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
+            const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
                 obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                                  kp.do_rm != 0, kp.nonfinite, lane, fu);
+                                  kp.do_rm != 0, kp.nonfinite, lane, fu, Vc);
             else
                 obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
-                                   kp.do_rm != 0, kp.nonfinite, fu);
+                                   kp.do_rm != 0, kp.nonfinite, fu, Vc, t.skip_v != 0);
         } else {
             const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
@@ -777,11 +779,14 @@ struct Launcher : LaunchBase {
     // One launch over level la of A and level lb of Bp (either may be absent).
     template <class R>
     void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
-               R* xa, R* xb, bool do_rm, const R* vca = nullptr, const R* vcb = nullptr) {
+               R* xa, R* xb, bool do_rm, const R* vca = nullptr, const R* vcb = nullptr, int skipa = 0,
+               int skipb = 0) {
         TaskT<R> t0 = A ? task<R>(*A, la, ua, xa) : TaskT<R>{};
         TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
         t0.Vc = vca;
         t1.Vc = vcb;
+        t0.skip_v = skipa;
+        t1.skip_v = skipb;
         if (t0.n == 0 && t1.n == 0) return;
         const bool fused = lk == LK_OBS && fuse_spmv();
         if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
@@ -812,7 +817,7 @@ struct Launcher : LaunchBase {
                 case LK_TD_AVG: bytes += LevelBytes::td(*P, l, true, v); break;
                 case LK_TD: bytes += LevelBytes::td(*P, l, false, v); break;
                 case LK_CUR: bytes += LevelBytes::cur(*P, l, v); break;
-                case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm, v); break;
+                case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm, v) - ((k == 0 ? skipa : skipb) ? v * P->lvl_nj[l] : 0.0); break;
                 default: bytes += LevelBytes::pred(*P, l, v); break;
             }
             if (fused) {  // this level's payoff rows; u is written instead of read
@@ -889,16 +894,24 @@ struct Launcher : LaunchBase {
         for (int k = 0; k < L; ++k)
             level<R>(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, Ax, Bx, false);
         const bool fused = fuse_spmv();
+        // OBS on a forced leaf level: its V equals u (leaf_note), so the
+        // parent level reads u and the leaf launch skips writing V
+        const bool oa = leaf_single(A), ob = leaf_single(Bp);
+        auto leaf_u = [](const Player& P, const R* u) {
+            const DevTree& sh = P.lvl_shape[P.levels() - 1];
+            return u + (sh.s_lo - sh.j_lo);
+        };
         if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
             if (!fused) spmv<R>(h->UT, Ax, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1
             for (int k = 0; k < L; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, Au, Bu, Ax, Bx,
-                         !pr);
+                         !pr, oa && k == 1 ? leaf_u(A, Au) : nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr,
+                         oa && k == 0, ob && k == 0);
         } else {
             for (int k = 0; k < LA; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, Au, nullptr, Ax,
-                         nullptr, !pr);
+                         nullptr, !pr, oa && k == 1 ? leaf_u(A, Au) : nullptr, nullptr, oa && k == 0, 0);
             // current_strategy of player 1 into xpost: RM on the fly
             // (predictive) or TD of the b that OBS already regret-matched
             for (int k = 0; k < LA; ++k)
@@ -907,7 +920,7 @@ struct Launcher : LaunchBase {
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
-                         nullptr, Bx, !pr);
+                         nullptr, Bx, !pr, nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0, ob && k == 0);
         }
         launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p); });
     }
