@@ -138,8 +138,10 @@ struct DevCsr {
         return it != h_rows.end() && *it == row ? h_ptr[it - h_rows.begin()] : 0;
     }
     DevBuf<int> indptr, indices;
+    DevBuf<int> indices_iter;  // iteration copy with forced-leaf columns -> parent columns (solver.cu leaf_x)
     DevBuf<double> data;
     DevBuf<float> data32;  // fp32 mode: the values rounded once
+    const int* iter_indices() const { return indices_iter.p ? indices_iter.p : indices.p; }
 };
 
 // One phase of the persistent program: a DP level of one or both players
@@ -275,6 +277,7 @@ struct scfr_handle {
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
     bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)
+    bool leaf_x = false;    // level engine: forced leaf x / avg are parent copies (solver.cu k_expand_leaf)
     bool wave_ctas_env = false;
     int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;

@@ -676,6 +676,52 @@ static DevTree shaped_tree(const Player& P, int l) {
     return t;
 }
 
+// The deepest level is single-action DPs into end nodes (affine, no child
+// DPs) and all its DPs hang under the level above (kernels.cuh leaf_note).
+static bool leaf_single(const scfr_handle* h, const Player& P) {
+    const int L = P.levels();
+    if (!h->leaf_skip || L < 2) return false;
+    const DevTree& sh = P.lvl_shape[L - 1];
+    return sh.un == 1 && sh.cn == 0 && P.lvl_nc[L - 2] == P.lvl_nj[L - 1];
+}
+
+// Forced leaf sequences carry copies of their parent sequence's x, xpost
+// and avg, bit for bit: x_leaf = 1.0 * x_parent, and avg_leaf accumulates
+// w * x_parent from zero exactly as avg_parent does.  With h->leaf_x the
+// level engine does not run those top-down launches; the opponent's payoff
+// rows read the parent's column instead (DevCsr::iter_indices) and reads
+// restore the copies here.  v: one solve's seq-indexed vector.
+template <class R>
+__global__ void k_expand_leaf(DevTree T, int j_lo, int n, int shift, R* __restrict__ v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int j = j_lo + i;
+    v[j + shift] = v[parent_of<LdL1>(T, j)];
+}
+
+// The iteration's column indices of M when the column player's deepest level
+// is a forced leaf level: leaf columns read the parent sequence instead
+// (whose x / xpost equals the leaf's, k_expand_leaf), so that level's
+// top-down launches can be skipped.  This rank's rows only.
+static void build_iter_indices(scfr_handle* h, const scfr_csr* m, DevCsr& D, const Player& colP) {
+    const int l = colP.levels() - 1;
+    const int j0 = colP.lvl[l], n = colP.lvl[l + 1] - j0;
+    const int s_lo = colP.lvl_shape[l].s_lo, shift = s_lo - j0;
+    const std::vector<int>& par = *colP.h_dp_parent;
+    const int64_t k0 = m->indptr[D.row0];
+    std::vector<int> ix(std::max(D.nnz, 1));
+    parallel_chunks(D.nnz, 1 << 16, [&](int, int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) {
+            int c = (int)m->indices[k0 + k];
+            if (c >= s_lo && c < s_lo + n) c = par[c - shift];
+            ix[k] = c;
+        }
+    });
+    D.indices_iter.alloc(ix.size());
+    CUDA_OK(copy_async(D.indices_iter.p, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+}
+
 // Structure bytes are counted only where the kernel loads them: an affine
 // level (lvl_shape) computes seq_ptr / child / dp_parent arithmetically.
 struct LevelBytes {  // v: bytes per value (8 fp64, 4 in the fp32 mode)
@@ -754,12 +800,7 @@ struct Launcher : LaunchBase {
 
     // The deepest level is single-action DPs into end nodes (affine, no child
     // DPs) and all its DPs hang under the level above (kernels.cuh leaf_note).
-    bool leaf_single(const Player& P) const {
-        const int L = P.levels();
-        if (!h->leaf_skip || L < 2) return false;
-        const DevTree& sh = P.lvl_shape[L - 1];
-        return sh.un == 1 && sh.cn == 0 && P.lvl_nc[L - 2] == P.lvl_nj[L - 1];
-    }
+    bool leaf_single(const Player& P) const { return scfr::leaf_single(h, P); }
 
     // SpMV fused into OBS unless a player has no decision points (then no
     // OBS level would produce its u) or SCFR_NO_FUSE=1.
@@ -792,9 +833,9 @@ struct Launcher : LaunchBase {
         if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
             Player& P1 = h->P[0];
             Player& P2 = h->P[1];
-            t0.fu = FuseUT<R>{h->U.indptr.p, h->U.indices.p, payoff_data<R>(h->U), vals<R>(P2.x), 0};
+            t0.fu = FuseUT<R>{h->U.indptr.p, h->U.iter_indices(), payoff_data<R>(h->U), vals<R>(P2.x), 0};
             t0.fu_sx = P2.S;
-            t1.fu = FuseUT<R>{h->UT.indptr.p, h->UT.indices.p, payoff_data<R>(h->UT),
+            t1.fu = FuseUT<R>{h->UT.indptr.p, h->UT.iter_indices(), payoff_data<R>(h->UT),
                               h->mode == SCFR_MODE_ALT ? vals<R>(P1.xpost) : vals<R>(P1.x), 1};
             t1.fu_sx = P1.S;
         }
@@ -844,7 +885,7 @@ struct Launcher : LaunchBase {
     void spmv(const DevCsr& M, const R* x, int sx, R* out, int so, bool neg) {
         launch(KK_SPMV, LevelBytes::spmv(M, sizeof(R)), [&] {
             dim3 grid(grid_for(M.rows), h->B);
-            run(k_spmv<R>, grid, M.rows, (const int*)M.indptr.p, (const int*)M.indices.p,
+            run(k_spmv<R>, grid, M.rows, (const int*)M.indptr.p, (const int*)M.iter_indices(),
                 payoff_data<R>(M), x, sx, out + M.row0, so, neg ? 1 : 0, h->nonfinite.p);
         });
         if constexpr (sizeof(R) == 8)
@@ -891,8 +932,11 @@ struct Launcher : LaunchBase {
                     run1(k_avg0<R>, dim3(h->B), P->S, (const R*)vals<R>(P->x), vals<R>(P->avg),
                          (const double*)h->wsched.p, h->cap, (const long long*)h->tdev.p);
                 });
+        // forced leaf levels: their x / avg are the parents' (k_expand_leaf)
+        const bool xa = h->leaf_x && leaf_single(A), xb = h->leaf_x && leaf_single(Bp);
         for (int k = 0; k < L; ++k)
-            level<R>(LK_TD_AVG, KK_TD_AVG, &A, k, &Bp, k, nullptr, nullptr, Ax, Bx, false);
+            level<R>(LK_TD_AVG, KK_TD_AVG, &A, xa && k == LA - 1 ? -1 : k, &Bp, xb && k == LB - 1 ? -1 : k,
+                     nullptr, nullptr, Ax, Bx, false);
         const bool fused = fuse_spmv();
         // OBS on a forced leaf level: its V equals u (leaf_note), so the
         // parent level reads u and the leaf launch skips writing V
@@ -915,8 +959,8 @@ struct Launcher : LaunchBase {
             // current_strategy of player 1 into xpost: RM on the fly
             // (predictive) or TD of the b that OBS already regret-matched
             for (int k = 0; k < LA; ++k)
-                level<R>(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, k, nullptr, -1, nullptr, nullptr,
-                         Axp, nullptr, false);
+                level<R>(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : k, nullptr, -1,
+                         nullptr, nullptr, Axp, nullptr, false);
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
@@ -1046,9 +1090,28 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
 
 // Device pointer to the solve's profile component: normalised average
 // (written into xbar) or the last emitted strategy.
+// Restores the forced leaf copies (k_expand_leaf) of x / xpost / avg of
+// one solve before it is read.
+static void expand_leaves(scfr_handle* h, int player, DevBuf<double>& buf, int solve) {
+    Player& P = h->P[player - 1];
+    if (!h->leaf_x || !leaf_single(h, P)) return;
+    const int l = P.levels() - 1;
+    const DevTree T = shaped_tree(P, l);
+    const int j0 = P.lvl[l], n = P.lvl[l + 1] - j0, shift = P.lvl_shape[l].s_lo - j0;
+    if (h->f32)
+        k_expand_leaf<float><<<grid_for(n), TPB, 0, h->stream>>>(T, j0, n, shift, vals<float>(buf) + (size_t)solve * P.S);
+    else
+        k_expand_leaf<double><<<grid_for(n), TPB, 0, h->stream>>>(T, j0, n, shift, buf.p + (size_t)solve * P.S);
+    CUDA_OK(cudaGetLastError());
+}
+
 static const double* profile(scfr_handle* h, int player, int solve, int which) {
     Player& P = h->P[player - 1];
-    if (which == 1) return orig_order(h, player, P.x.p, solve);
+    if (which == 1) {
+        expand_leaves(h, player, P.x, solve);
+        return orig_order(h, player, P.x.p, solve);
+    }
+    expand_leaves(h, player, P.avg, solve);
     if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
     const double* avg = orig_order(h, player, P.avg.p, solve);
     k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
@@ -1197,6 +1260,13 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID ||
             h->engine == SCFR_ENGINE_PERSISTENT_CLUSTER)
             prepare_persistent(h.get());
+        if (h->engine == SCFR_ENGINE_LEVELS && !h->comm) {
+            // forced leaf levels: skip their top-down launches (k_expand_leaf)
+            const bool l1 = leaf_single(h.get(), h->P[0]), l2 = leaf_single(h.get(), h->P[1]);
+            h->leaf_x = l1 || l2;
+            if (l2) build_iter_indices(h.get(), U, h->U, h->P[1]);   // U's columns: player 2's sequences
+            if (l1) build_iter_indices(h.get(), UT, h->UT, h->P[0]);  // Uᵀ's columns: player 1's
+        }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
         stage("engine");
@@ -1380,7 +1450,10 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
             // Non-predictive variants regret-match inside OBS, so this is the
             // behaviour the *next* iteration will play.
             case SCFR_STATE_BEHAVIOR: src = P.b.p; off = 1; cnt = P.S - 1; break;
-            case SCFR_STATE_ACCUM: src = P.avg.p; break;
+            case SCFR_STATE_ACCUM:
+                expand_leaves(h, player, P.avg, solve);
+                src = P.avg.p;
+                break;
             case SCFR_STATE_UTILITY: src = P.u.p; break;
             default: fail(SCFR_EINVAL, "unknown state selector");
         }
@@ -1397,6 +1470,7 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         set_device(h);
         Player& P = h->P[player - 1];
         // avg_accum / avg_weight (IEEE division, as the reference's numpy divide)
+        expand_leaves(h, player, P.avg, solve);
         const double* avg = orig_order(h, player, P.avg.p, solve);
         k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
         CUDA_OK(cudaGetLastError());
@@ -1411,6 +1485,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
         if (h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
         set_device(h);
         Player& P = h->P[player - 1];
+        expand_leaves(h, player, P.x, solve);
         read_to_host(h, host_out, orig_order(h, player, P.x.p, solve), P.S);
     });
 }
