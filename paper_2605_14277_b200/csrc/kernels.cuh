@@ -138,6 +138,14 @@ __device__ __forceinline__ R child_sum(int2 c, const R* __restrict__ V) {
     return child_value<Ld>(c, c.y > 0 ? Ld::ld(V + c.x) : R(0), V);
 }
 
+// Utility / prediction of sequence s.  u == nullptr: the level's payoff rows
+// are structurally empty, so u is the constant ±0.0 (+0.0 player 1, -0.0 =
+// -1.0*0.0 player 2) and every use adds it to 0.0 first: +0.0 either way.
+template <class Ld, class R>
+__device__ __forceinline__ R ld_u(const R* u, int s) {
+    return u ? Ld::ld(u + s) : R(0);
+}
+
 // Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
 template <class Ld, class R>
 __device__ __forceinline__ R spmv_row(const int* __restrict__ indptr,
@@ -193,7 +201,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const R* __restrict__ u
     for (int a = 0; a < MAXA; ++a)
         if (a < n) {
             c[a] = child_of<Ld>(T, s0 + a);
-            uu[a] = f.ip ? fused_u<Ld>(f, const_cast<R*>(u), s0 + a, *bad) : Ld::ld(u + s0 + a);
+            uu[a] = f.ip ? fused_u<Ld>(f, const_cast<R*>(u), s0 + a, *bad) : ld_u<Ld>(u, s0 + a);
         }
 #pragma unroll
     for (int a = 0; a < MAXA; ++a)
@@ -206,7 +214,7 @@ __device__ __forceinline__ void load_q(const DevTree& T, const R* __restrict__ u
 template <class Ld, class R>
 __device__ __forceinline__ R qval(const DevTree& T, const R* __restrict__ u,
                                        const R* __restrict__ V, int s) {
-    return dadd(dadd(R(0), Ld::ld(u + s)), child_sum<Ld>(child_of<Ld>(T, s), V));
+    return dadd(dadd(R(0), ld_u<Ld>(u, s)), child_sum<Ld>(child_of<Ld>(T, s), V));
 }
 
 template <class R>
@@ -261,7 +269,7 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
     dp_range<Ld>(T, j, s0, n);
     bool bad = false;
     if (T.un == 1) {  // single-action level: r and b are constants (see single_action_note)
-        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s0, bad) : Ld::ld(u + s0);
+        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s0, bad) : ld_u<Ld>(u, s0);
         const R q = dadd(dadd(R(0), uu), child_sum<Ld>(child_of<Ld>(T, s0), Vr));
         if (!skip_v) V[j] = dadd(R(0), dmul(R(1), q));
         bad |= !isfinite(q);
@@ -337,7 +345,7 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const R* __rest
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (T.un == 1) {  // single-action level: b stays R(1) (see single_action_note)
-        const R q = dadd(dadd(R(0), Ld::ld(m + s0)), child_sum<Ld>(child_of<Ld>(T, s0), Vr));
+        const R q = dadd(dadd(R(0), ld_u<Ld>(m, s0)), child_sum<Ld>(child_of<Ld>(T, s0), Vr));
         V[j] = dadd(R(0), dmul(R(1), q));
         return;
     }
@@ -516,7 +524,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
     if (lane < n) {
         const int s = s0 + lane;
         const int2 c = child_of<Ld>(T, s);
-        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : Ld::ld(u + s);
+        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : ld_u<Ld>(u, s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
         q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, Vr));
@@ -552,7 +560,7 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const R* _
     if (lane < n) {
         const int s = s0 + lane;
         const int2 c = child_of<Ld>(T, s);
-        const R mm = Ld::ld(m + s);
+        const R mm = ld_u<Ld>(m, s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
         q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, Vr));

@@ -278,6 +278,8 @@ struct scfr_handle {
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
     bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)
     bool leaf_x = false;    // level engine: forced leaf x / avg are parent copies (solver.cu k_expand_leaf)
+    bool u_empty_skip = false;  // levels with empty payoff rows neither compute nor read u (kernels.cuh ld_u)
+    std::vector<std::pair<int, int>> neg_zero_rows;  // player 2 rows {first, count} holding -0.0
     bool wave_ctas_env = false;
     int wave_ctas = 12;  // level-kernel grid cap per task, in CTAs per SM (SCFR_WAVE_CTAS)
     bool timed = false;

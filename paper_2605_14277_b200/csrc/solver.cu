@@ -113,17 +113,17 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
         } else if constexpr (KIND == LK_OBS) {
             const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
-                obs_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                obs_dp_warp<LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post, pf, nf,
                                   kp.do_rm != 0, kp.nonfinite, lane, fu, Vc);
             else
-                obs_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.post, pf, nf,
+                obs_dp<MAXA, LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post, pf, nf,
                                    kp.do_rm != 0, kp.nonfinite, fu, Vc, t.skip_v != 0);
         } else {
             const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
-                pred_dp_warp<LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, lane, Vc);
+                pred_dp_warp<LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.plus != 0, lane, Vc);
             else
-                pred_dp<MAXA, LdL1>(t.T, j, t.u + so, t.r + so, t.b + so, V, kp.plus != 0, Vc);
+                pred_dp<MAXA, LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.plus != 0, Vc);
         }
     }
 }
@@ -722,6 +722,16 @@ static void build_iter_indices(scfr_handle* h, const scfr_csr* m, DevCsr& D, con
     CUDA_OK(cudaStreamSynchronize(h->stream));
 }
 
+// Player 2's structurally empty payoff rows hold u = -1.0 * 0.0 = -0.0 after
+// the first iteration (the reference's scale(-1, Uᵀx)); with u_empty_skip
+// nothing recomputes them, so the first scfr_step writes the constant.
+template <class R>
+__global__ void k_fill_rows(R* __restrict__ u, int S, int B, int lo, int n, R v) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)n * B) return;
+    u[(i / n) * S + lo + i % n] = v;
+}
+
 // Structure bytes are counted only where the kernel loads them: an affine
 // level (lvl_shape) computes seq_ptr / child / dp_parent arithmetically.
 struct LevelBytes {  // v: bytes per value (8 fp64, 4 in the fp32 mode)
@@ -801,6 +811,12 @@ struct Launcher : LaunchBase {
     // The deepest level is single-action DPs into end nodes (affine, no child
     // DPs) and all its DPs hang under the level above (kernels.cuh leaf_note).
     bool leaf_single(const Player& P) const { return scfr::leaf_single(h, P); }
+    // All payoff rows of level l's sequences are empty (level 0: with row 0).
+    static bool rows_empty(const Player& P, int l, const DevCsr& M) {
+        if (l < 0 || l >= P.levels()) return false;
+        const int s0 = l == 0 ? 0 : P.lvl_s0[l], s1 = P.lvl_s0[l] + (int)P.lvl_ns[l];
+        return M.ptr_at(s1) - M.ptr_at(s0) == 0 && M.ptr_at(s1) >= 0;
+    }
 
     // SpMV fused into OBS unless a player has no decision points (then no
     // OBS level would produce its u) or SCFR_NO_FUSE=1.
@@ -828,8 +844,9 @@ struct Launcher : LaunchBase {
         t1.Vc = vcb;
         t0.skip_v = skipa;
         t1.skip_v = skipb;
+        const bool fused_here = lk == LK_OBS && fuse_spmv();
         if (t0.n == 0 && t1.n == 0) return;
-        const bool fused = lk == LK_OBS && fuse_spmv();
+        const bool fused = fused_here;
         if (fused) {  // u1 = U x2 and u2 = -Uᵀ x1 (x1' in alt mode) computed inside OBS
             Player& P1 = h->P[0];
             Player& P2 = h->P[1];
@@ -838,6 +855,21 @@ struct Launcher : LaunchBase {
             t1.fu = FuseUT<R>{h->UT.indptr.p, h->UT.iter_indices(), payoff_data<R>(h->UT),
                               h->mode == SCFR_MODE_ALT ? vals<R>(P1.xpost) : vals<R>(P1.x), 1};
             t1.fu_sx = P1.S;
+        }
+        // levels whose payoff rows are all empty: u is a constant ±0.0
+        // (kernels.cuh ld_u), neither computed nor read
+        bool empty[2] = {false, false};
+        if ((lk == LK_OBS || lk == LK_PRED) && h->u_empty_skip) {
+            empty[0] = A && rows_empty(*A, la, h->U);
+            empty[1] = Bp && rows_empty(*Bp, lb, h->UT);
+            if (empty[0]) {
+                t0.u = nullptr;
+                t0.fu = FuseUT<R>{};
+            }
+            if (empty[1]) {
+                t1.u = nullptr;
+                t1.fu = FuseUT<R>{};
+            }
         }
         const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
                           ((A && fat(*A, la)) || (Bp && fat(*Bp, lb)));
@@ -860,6 +892,10 @@ struct Launcher : LaunchBase {
                 case LK_CUR: bytes += LevelBytes::cur(*P, l, v); break;
                 case LK_OBS: bytes += LevelBytes::obs(*P, l, do_rm, v) - ((k == 0 ? skipa : skipb) ? v * P->lvl_nj[l] : 0.0); break;
                 default: bytes += LevelBytes::pred(*P, l, v); break;
+            }
+            if (empty[k]) {  // no u read / write, no row pointers
+                bytes -= v * P->lvl_ns[l];
+                continue;
             }
             if (fused) {  // this level's payoff rows; u is written instead of read
                 const DevCsr& M = k == 0 ? h->U : h->UT;
@@ -1024,6 +1060,23 @@ static void build_graph(scfr_handle* h) {
 }
 
 static void set_device(const scfr_handle* h) { CUDA_OK(cudaSetDevice(h->device)); }
+
+// Before the first iteration: player 2's structurally empty rows get the
+// -0.0 that iteration would leave in u (k_fill_rows).
+static void preset_constant_rows(scfr_handle* h) {
+    if (h->t != 0) return;
+    for (const auto& rg : h->neg_zero_rows) {
+        const size_t cnt = (size_t)rg.second * h->B;
+        const unsigned grid = (unsigned)((cnt + TPB - 1) / TPB);
+        if (h->f32)
+            k_fill_rows<float><<<grid, TPB, 0, h->stream>>>(vals<float>(h->P[1].u), h->P[1].S, h->B, rg.first,
+                                                            rg.second, -0.0f);
+        else
+            k_fill_rows<double><<<grid, TPB, 0, h->stream>>>(h->P[1].u.p, h->P[1].S, h->B, rg.first, rg.second,
+                                                             -0.0);
+        CUDA_OK(cudaGetLastError());
+    }
+}
 
 // Device -> caller memory for large state reads: DMA into the pinned arena,
 // then a parallel copy out (pageable DMA of a Goofspiel-5 vector is ~3 ms).
@@ -1260,6 +1313,17 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID ||
             h->engine == SCFR_ENGINE_PERSISTENT_CLUSTER)
             prepare_persistent(h.get());
+        if (h->engine == SCFR_ENGINE_LEVELS && !h->comm && h->fuse && h->P[0].J > 0 && h->P[1].J > 0) {
+            // structurally empty payoff rows: u is a constant ±0.0 (kernels.cuh ld_u)
+            const char* nue = std::getenv("SCFR_NO_EMPTY_ROWS");
+            h->u_empty_skip = !(nue && nue[0] == '1');
+            const Player& P2 = h->P[1];
+            for (int l = 0; h->u_empty_skip && l < P2.levels(); ++l)
+                if (Launcher::rows_empty(P2, l, h->UT)) {
+                    const int s0 = l == 0 ? 0 : P2.lvl_s0[l];
+                    h->neg_zero_rows.emplace_back(s0, P2.lvl_s0[l] + (int)P2.lvl_ns[l] - s0);
+                }
+        }
         if (h->engine == SCFR_ENGINE_LEVELS && !h->comm) {
             // forced leaf levels: skip their top-down launches (k_expand_leaf)
             const bool l1 = leaf_single(h.get(), h->P[0]), l2 = leaf_single(h.get(), h->P[1]);
@@ -1311,6 +1375,7 @@ int scfr_step(scfr_handle* h, int64_t n) {
         if (n == 0) return;
         set_device(h);
         add_weights(h, n);
+        preset_constant_rows(h);
         CUDA_OK(cudaEventRecord(h->ev0, h->stream));
         if (is_persistent(h->engine)) {
             h->launches += launch_persistent(h, n);
@@ -1336,6 +1401,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
         if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
         set_device(h);
         add_weights(h, n);
+        preset_constant_rows(h);
         std::vector<KernelRecord> recs;
         int64_t issued = 0;
         if (is_persistent(h->engine)) {
