@@ -21,9 +21,13 @@ namespace scfr {
 
 inline int host_threads() {
     static const int n = [] {
-        // half the cores: a worker descheduled behind another busy thread
-        // stalls the whole split (measured 20+ ms outliers at 16 of 16 vCPUs)
-        int v = (int)std::thread::hardware_concurrency() / 2;
+        // three quarters of the cores: a worker descheduled behind another
+        // busy thread stalls the whole split.  Goofspiel-5 create on a
+        // 16-vCPU B200 host: 16 threads 22-43 ms, 12 threads 20-28 ms,
+        // 8 threads 24-71 ms, 4 threads 27 ms.
+        int v = (int)std::thread::hardware_concurrency() * 3 / 4;
+        // one process per GPU (torchrun): share the host among the local ranks
+        if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) v /= std::max(1, std::atoi(lw));
         if (const char* e = std::getenv("SCFR_HOST_THREADS")) v = std::atoi(e);
         return std::max(1, std::min(v, 32));
     }();

@@ -702,24 +702,25 @@ __global__ void k_expand_leaf(DevTree T, int j_lo, int n, int shift, R* __restri
 // The iteration's column indices of M when the column player's deepest level
 // is a forced leaf level: leaf columns read the parent sequence instead
 // (whose x / xpost equals the leaf's, k_expand_leaf), so that level's
-// top-down launches can be skipped.  This rank's rows only.
-static void build_iter_indices(scfr_handle* h, const scfr_csr* m, DevCsr& D, const Player& colP) {
+// top-down launches can be skipped.  Built on the device from this rank's
+// int32 indices.
+__global__ void k_leaf_columns(int nnz, const int* __restrict__ ix, int* __restrict__ out, DevTree T,
+                               int s_lo, int n, int shift) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    const int c = ix[k];
+    out[k] = c >= s_lo && c < s_lo + n ? parent_of<LdL1>(T, c - shift) : c;
+}
+
+static void build_iter_indices(scfr_handle* h, DevCsr& D, const Player& colP) {
     const int l = colP.levels() - 1;
     const int j0 = colP.lvl[l], n = colP.lvl[l + 1] - j0;
     const int s_lo = colP.lvl_shape[l].s_lo, shift = s_lo - j0;
-    const std::vector<int>& par = *colP.h_dp_parent;
-    const int64_t k0 = m->indptr[D.row0];
-    std::vector<int> ix(std::max(D.nnz, 1));
-    parallel_chunks(D.nnz, 1 << 16, [&](int, int64_t lo, int64_t hi) {
-        for (int64_t k = lo; k < hi; ++k) {
-            int c = (int)m->indices[k0 + k];
-            if (c >= s_lo && c < s_lo + n) c = par[c - shift];
-            ix[k] = c;
-        }
-    });
-    D.indices_iter.alloc(ix.size());
-    CUDA_OK(copy_async(D.indices_iter.p, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
-    CUDA_OK(cudaStreamSynchronize(h->stream));
+    D.indices_iter.alloc(std::max(D.nnz, 1));
+    if (D.nnz)
+        k_leaf_columns<<<grid_for(D.nnz), TPB, 0, h->stream>>>(D.nnz, D.indices.p, D.indices_iter.p,
+                                                               shaped_tree(colP, l), s_lo, n, shift);
+    CUDA_OK(cudaGetLastError());
 }
 
 // Player 2's structurally empty payoff rows hold u = -1.0 * 0.0 = -0.0 after
@@ -1328,8 +1329,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // forced leaf levels: skip their top-down launches (k_expand_leaf)
             const bool l1 = leaf_single(h.get(), h->P[0]), l2 = leaf_single(h.get(), h->P[1]);
             h->leaf_x = l1 || l2;
-            if (l2) build_iter_indices(h.get(), U, h->U, h->P[1]);   // U's columns: player 2's sequences
-            if (l1) build_iter_indices(h.get(), UT, h->UT, h->P[0]);  // Uᵀ's columns: player 1's
+            if (l2) build_iter_indices(h.get(), h->U, h->P[1]);   // U's columns: player 2's sequences
+            if (l1) build_iter_indices(h.get(), h->UT, h->P[0]);  // Uᵀ's columns: player 1's
         }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
