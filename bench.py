@@ -115,6 +115,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def survey_step_bytes(bundle, cfg, v: int = 8) -> int:
+    """SURVEY.md §8(d)'s fused compulsory bytes per iteration (8 B values,
+    4 B indices): per player OBS = 8Σ+40S+20J, NEXT = 8S+12J+24Σ, PRED =
+    8Σ+32S+20J (and OBS drops its b write, −8S), one SpMV each way
+    4(R+1)+12Z+8C+8R, and alt adds NEXT_1 without avg (8S+12J+8Σ).
+    Σ counts the empty sequence, S does not.  Scaled to v-byte values."""
+    Z = bundle.payoff.nnz
+    sig = [p.num_seqs for p in bundle.procs]
+    tot = 0
+    for p, sg in zip(bundle.procs, sig):
+        S, J = sg - 1, p.num_decisions
+        obs = v * sg + 5 * v * S + 20 * J
+        nxt = v * S + 12 * J + 3 * v * sg
+        if cfg.predictive:
+            tot += (obs - v * S) + (v * sg + 4 * v * S + 20 * J) + nxt
+        else:
+            tot += obs + nxt
+    spmv = lambda R, C_: 4 * (R + 1) + (4 + v) * Z + v * C_ + v * R
+    tot += spmv(sig[0], sig[1]) + spmv(sig[1], sig[0])
+    if cfg.mode == "alt":
+        S, J = sig[0] - 1, bundle.procs[0].num_decisions
+        tot += v * S + 12 * J + v * sig[0]
+    return tot
+
+
 def size_matched_copy(device: int, bytes_per_launch: float, achieved_gbs: float) -> dict:
     """What a bare fp64 device copy moving the dominant kernel's average
     bytes per launch achieves on this GPU (cold L2, CUDA events, best of 10):
@@ -342,6 +367,8 @@ def run_ours(args):
             traffic = None
 
     copy_ref = size_matched_copy(device, d["bytes"] / max(1, d["launches"]), achieved)
+    survey_bytes = survey_step_bytes(bundle, cfg, 4 if args.dtype == "f32" else 8)
+    survey_gbs = survey_bytes / (ms_max / args.steps / 1e3) / 1e9
 
     solves = 1 if sharded else ws  # sharded: all ranks advance ONE solve
     value = solves * args.steps / (ms_max / 1e3)
@@ -372,6 +399,12 @@ def run_ours(args):
                      "step": {"algorithmic_bytes": step_bytes, "profiled_ms": prof_ms,
                               "achieved_gbs": step_bytes / (prof_ms / 1e3) / 1e9,
                               "frac": step_bytes / (prof_ms / 1e3) / 1e9 / peak},
+                     "survey_8d": {"algorithmic_bytes_per_step": survey_bytes,
+                                   "achieved_gbs": survey_gbs, "frac": survey_gbs / peak,
+                                   "note": "SURVEY §8(d) fused compulsory bytes over the graph-timed step; "
+                                           "the exact shortcuts (DESIGN §4) skip part of them, so this "
+                                           "overstates bandwidth use: frac above uses the bytes the "
+                                           "kernels load"},
                      "kernels": {k: {"launches": v["launches"] // args.profile_iters,
                                      "ms": v["ms"] / args.profile_iters,
                                      "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
