@@ -301,6 +301,51 @@ static void trace_stage(const char* what) {
     prev = now;
 }
 
+// Coarsens the reference's levels (DPs grouped by node depth) into the
+// fewest contiguous j ranges in which no DP's parent sequence belongs to a DP
+// of the same range.  Every pass only needs that order (TD reads the parent
+// sequence's x, OBS / PRED / BR the child DPs' V), and each DP's arithmetic is
+// unchanged, so the iterates stay bit-identical while a level launch (or a
+// persistent phase) covers more DPs: Liar's dice 12 / 11 -> 7 / 6 levels,
+// Leduc 5 / 5 -> 4 / 4.  Greedy over the node-depth levels: level l joins the
+// current range unless one of its parents is a sequence of that range
+// (sequence s belongs to a DP >= start iff s >= seq_ptr[start]).
+// SCFR_NO_LEVEL_MERGE=1 keeps the node-depth levels.
+static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::vector<int>& dp_parent) {
+    static const bool off = [] {
+        const char* e = std::getenv("SCFR_NO_LEVEL_MERGE");
+        return e && e[0] == '1';
+    }();
+    const int L = (int)P.lvl.size() - 1;
+    if (off || L < 2) return;
+    const int T = host_threads();
+    std::vector<std::vector<int>> cmax(T);
+    parallel_chunks(P.J, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
+        std::vector<int> mx(L, -1);
+        if (lo < hi) {
+            int l = (int)(std::upper_bound(P.lvl.begin(), P.lvl.end(), (int)lo) - P.lvl.begin()) - 1;
+            for (int64_t j = lo; j < hi; ++j) {
+                while (j >= P.lvl[l + 1]) ++l;
+                mx[l] = std::max(mx[l], dp_parent[j]);
+            }
+        }
+        cmax[c] = std::move(mx);
+    });
+    std::vector<int> merged{0};
+    int start = 0;
+    for (int l = 1; l < L; ++l) {
+        int mx = -1;
+        for (const auto& v : cmax)
+            if (!v.empty()) mx = std::max(mx, v[l]);
+        if (mx >= seq_ptr[start]) {
+            start = P.lvl[l];
+            merged.push_back(start);
+        }
+    }
+    merged.push_back(P.J);
+    P.lvl.swap(merged);
+}
+
 // Validates the reference DecisionProcess arrays, builds the int32 device
 // structure (seq_ptr, dp_parent on the host: O(J); child ranges and the
 // initial behaviour on the device: O(S)) and the per-level bookkeeping.
@@ -393,6 +438,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         for (auto& v : starts) P.lvl.insert(P.lvl.end(), v.begin(), v.end());
         P.lvl.push_back(J);
     }
+    merge_levels(P, seq_ptr, dp_parent);
     trace_stage("validate+seq_ptr");
     const int L = (int)P.lvl.size() - 1;
     P.lvl_ns.assign(L, 0);
