@@ -506,6 +506,23 @@ __device__ __forceinline__ R lane_seq_sum(R v, int n) {
     return acc;
 }
 
+// Out-of-line single-lane paths for DPs wider than a warp (rare): kept out
+// of the warp kernels' register allocation (they run at 80 registers so 6
+// CTAs fit per SM).
+template <class Ld, class R>
+__device__ __noinline__ void obs_dp_wide(const DevTree& T, int j, const R* __restrict__ u, R* __restrict__ r,
+                                         R* __restrict__ b, R* __restrict__ V, int post,
+                                         typename nd<R>::type pf, typename nd<R>::type nf, bool do_rm,
+                                         int* nonfinite, FuseUT<R> fuse, const R* Vc) {
+    obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
+}
+template <class Ld, class R>
+__device__ __noinline__ void pred_dp_wide(const DevTree& T, int j, const R* __restrict__ m,
+                                          const R* __restrict__ r, R* __restrict__ b, R* __restrict__ V,
+                                          bool plus, const R* Vc) {
+    pred_dp<1, Ld>(T, j, m, r, b, V, plus, Vc);
+}
+
 template <class Ld, class R>
 __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __restrict__ u,
                                             R* __restrict__ r, R* __restrict__ b,
@@ -516,7 +533,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {  // wider than a warp: single-lane generic path
-        if (lane == 0) obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
+        if (lane == 0) obs_dp_wide<Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
         return;
     }
     R q = R(0), bb = R(0), rr = R(0);
@@ -553,7 +570,7 @@ __device__ __forceinline__ void pred_dp_warp(const DevTree& T, int j, const R* _
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {
-        if (lane == 0) pred_dp<1, Ld>(T, j, m, r, b, V, plus, Vc);
+        if (lane == 0) pred_dp_wide<Ld>(T, j, m, r, b, V, plus, Vc);
         return;
     }
     R q = R(0), bb = R(0), rr = R(0);

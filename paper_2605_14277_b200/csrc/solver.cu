@@ -135,7 +135,7 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
 // already run within ~10% of a bare fp64 stream of the same size on B200,
 // scripts/micro/stream_probe.cu.)
 template <int KIND, int MAXA, bool WARP, class R>
-__global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : 1) k_level(const __grid_constant__ TaskT<R> t0,
+__global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : WARP ? 4 : 1) k_level(const __grid_constant__ TaskT<R> t0,
                                                const __grid_constant__ TaskT<R> t1,
                                                const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
