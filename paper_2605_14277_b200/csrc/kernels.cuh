@@ -418,6 +418,24 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const R* __restri
     }
 }
 
+// TD on a wide level, warp per DP (lane = action): the same per-sequence
+// product and average update as td_dp, with the actions in parallel instead
+// of a serial chain of loads (Liar's dice: up to 12 actions per DP).
+template <class Ld, class R>
+__device__ __forceinline__ void td_dp_warp(const DevTree& T, int j, const R* __restrict__ b,
+                                           R* __restrict__ x, typename nd<R>::type* __restrict__ avg,
+                                           typename nd<R>::type w, int lane) {
+    int s0, n;
+    dp_range<Ld>(T, j, s0, n);
+    const R xp = Ld::ld(x + parent_of<Ld>(T, j));
+    for (int a = lane; a < n; a += 32) {
+        const int s = s0 + a;
+        const R xa = T.un == 1 ? dmul(R(1), xp) : dmul(Ld::ld(b + s), xp);
+        x[s] = xa;
+        if (avg) avg[s] = dadd(dmul(w, xa), Ld::ld(avg + s));
+    }
+}
+
 // CUR: side-effect-free current strategy (pkg/solvers.py:270-291): regret
 // matching on the fly, then the top-down product into x.
 // MAXA: actions held in registers; wider DPs take the generic (recompute) path.

@@ -276,6 +276,7 @@ struct scfr_handle {
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
+    bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)
     bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)
     bool leaf_x = false;    // level engine: forced leaf x / avg are parent copies (solver.cu k_expand_leaf)
     bool u_empty_skip = false;  // levels with empty payoff rows neither compute nor read u (kernels.cuh ld_u)

@@ -93,7 +93,7 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
     FuseUT<R> fu = t.fu;
     if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
     const int first = blk * kPerBlock + (WARP ? (int)threadIdx.x / 32 : (int)threadIdx.x);
-    if (KIND == LK_TD_AVG && first == 0 && t.lo == 0 && t.n > 0) {  // the reference axpy also covers the empty sequence (x[0] = 1)
+    if (KIND == LK_TD_AVG && first == 0 && (!WARP || lane == 0) && t.lo == 0 && t.n > 0) {  // the reference axpy also covers the empty sequence (x[0] = 1)
         R* avg = t.avg + so;
         avg[0] = dadd(dmul(w, t.x[so]), avg[0]);
     }
@@ -105,9 +105,11 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
     for (int item = first; item < t.n; item += stride) {  // warp-uniform in warp mode
         const int j = t.lo + item;
         if constexpr (KIND == LK_TD_AVG) {
-            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w);
+            if constexpr (WARP) td_dp_warp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w, lane);
+            else td_dp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w);
         } else if constexpr (KIND == LK_TD) {
-            td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0));
+            if constexpr (WARP) td_dp_warp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0), lane);
+            else td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0));
         } else if constexpr (KIND == LK_CUR) {
             cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
@@ -167,8 +169,8 @@ static LevelKernelT<R> pick_level_kernel(int kind, int maxa, bool warp) {
 #define SCFR_PICK(K) \
     (m == 0 ? k_level<K, 1, false, R> : m == 1 ? k_level<K, 2, false, R> : m == 2 ? k_level<K, 4, false, R> : k_level<K, 8, false, R>)
     switch (kind) {
-        case LK_TD_AVG: return k_level<LK_TD_AVG, 1, false, R>;
-        case LK_TD: return k_level<LK_TD, 1, false, R>;
+        case LK_TD_AVG: return warp ? k_level<LK_TD_AVG, 1, true, R> : k_level<LK_TD_AVG, 1, false, R>;
+        case LK_TD: return warp ? k_level<LK_TD, 1, true, R> : k_level<LK_TD, 1, false, R>;
         case LK_CUR: return SCFR_PICK(LK_CUR);
         case LK_OBS:
             if (warp) return k_level<LK_OBS, 1, true, R>;
@@ -869,6 +871,10 @@ struct Launcher : LaunchBase {
     // OBS level would produce its u) or SCFR_NO_FUSE=1.
     bool fuse_spmv() const { return h->fuse && h->P[0].J > 0 && h->P[1].J > 0; }
 
+    // Top-down passes go warp-per-DP on levels with >= kWideActions actions.
+    static bool wide(const Player& P, int l) {
+        return l >= 0 && l < P.levels() && P.lvl_maxa[l] >= kWideActions;
+    }
     static bool fat(const Player& P, int l) {
         return l >= 0 && l < P.levels() && warp_level(P, l);
     }
@@ -918,8 +924,9 @@ struct Launcher : LaunchBase {
                 t1.fu = FuseUT<R>{};
             }
         }
-        const bool warp = (lk == LK_OBS || lk == LK_PRED) &&
-                          ((A && fat(*A, la)) || (Bp && fat(*Bp, lb)));
+        const bool warp = (lk == LK_OBS || lk == LK_PRED) ? (A && fat(*A, la)) || (Bp && fat(*Bp, lb))
+                          : (lk == LK_TD_AVG || lk == LK_TD) && h->td_warp &&
+                                ((A && wide(*A, la)) || (Bp && wide(*Bp, lb)));
         const int per = warp ? TPB / 32 : TPB;
         // about one resident wave per task; the blocks grid-stride over the DPs
         const int cap = h->num_sms * h->wave_ctas;
@@ -1341,6 +1348,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->pdl = !(np && np[0] == '1');
         const char* nls = std::getenv("SCFR_NO_LEAF_SKIP");
         h->leaf_skip = !(nls && nls[0] == '1');
+        const char* ntw = std::getenv("SCFR_NO_TD_WARP");
+        h->td_warp = !(ntw && ntw[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
         h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
         if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) {
