@@ -158,8 +158,16 @@ using LevelKernel = LevelKernelT<double>;
 // Wide levels (>= 5 actions somewhere) also go warp-per-DP: the thread path
 // walks a wide DP's actions as a serial chain of L2 round trips (Liar's dice:
 // 12-way bids, ~15 µs per level launch).
+// Small multi-action levels (<= 4096 DPs, at most ~half a wave of warps)
+// too: their launch time is one DP's latency chain, and the thread path
+// serialises the actions' fused payoff rows (Liar's dice: a 1320-DP level
+// with 4 actions took 16 µs as 11 CTAs of threads).
 static bool warp_level(const Player& P, int l) {
-    return (P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l]) ||
+    static const bool small_warp = [] {
+        const char* e = std::getenv("SCFR_NO_SMALL_WARP");
+        return !(e && e[0] == '1');
+    }();
+    return (P.lvl_nj[l] <= 4096 && (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (small_warp && P.lvl_maxa[l] >= 2))) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
