@@ -167,7 +167,11 @@ static bool warp_level(const Player& P, int l) {
         const char* e = std::getenv("SCFR_NO_SMALL_WARP");
         return !(e && e[0] == '1');
     }();
-    return (P.lvl_nj[l] <= 4096 && (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (small_warp && P.lvl_maxa[l] >= 2))) ||
+    static const int64_t max_nj = [] {
+        const char* e = std::getenv("SCFR_WARP_NJ");
+        return e ? std::atoll(e) : 4096;
+    }();
+    return (P.lvl_nj[l] <= max_nj && (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (small_warp && P.lvl_maxa[l] >= 2))) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
