@@ -146,13 +146,10 @@ __device__ __forceinline__ R ld_u(const R* u, int s) {
     return u ? Ld::ld(u + s) : R(0);
 }
 
-// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
+// Entries [k0, k1) of a CSR row: ((0.0 + d0*x0) + d1*x1) + ... in order.
 template <class Ld, class R>
-__device__ __forceinline__ R spmv_row(const int* __restrict__ indptr,
-                                           const int* __restrict__ indices,
-                                           const R* __restrict__ data,
-                                           const R* __restrict__ x, int row) {
-    const int k0 = __ldg(indptr + row), k1 = __ldg(indptr + row + 1);
+__device__ __forceinline__ R spmv_range(const int* __restrict__ indices, const R* __restrict__ data,
+                                        const R* __restrict__ x, int k0, int k1) {
     R acc = R(0);
     int k = k0;
     for (; k + 2 <= k1; k += 2) {
@@ -162,6 +159,15 @@ __device__ __forceinline__ R spmv_row(const int* __restrict__ indptr,
     }
     if (k < k1) acc = dadd(acc, dmul(__ldg(data + k), Ld::ld(x + __ldg(indices + k))));
     return acc;
+}
+
+// Payoff SpMV row: ((0.0 + d0*x[c0]) + d1*x[c1]) + ... (pkg/kernels.py:149-154).
+template <class Ld, class R>
+__device__ __forceinline__ R spmv_row(const int* __restrict__ indptr,
+                                           const int* __restrict__ indices,
+                                           const R* __restrict__ data,
+                                           const R* __restrict__ x, int row) {
+    return spmv_range<Ld>(indices, data, x, __ldg(indptr + row), __ldg(indptr + row + 1));
 }
 
 // Optional fusion of the payoff SpMV into the observe pass: when `ip` is set
@@ -175,12 +181,22 @@ struct FuseUT {
     const R* d;
     const R* x;
     int neg;
+    // rc > 0: every row of this launch's level holds rc non-zeros, so row s
+    // starts at rk0 + (s - rs0) * rc and indptr is not loaded (Goofspiel's
+    // terminal rows: one each).  Same k range, same sum order.
+    int rc = 0, rs0 = 0, rk0 = 0;
 };
 using FuseU = FuseUT<double>;
 
 template <class Ld, class R>
 __device__ __forceinline__ R fused_u(const FuseUT<R>& f, R* u, int s, bool& bad) {
-    R v = spmv_row<Ld>(f.ip, f.ix, f.d, f.x, s);
+    R v;
+    if (f.rc > 0) {
+        const int k0 = f.rk0 + (s - f.rs0) * f.rc;
+        v = spmv_range<Ld>(f.ix, f.d, f.x, k0, k0 + f.rc);
+    } else {
+        v = spmv_row<Ld>(f.ip, f.ix, f.d, f.x, s);
+    }
     if (f.neg) v = dmul(R(-1), v);
     bad |= !isfinite(v);
     u[s] = v;

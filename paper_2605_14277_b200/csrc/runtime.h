@@ -133,6 +133,9 @@ struct DevCsr {
     // per-launch byte accounting of the fused SpMV
     std::vector<int> h_rows;
     std::vector<int64_t> h_ptr;
+    // per level of the row player: the non-zero count every row of the level
+    // shares, else -1 (kernels.cuh FuseUT::rc; unsharded matrices only)
+    std::vector<int> lvl_rowc;
     int64_t ptr_at(int row) const {
         const auto it = std::lower_bound(h_rows.begin(), h_rows.end(), row);
         return it != h_rows.end() && *it == row ? h_ptr[it - h_rows.begin()] : 0;
@@ -276,6 +279,7 @@ struct scfr_handle {
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
+    bool affine_rows = true;  // fused SpMV indexes equal-length level rows without indptr (SCFR_NO_ROW_SHAPE)
     bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)
     bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)
     bool leaf_x = false;    // level engine: forced leaf x / avg are parent copies (solver.cu k_expand_leaf)

@@ -99,7 +99,9 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
     }
     if (KIND == LK_OBS && fu.ip && first == 0 && lane == 0 && t.lo == 0 && t.n > 0) {  // the empty sequence's row: u[0] (next prediction)
         bool bad = false;
-        fused_u<LdL1>(fu, const_cast<R*>(t.u) + so, 0, bad);
+        FuseUT<R> f0 = fu;  // row 0 is outside the level's row shape
+        f0.rc = 0;
+        fused_u<LdL1>(f0, const_cast<R*>(t.u) + so, 0, bad);
         if (bad) atomicOr(kp.nonfinite, 1);
     }
     for (int item = first; item < t.n; item += stride) {  // warp-uniform in warp mode
@@ -631,9 +633,38 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Playe
             D.h_ptr.push_back(m->indptr[r]);
         }
     }
-    parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
+    const int L = rowP.levels();
+    const bool rowc = world == 1 && L > 0;
+    std::vector<std::vector<int>> cmn(host_threads()), cmx(host_threads());
+    parallel_chunks(D.rows + 1, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
         for (int64_t i = lo; i < hi; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
+        if (!rowc) return;
+        // per-level min / max row length (rows of level l: [lvl_s0[l], next level's))
+        std::vector<int> mn(L, INT32_MAX), mx(L, -1);
+        const int64_t e = std::min<int64_t>(hi, D.rows);
+        if (lo < e) {
+            int l = (int)(std::upper_bound(rowP.lvl_s0.begin(), rowP.lvl_s0.end(), (int)lo) - rowP.lvl_s0.begin()) - 1;
+            for (int64_t i = lo; i < e; ++i) {
+                while (l + 1 < L && i >= rowP.lvl_s0[l + 1]) ++l;
+                if (l < 0 || i >= (int64_t)rowP.lvl_s0[l] + rowP.lvl_ns[l]) continue;
+                const int n = (int)(m->indptr[i + 1] - m->indptr[i]);
+                mn[l] = std::min(mn[l], n);
+                mx[l] = std::max(mx[l], n);
+            }
+        }
+        cmn[c] = std::move(mn);
+        cmx[c] = std::move(mx);
     });
+    D.lvl_rowc.assign(rowc ? L : 0, -1);
+    for (int l = 0; l < (int)D.lvl_rowc.size(); ++l) {
+        int mn = INT32_MAX, mx = -1;
+        for (size_t c = 0; c < cmn.size(); ++c)
+            if (!cmn[c].empty()) {
+                mn = std::min(mn, cmn[c][l]);
+                mx = std::max(mx, cmx[c][l]);
+            }
+        if (mx >= 1 && mn == mx) D.lvl_rowc[l] = mx;
+    }
     std::vector<int> badcol(host_threads(), 0);
     parallel_chunks(D.nnz, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; ++k) {
@@ -891,6 +922,15 @@ struct Launcher : LaunchBase {
         return l >= 0 && l < P.levels() && warp_level(P, l);
     }
 
+    // Rows of level l all of one length: index them without indptr.
+    template <class R>
+    static void set_row_shape(FuseUT<R>& f, const DevCsr& M, const Player* P, int l) {
+        if (!P || l < 0 || l >= P->levels() || l >= (int)M.lvl_rowc.size() || M.lvl_rowc[l] < 1) return;
+        f.rc = M.lvl_rowc[l];
+        f.rs0 = P->lvl_s0[l];
+        f.rk0 = (int)M.ptr_at(P->lvl_s0[l]);
+    }
+
     // Payoff values in the handle's arithmetic (fp32 copy in the fp32 mode).
     template <class R>
     const R* payoff_data(const DevCsr& M) const {
@@ -920,6 +960,10 @@ struct Launcher : LaunchBase {
             t1.fu = FuseUT<R>{h->UT.indptr.p, h->UT.iter_indices(), payoff_data<R>(h->UT),
                               h->mode == SCFR_MODE_ALT ? vals<R>(P1.xpost) : vals<R>(P1.x), 1};
             t1.fu_sx = P1.S;
+            if (h->affine_rows) {
+                set_row_shape(t0.fu, h->U, A, la);
+                set_row_shape(t1.fu, h->UT, Bp, lb);
+            }
         }
         // levels whose payoff rows are all empty: u is a constant ±0.0
         // (kernels.cuh ld_u), neither computed nor read
@@ -967,7 +1011,8 @@ struct Launcher : LaunchBase {
                 const DevCsr& M = k == 0 ? h->U : h->UT;
                 const int s0 = P->lvl_s0[l], s1 = s0 + (int)P->lvl_ns[l];
                 const double nnz = (double)(M.ptr_at(s1) - M.ptr_at(s0));
-                bytes += 4.0 * (s1 - s0 + 1) + (4.0 + v) * nnz + v * nnz;
+                const bool shaped = h->affine_rows && l < (int)M.lvl_rowc.size() && M.lvl_rowc[l] >= 1;
+                bytes += (shaped ? 0.0 : 4.0 * (s1 - s0 + 1)) + (4.0 + v) * nnz + v * nnz;
             }
         }
         const LevelKernelT<R> kern = pick_level_kernel<R>(lk, maxa, warp);
@@ -1360,6 +1405,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->pdl = !(np && np[0] == '1');
         const char* nls = std::getenv("SCFR_NO_LEAF_SKIP");
         h->leaf_skip = !(nls && nls[0] == '1');
+        const char* nar = std::getenv("SCFR_NO_ROW_SHAPE");
+        h->affine_rows = !(nar && nar[0] == '1');
         const char* ntw = std::getenv("SCFR_NO_TD_WARP");
         h->td_warp = !(ntw && ntw[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
