@@ -66,6 +66,10 @@ struct LdL2 {
     template <class X>
     static __device__ __forceinline__ X st(const X* p) { return __ldg(p); }
 };
+// L1 loads with a shallow chunk (group mode: 6 CTAs per SM at 80 registers).
+struct LdL1s : LdL1 {
+    static constexpr int kChunk = 8;
+};
 // L2-only loads with a shallow chunk: the tile engine's top pass, which
 // shares a kernel (and so a register budget) with the tile walk.
 struct LdL2s {
@@ -538,6 +542,104 @@ __device__ __forceinline__ R lane_seq_sum(R v, int n) {
     R acc = R(0);
     for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, a));
     return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Group mode: on a big level whose DPs all have n = T.un actions (2..16), a
+// warp runs G = 32/n DPs side by side, lane = (DP g, action a), so that
+// consecutive lanes touch consecutive sequences (coalesced r / b / u / x /
+// avg, and child ranges adjacent across lanes) instead of one thread walking
+// its DP's n sequences.  The per-sequence arithmetic and the in-order sums
+// are those of the thread and warp paths: group_seq_sum adds the group's n
+// lanes from 0.0 in action order.  Every lane of the warp executes the
+// shuffles (n is warp-uniform); `valid` masks the lanes past the level's end
+// and the 32 - G*n idle lanes.
+
+template <class R>
+__device__ __forceinline__ R group_seq_sum(R v, int gb, int n) {
+    R acc = R(0);
+    for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, gb + a));
+    return acc;
+}
+
+template <class Ld, class R>
+__device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
+                                             const R* __restrict__ u, R* __restrict__ r, R* __restrict__ b,
+                                             R* __restrict__ V, int post, typename nd<R>::type pf,
+                                             typename nd<R>::type nf, bool do_rm, int* nonfinite,
+                                             FuseUT<R> fuse, const R* Vc) {
+    const R* Vr = Vc ? Vc : V;
+    const int s = T.s_lo + (j - T.j_lo) * n + a;
+    R q = R(0), bb = R(0), rr = R(0);
+    bool bad = false;
+    if (valid) {
+        const int2 c = child_of<Ld>(T, s);
+        const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : ld_u<Ld>(u, s);
+        bb = Ld::ld(b + s);
+        rr = Ld::ld(r + s);
+        q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, Vr));
+    }
+    const R E = group_seq_sum(dmul(bb, q), gb, n);
+    if (valid && a == 0) V[j] = E;
+    const R negE = dmul(R(-1), dadd(R(0), E));
+    R rv = R(0);
+    if (valid) {
+        bad |= !isfinite(q);
+        rv = post_op(dadd(rr, dadd(negE, q)), post, pf, nf);
+        bad |= !isfinite(rv);
+        r[s] = rv;
+    }
+    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    if (do_rm && valid) b[s] = rm_prob(rv, S, n);
+    if (bad) atomicOr(nonfinite, 1);
+}
+
+template <class Ld, class R>
+__device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
+                                              const R* __restrict__ m, const R* __restrict__ r,
+                                              R* __restrict__ b, R* __restrict__ V, bool plus, const R* Vc) {
+    const R* Vr = Vc ? Vc : V;
+    const int s = T.s_lo + (j - T.j_lo) * n + a;
+    R q = R(0), bb = R(0), rr = R(0);
+    if (valid) {
+        const int2 c = child_of<Ld>(T, s);
+        const R mm = ld_u<Ld>(m, s);
+        bb = Ld::ld(b + s);
+        rr = Ld::ld(r + s);
+        q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, Vr));
+    }
+    const R E = group_seq_sum(dmul(bb, q), gb, n);
+    if (valid && a == 0) V[j] = E;
+    const R negE = dmul(R(-1), dadd(R(0), E));
+    R rv = R(0);
+    if (valid) {
+        rv = dadd(rr, dadd(negE, q));
+        if (plus) rv = rv > R(0) ? rv : R(0);
+    }
+    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    if (valid) b[s] = rm_prob(rv, S, n);
+}
+
+// TD (+ average): x[s] = b[s] * x[parent(j)], avg[s] = w*x[s] + avg[s].
+template <class Ld, class R>
+__device__ __forceinline__ void td_dp_group(const DevTree& T, int j, bool valid, int a, int n,
+                                            const R* __restrict__ b, R* __restrict__ x,
+                                            typename nd<R>::type* __restrict__ avg, typename nd<R>::type w) {
+    if (!valid) return;
+    const int s = T.s_lo + (j - T.j_lo) * n + a;
+    const R xa = dmul(Ld::ld(b + s), Ld::ld(x + parent_of<Ld>(T, j)));
+    x[s] = xa;
+    if (avg) avg[s] = dadd(dmul(w, xa), Ld::ld(avg + s));
+}
+
+// CUR: regret matching on the fly, then the top-down product.
+template <class Ld, class R>
+__device__ __forceinline__ void cur_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
+                                             const R* __restrict__ r, R* __restrict__ x) {
+    const int s = T.s_lo + (j - T.j_lo) * n + a;
+    const R rv = valid ? Ld::ld(r + s) : R(0);
+    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    if (valid) x[s] = dmul(rm_prob(rv, S, n), Ld::ld(x + parent_of<Ld>(T, j)));
 }
 
 // Out-of-line single-lane paths for DPs wider than a warp (rare): kept out

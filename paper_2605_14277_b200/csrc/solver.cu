@@ -132,6 +132,57 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
     }
 }
 
+// Group mode (kernels.cuh): G = 32/n DPs per warp, lane = (DP, action), on
+// big affine levels with n = T.un actions.  The task's warps stride over
+// groups of G DPs; the loop bound is warp-uniform so every lane reaches the
+// shuffles.  Never used on level 0 (the empty sequence's extra work).
+template <int KIND, class R>
+__device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, const KParams& kp) {
+    constexpr int W = TPB / 32;
+    const size_t so = (size_t)blockIdx.y * t.S;
+    R* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
+    const int n = t.T.un, G = 32 / n;
+    const int lane = threadIdx.x & 31, g = lane / n, a = lane - g * n, gb = g * n;
+    R w = R(0), pf = R(1), nf = R(1);
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_OBS && kp.post == POST_DCFR) {
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        pf = (R)kp.pfsched[k];
+        nf = (R)kp.nfsched[k];
+    }
+    FuseUT<R> fu = t.fu;
+    if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
+    const R* Vc = t.Vc ? t.Vc + so : nullptr;
+    for (int wi = blk * W + (int)(threadIdx.x >> 5); wi * G < t.n; wi += t.nblk * W) {
+        const int item = wi * G + g;
+        const bool valid = g < G && item < t.n;
+        const int j = t.lo + (valid ? item : 0);
+        if constexpr (KIND == LK_TD_AVG) {
+            td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, t.avg + so, w);
+        } else if constexpr (KIND == LK_TD) {
+            td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, nullptr, R(0));
+        } else if constexpr (KIND == LK_CUR) {
+            cur_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.r + so, t.x + so);
+        } else if constexpr (KIND == LK_OBS) {
+            obs_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post,
+                               pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc);
+        } else {
+            pred_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
+                                kp.plus != 0, Vc);
+        }
+    }
+}
+
+template <int KIND, class R>
+__global__ void __launch_bounds__(TPB, 6) k_level_g(const __grid_constant__ TaskT<R> t0,
+                                                    const __grid_constant__ TaskT<R> t1,
+                                                    const __grid_constant__ KParams kp) {
+    pdl_launch_dependents();
+    pdl_wait();
+    if ((int)blockIdx.x < t0.nblk) level_body_group<KIND, R>(t0, blockIdx.x, kp);
+    else level_body_group<KIND, R>(t1, blockIdx.x - t0.nblk, kp);
+}
+
 // Narrow variants (<= 2 actions in registers: the deep, bandwidth-bound
 // levels) are held to 40 registers so 12 CTAs fit per SM (more loads in
 // flight); wide / warp variants keep the default budget.  (A batched variant
@@ -175,6 +226,17 @@ static bool warp_level(const Player& P, int l) {
     }();
     return (P.lvl_nj[l] <= max_nj && (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (small_warp && P.lvl_maxa[l] >= 2))) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
+}
+
+template <class R>
+static LevelKernelT<R> pick_group_kernel(int kind) {
+    switch (kind) {
+        case LK_TD_AVG: return k_level_g<LK_TD_AVG, R>;
+        case LK_TD: return k_level_g<LK_TD, R>;
+        case LK_CUR: return k_level_g<LK_CUR, R>;
+        case LK_OBS: return k_level_g<LK_OBS, R>;
+        default: return k_level_g<LK_PRED, R>;
+    }
 }
 
 template <class R>
@@ -983,11 +1045,22 @@ struct Launcher : LaunchBase {
         const bool warp = (lk == LK_OBS || lk == LK_PRED) ? (A && fat(*A, la)) || (Bp && fat(*Bp, lb))
                           : (lk == LK_TD_AVG || lk == LK_TD) && h->td_warp &&
                                 ((A && wide(*A, la)) || (Bp && wide(*Bp, lb)));
+        // group mode: big affine levels of 2..16 actions (both tasks, if two)
+        auto groupable = [&](const Player* P, int l) {
+            return !P || l < 0 || l >= P->levels() ||
+                   (l > 0 && P->lvl_shape[l].un >= 2 && P->lvl_shape[l].un <= 16 && P->lvl_nj[l] > h->group_nj);
+        };
+        const bool group = h->group && !warp && (A || Bp) && groupable(A, la) && groupable(Bp, lb) &&
+                           !(A && la == 0) && !(Bp && lb == 0);
+        auto group_per = [&](const Player* P, int l) {
+            return P && l >= 0 && l < P->levels() ? (TPB / 32) * (32 / P->lvl_shape[l].un) : TPB;
+        };
         const int per = warp ? TPB / 32 : TPB;
         // about one resident wave per task; the blocks grid-stride over the DPs
         const int cap = h->num_sms * h->wave_ctas;
-        t0.nblk = std::min((t0.n + per - 1) / per, cap);
-        t1.nblk = std::min((t1.n + per - 1) / per, cap);
+        const int per0 = group ? group_per(A, la) : per, per1 = group ? group_per(Bp, lb) : per;
+        t0.nblk = std::min((t0.n + per0 - 1) / per0, cap);
+        t1.nblk = std::min((t1.n + per1 - 1) / per1, cap);
         int maxa = 1;
         double bytes = 0.0;
         const double v = sizeof(R);
@@ -1015,7 +1088,7 @@ struct Launcher : LaunchBase {
                 bytes += (shaped ? 0.0 : 4.0 * (s1 - s0 + 1)) + (4.0 + v) * nnz + v * nnz;
             }
         }
-        const LevelKernelT<R> kern = pick_level_kernel<R>(lk, maxa, warp);
+        const LevelKernelT<R> kern = group ? pick_group_kernel<R>(lk) : pick_level_kernel<R>(lk, maxa, warp);
         // grid-stride tasks: cap each at one resident wave of this kernel
         const int wave = resident_ctas(kern);
         t0.nblk = std::min(t0.nblk, wave);
@@ -1405,6 +1478,9 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->pdl = !(np && np[0] == '1');
         const char* nls = std::getenv("SCFR_NO_LEAF_SKIP");
         h->leaf_skip = !(nls && nls[0] == '1');
+        const char* ngr = std::getenv("SCFR_NO_GROUP");
+        h->group = !(ngr && ngr[0] == '1');
+        if (const char* gnj = std::getenv("SCFR_GROUP_NJ")) h->group_nj = std::atoll(gnj);
         const char* nar = std::getenv("SCFR_NO_ROW_SHAPE");
         h->affine_rows = !(nar && nar[0] == '1');
         const char* ntw = std::getenv("SCFR_NO_TD_WARP");

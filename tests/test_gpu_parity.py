@@ -92,6 +92,20 @@ def test_best_response_uniform(gpu):
         assert list(got) == rec["uniform"], name
 
 
+@pytest.mark.parametrize("key", CASES)
+def test_group_mode_bit_exact(gpu, key, monkeypatch):
+    """Level engine with group mode (G = 32/n DPs per warp) forced onto every
+    eligible level (uniform 2..16 actions, below level 0) of the lockstep cases."""
+    monkeypatch.setenv("SCFR_GROUP_NJ", "0")
+    rec = golden_meta()["lockstep"][key]
+    s = Solver(bundle(rec["game"]), _cfg(rec), device=gpu, engine="levels")
+    s.step(rec["iters"])
+    for k, v in _state(s).items():
+        assert digest(v) == rec["digests"][k], (key, k)
+    e, br = s.exploitability("average")
+    assert e == rec["expl"] and list(br) == rec["br_avg"]
+
+
 def test_deterministic_and_graph_free_path_agree(gpu, monkeypatch):
     """The level engine with and without CUDA-graph replay."""
     rec = golden_meta()["lockstep"]["liars3.pcfr+.alt.60"]

@@ -28,6 +28,24 @@ def _bundles(shape):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
+def test_random_trees_group_mode(gpu, shape, monkeypatch):
+    """Group mode forced onto every eligible level, against the oracle."""
+    monkeypatch.setenv("SCFR_GROUP_NJ", "0")
+    b, ob = _bundles(shape)
+    for k, (variant, mode) in enumerate(VARIANTS):
+        iters = 20 + 5 * k
+        o = OracleSolver(ob, variant, mode)
+        o.step(iters)
+        s = Solver(b, SolverConfig(variant, mode=mode), device=gpu, engine="levels")
+        s.step(iters)
+        for pl in (1, 2):
+            np.testing.assert_array_equal(s.regrets(pl), o.regrets(pl), err_msg=f"{shape} {variant}")
+            np.testing.assert_array_equal(s.average(pl), o.average(pl))
+            np.testing.assert_array_equal(s.state(pl, "utility"), o.utility(pl))
+        s.close()
+
+
+@pytest.mark.parametrize("shape", SHAPES)
 def test_random_trees_bit_exact(gpu, shape):
     b, ob = _bundles(shape)
     for k, (variant, mode) in enumerate(VARIANTS):
