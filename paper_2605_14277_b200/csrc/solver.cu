@@ -174,7 +174,7 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
 }
 
 template <int KIND, class R>
-__global__ void __launch_bounds__(TPB, 6) k_level_g(const __grid_constant__ TaskT<R> t0,
+__global__ void __launch_bounds__(TPB, 8) k_level_g(const __grid_constant__ TaskT<R> t0,
                                                     const __grid_constant__ TaskT<R> t1,
                                                     const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
