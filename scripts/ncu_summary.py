@@ -26,7 +26,7 @@ LK = {0: "td_avg", 1: "td", 2: "cur", 3: "obs", 4: "pred"}
 
 
 def kind_of(name: str, predictive: bool) -> str:
-    m = re.search(r"k_level<(\d+)", name)
+    m = re.search(r"k_level(?:_g)?<(\d+)", name)
     if m:
         k = LK[int(m.group(1))]
         if k == "obs" and not predictive:
