@@ -17,6 +17,8 @@
 // graph serves every iteration.
 
 #include <algorithm>
+#include <exception>
+#include <thread>
 #include <atomic>
 #include <chrono>
 #include <memory>
@@ -372,7 +374,7 @@ static void trace_stage(const char* what) {
         return e && e[0] == '1';
     }();
     if (!on) return;
-    static auto prev = std::chrono::steady_clock::now();
+    static thread_local auto prev = std::chrono::steady_clock::now();
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[scfr_create]   %-22s %8.2f ms\n", what,
                  std::chrono::duration<double, std::milli>(now - prev).count());
@@ -424,6 +426,131 @@ static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::
     P.lvl.swap(merged);
 }
 
+// Per-level statistics and exact affine shapes (kernels then compute indices
+// instead of loading them), reduced on the device from seq_ptr, dp_parent and
+// the derived child ranges: widest / narrowest DP, child-DP references per
+// level, whether every DP's parent follows p_lo + (j - j0) / pc, and whether
+// every sequence's child range follows c_lo + (s - s0) * cn.  (On the host
+// this walk over ~5 M DPs and sequences per player cost 2.5 ms at best and
+// up to 70 ms on a busy host.)
+struct LevelStat {
+    int maxa, mina, par_ok, aff_ok;
+    int c0, cfirst0, pc, pad;
+    unsigned long long nc;
+};
+
+__device__ __forceinline__ int find_level(const int* __restrict__ starts, int n, int v) {
+    int lo = 0, hi = n;  // last i with starts[i] <= v
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (starts[mid] <= v) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_level_stats_j(int J, int L, const int* __restrict__ lvl, const int* __restrict__ lvl_s0,
+                                const int* __restrict__ seq_ptr, const int* __restrict__ dp_parent,
+                                const int2* __restrict__ child, LevelStat* __restrict__ st) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool on = j < J;
+    int l = 0, n = 0, ok = 1, lp = -1;
+    if (on) {
+        l = find_level(lvl, L, j);
+        n = seq_ptr[j + 1] - seq_ptr[j];
+        const int j0 = lvl[l], p0 = dp_parent[j0], pc = child[p0].y;
+        const int ps = dp_parent[j];
+        ok = ps == p0 + (j - j0) / pc;
+        if (ps != 0) lp = find_level(lvl_s0, L, ps);
+    }
+    const unsigned full = 0xffffffffu;
+    const int l0 = __shfl_sync(full, l, 0);
+    if (__all_sync(full, !on || l == l0)) {
+        const int mx = (int)__reduce_max_sync(full, on ? (unsigned)n : 0u);
+        const int mn = (int)__reduce_min_sync(full, on ? (unsigned)n : 0xffffffffu);
+        const int ak = (int)__reduce_and_sync(full, on ? (unsigned)ok : 1u);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&st[l0].maxa, mx);
+            atomicMin(&st[l0].mina, mn);
+            if (!ak) atomicAnd(&st[l0].par_ok, 0);
+        }
+    } else if (on) {
+        atomicMax(&st[l].maxa, n);
+        atomicMin(&st[l].mina, n);
+        if (!ok) atomicAnd(&st[l].par_ok, 0);
+    }
+    if (lp >= 0) {
+        const unsigned m = __match_any_sync(__activemask(), lp);
+        if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&st[lp].nc, (unsigned long long)__popc(m));
+    }
+}
+
+__global__ void k_level_stats_s(int S, int L, const int* __restrict__ lvl_s0, const int2* __restrict__ child,
+                                LevelStat* __restrict__ st) {
+    const int q = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    const int l = find_level(lvl_s0, L, q), s0 = lvl_s0[l];
+    const int2 c = child[q], c0 = child[s0];
+    if (!(c.y == c0.y && (c0.y == 0 || c.x == c0.x + (q - s0) * c0.y))) atomicAnd(&st[l].aff_ok, 0);
+}
+
+__global__ void k_level_stats_fin(int L, const int* __restrict__ lvl, const int* __restrict__ lvl_s0,
+                                  const int* __restrict__ dp_parent, const int2* __restrict__ child,
+                                  LevelStat* __restrict__ st) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const int2 c0 = child[lvl_s0[l]];
+    st[l].c0 = c0.y;
+    st[l].cfirst0 = c0.x;
+    st[l].pc = child[dp_parent[lvl[l]]].y;
+}
+
+static void level_shapes(Player& P, const std::vector<int>& seq_ptr, const std::vector<int>& dp_parent,
+                         cudaStream_t s) {
+    const int L = P.levels(), J = P.J, S = P.S;
+    P.lvl_maxa.assign(L, 0);
+    P.lvl_nc.assign(L, 0.0);
+    P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
+    if (L == 0) {
+        CUDA_OK(cudaStreamSynchronize(s));
+        return;
+    }
+    std::vector<int> meta(2 * L + 1);  // lvl[0..L-1], lvl_s0[0..L-1] (+ pad)
+    for (int l = 0; l < L; ++l) {
+        meta[l] = P.lvl[l];
+        meta[L + l] = P.lvl_s0[l];
+    }
+    std::vector<LevelStat> st(L, LevelStat{0, INT32_MAX, 1, 1, 0, 0, 1, 0, 0ull});
+    DevBuf<int> dmeta;
+    DevBuf<LevelStat> dst;
+    dmeta.alloc(meta.size());
+    dst.alloc(L);
+    CUDA_OK(copy_async(dmeta.p, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_OK(copy_async(dst.p, st.data(), L * sizeof(LevelStat), cudaMemcpyHostToDevice, s));
+    if (J > 0)
+        k_level_stats_j<<<grid_for(J), TPB, 0, s>>>(J, L, dmeta.p, dmeta.p + L, P.seq_ptr.p, P.dp_parent.p,
+                                                 P.child.p, dst.p);
+    if (S > 1) k_level_stats_s<<<grid_for(S - 1), TPB, 0, s>>>(S, L, dmeta.p + L, P.child.p, dst.p);
+    k_level_stats_fin<<<grid_for(L), TPB, 0, s>>>(L, dmeta.p, dmeta.p + L, P.dp_parent.p, P.child.p, dst.p);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(copy_async(st.data(), dst.p, L * sizeof(LevelStat), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    for (int l = 0; l < L; ++l) {
+        const LevelStat& t = st[l];
+        P.lvl_maxa[l] = t.maxa;
+        P.lvl_nc[l] = (double)t.nc;
+        DevTree& sh = P.lvl_shape[l];
+        const int j0 = P.lvl[l];
+        sh.j_lo = j0;
+        sh.s_lo = seq_ptr[j0];
+        sh.un = t.mina == t.maxa ? t.maxa : 0;
+        sh.cn = t.aff_ok ? t.c0 : -1;
+        sh.c_lo = t.aff_ok && t.c0 > 0 ? t.cfirst0 : 0;
+        sh.pc = t.par_ok ? t.pc : 0;
+        sh.p_lo = dp_parent[j0];
+    }
+}
+
 // Validates the reference DecisionProcess arrays, builds the int32 device
 // structure (seq_ptr, dp_parent on the host: O(J); child ranges and the
 // initial behaviour on the device: O(S)) and the per-level bookkeeping.
@@ -442,7 +569,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     HostScratch& hs = host_scratch();  // create_impl holds the arena lock
     std::vector<int>& seq_ptr = hs.sp[slot];
     std::vector<int>& dp_parent = hs.par[slot];
-    std::vector<int64_t>& dpd = hs.dpd;  // depth of each DP's node
+    std::vector<int64_t>& dpd = hs.dpd[slot];  // depth of each DP's node
     seq_ptr.resize(J + 1);
     dp_parent.resize(std::max(J, 1));
     dpd.resize(std::max(J, 1));
@@ -530,94 +657,6 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         P.lvl_ns[l] = seq_ptr[j1] - seq_ptr[j0];
         P.lvl_nj[l] = j1 - j0;
     }
-    // Per-level statistics and exact affine shapes (kernels then compute
-    // indices instead of loading them), parallel over j and over sequences.
-    std::vector<int>& ccnt = hs.ccnt;  // child-DP group of each sequence
-    std::vector<int>& cfirst = hs.cfirst;
-    ccnt.resize(S);
-    cfirst.resize(S);
-    parallel_chunks(S, kGrain, [&](int, int64_t lo, int64_t hi) {
-        std::fill(ccnt.begin() + lo, ccnt.begin() + hi, 0);
-        std::fill(cfirst.begin() + lo, cfirst.begin() + hi, -1);
-    });
-    std::vector<int> pc(L, 1);
-    for (int l = 0; l < L; ++l) {
-        const int j0 = P.lvl[l], j1 = P.lvl[l + 1];
-        while (j0 + pc[l] < j1 && dp_parent[j0 + pc[l]] == dp_parent[j0]) ++pc[l];
-    }
-    auto level_of_j = [&](int64_t j) {
-        return (int)(std::upper_bound(P.lvl.begin(), P.lvl.end(), (int)j) - P.lvl.begin()) - 1;
-    };
-    std::vector<std::vector<int>> cmax(T, std::vector<int>(L, 0)), cmin(T, std::vector<int>(L, INT32_MAX)),
-        cpar(T, std::vector<int>(L, 1));
-    std::vector<std::vector<double>> cnc(T, std::vector<double>(L, 0.0));
-    parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
-        // chunk-local accumulators (written back once: no false sharing)
-        std::vector<int> mx(L, 0), mn(L, INT32_MAX), pr(L, 1);
-        std::vector<double> nc(L, 0.0);
-        int l = lo < hi ? level_of_j(lo) : 0;
-        for (int64_t j = lo; j < hi; ++j) {
-            while (j >= P.lvl[l + 1]) ++l;
-            const int a = seq_ptr[j + 1] - seq_ptr[j];
-            mx[l] = std::max(mx[l], a);
-            mn[l] = std::min(mn[l], a);
-            const int ps = dp_parent[j];
-            const int j0 = P.lvl[l];
-            if (ps != dp_parent[j0] + (int)((j - j0) / pc[l])) pr[l] = 0;
-            if (ps != 0) {  // child-DP references per level = DPs whose parent lies in it
-                const int lp = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), ps) - P.lvl_s0.begin()) - 1;
-                if (lp >= 0) nc[lp] += 1;
-            }
-            if (j == 0 || dp_parent[j - 1] != ps) {  // group start: record the group
-                int64_t e = j + 1;
-                while (e < J && dp_parent[e] == ps) ++e;
-                cfirst[ps] = (int)j;
-                ccnt[ps] = (int)(e - j);
-            }
-        }
-        cmax[c] = std::move(mx);
-        cmin[c] = std::move(mn);
-        cpar[c] = std::move(pr);
-        cnc[c] = std::move(nc);
-    });
-    std::vector<std::vector<int>> caff(T, std::vector<int>(L, 1));
-    parallel_chunks(S > 1 ? S - 1 : 0, kGrain, [&](int c, int64_t lo, int64_t hi) {
-        if (lo >= hi) return;
-        std::vector<int> af(L, 1);
-        int l = (int)(std::upper_bound(P.lvl_s0.begin(), P.lvl_s0.end(), (int)(lo + 1)) - P.lvl_s0.begin()) - 1;
-        for (int64_t q1 = lo; q1 < hi; ++q1) {
-            const int q = (int)q1 + 1;  // sequences 1..S-1, level by level
-            while (l + 1 < L && q >= P.lvl_s0[l + 1]) ++l;
-            const int s0 = P.lvl_s0[l], c0 = ccnt[s0];
-            if (!(ccnt[q] == c0 && (c0 == 0 || cfirst[q] == cfirst[s0] + (q - s0) * c0))) af[l] = 0;
-        }
-        caff[c] = std::move(af);
-    });
-    P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
-    for (int l = 0; l < L; ++l) {
-        int mx = 0, mn = INT32_MAX, par = 1, aff = 1;
-        double nc = 0;
-        for (int c = 0; c < T; ++c) {
-            mx = std::max(mx, cmax[c][l]);
-            mn = std::min(mn, cmin[c][l]);
-            par &= cpar[c][l];
-            aff &= caff[c][l];
-            nc += cnc[c][l];
-        }
-        P.lvl_maxa[l] = mx;
-        P.lvl_nc[l] = nc;
-        DevTree& sh = P.lvl_shape[l];
-        const int j0 = P.lvl[l], s0 = seq_ptr[j0];
-        sh.j_lo = j0;
-        sh.s_lo = s0;
-        sh.un = mn == mx ? mx : 0;
-        const int c0 = ccnt[s0];
-        sh.cn = aff ? c0 : -1;
-        sh.c_lo = aff && c0 > 0 ? cfirst[s0] : 0;
-        sh.pc = par ? pc[l] : 0;
-        sh.p_lo = dp_parent[j0];
-    }
-    trace_stage("affine shapes");
     P.seq_ptr.alloc(J + 1);
     P.dp_parent.alloc(std::max(J, 1));
     P.child.alloc(S);
@@ -646,8 +685,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     if (f32) k_init_root<float><<<grid_for(B), TPB, 0, s>>>(S, B, vals<float>(P.x), vals<float>(P.xpost));
     else k_init_root<double><<<grid_for(B), TPB, 0, s>>>(S, B, P.x.p, P.xpost.p);
     CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaStreamSynchronize(s));
-    trace_stage("derive+sync");
+    level_shapes(P, seq_ptr, dp_parent, s);
+    trace_stage("derive+shapes+sync");
     P.h_seq_ptr = &seq_ptr;  // for the tile planner, during this create only
     P.h_dp_parent = &dp_parent;
 }
@@ -672,8 +711,7 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Playe
     trace_stage("upload_csr begin");
     // int32 conversion straight into pinned staging (parallel over rows and
     // nnz), then DMA; pageable host vectors if pinning is unavailable.
-    PinnedArena& pa = pinned_arena();  // create_impl holds pa.lock
-    pa.reset();
+    PinnedArena& pa = pinned_arena();  // create_impl holds pa.lock and reset it
     int* ip = static_cast<int*>(pa.take((size_t)(D.rows + 1) * sizeof(int)));
     int* ix = static_cast<int*>(pa.take((size_t)std::max(D.nnz, 1) * sizeof(int)));
     double* dv = static_cast<double*>(pa.take((size_t)std::max(D.nnz, 1) * sizeof(double)));
@@ -1438,14 +1476,41 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         stage("stream");
         PinnedArena& pa = pinned_arena();
         std::lock_guard<std::mutex> pin_guard(pa.lock);
-        pa.reserve((size_t)std::max(U->rows, UT->rows) * 4 + (size_t)std::max<int64_t>(U->nnz, 1) * 12 + 4096);
-        upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32);
-        stage("player1");
-        upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32);
-        stage("player2");
+        pa.reserve((size_t)(U->rows + UT->rows) * 4 + (size_t)std::max<int64_t>(U->nnz, 1) * 24 + 8192);
+        pa.reset();
         const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
-        upload_csr(U, h->U, h->stream, h->P[0], h->f32, w, rk);
-        upload_csr(UT, h->UT, h->stream, h->P[1], h->f32, w, rk);
+        {
+            // two independent pipelines, each on half the host threads:
+            // player 1 then U (its rows are player 1's sequences), and
+            // player 2 then Uᵀ on a second thread
+            const int half = std::max(1, host_threads() / 2);
+            std::exception_ptr err_b;
+            std::thread tb([&] {
+                try {
+                    tl_host_threads = half;
+                    AllocStream alloc_b(h->stream);
+                    upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32);
+                    upload_csr(UT, h->UT, h->stream, h->P[1], h->f32, w, rk);
+                } catch (...) {
+                    err_b = std::current_exception();
+                }
+            });
+            std::exception_ptr err_a;
+            const int saved = tl_host_threads;
+            try {
+                tl_host_threads = half;
+                upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32);
+                upload_csr(U, h->U, h->stream, h->P[0], h->f32, w, rk);
+            } catch (...) {
+                err_a = std::current_exception();
+            }
+            tl_host_threads = saved;
+            tb.join();
+            if (err_a) std::rethrow_exception(err_a);
+            if (err_b) std::rethrow_exception(err_b);
+            CUDA_OK(cudaStreamSynchronize(h->stream));
+        }
+        stage("players+payoff");
         if (nccl_id) {
             // u and the BR gradient are gathered as world x chunk (padded) vectors
             for (int k = 0; k < 2; ++k) {
