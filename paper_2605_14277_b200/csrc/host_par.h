@@ -152,6 +152,24 @@ struct PinnedArena {
 // Host scratch of scfr_create, grow-only and reused (fresh multi-MB vectors
 // cost more in first-touch page faults than the loops that fill them).
 // Guarded by the pinned arena's lock.
+// Grow-only host vector whose buffer stays page-locked (cudaHostRegister), so
+// the structure uploads DMA straight from it; plain pageable memory if
+// registration fails or SCFR_NO_PINNED=1.
+inline void resize_pinned(std::vector<int>& v, size_t n) {
+    static const bool off = [] {
+        const char* e = std::getenv("SCFR_NO_PINNED");
+        return e && e[0] == '1';
+    }();
+    if (!off && v.capacity() < n) {
+        if (v.data() && v.capacity()) cudaHostUnregister(v.data());
+        std::vector<int>().swap(v);
+        v.reserve(n + n / 8);
+        if (cudaHostRegister(v.data(), v.capacity() * sizeof(int), cudaHostRegisterDefault) != cudaSuccess)
+            cudaGetLastError();  // stays pageable
+    }
+    v.resize(n);
+}
+
 struct HostScratch {  // per player (the two upload pipelines run concurrently)
     std::vector<int> sp[2], par[2];  // int32 seq_ptr / dp_parent
     std::vector<int64_t> dpd[2];     // per DP: depth

@@ -570,8 +570,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     std::vector<int>& seq_ptr = hs.sp[slot];
     std::vector<int>& dp_parent = hs.par[slot];
     std::vector<int64_t>& dpd = hs.dpd[slot];  // depth of each DP's node
-    seq_ptr.resize(J + 1);
-    dp_parent.resize(std::max(J, 1));
+    resize_pinned(seq_ptr, J + 1);  // page-locked: uploaded below
+    resize_pinned(dp_parent, std::max(J, 1));
     dpd.resize(std::max(J, 1));
     // Pass 1 (parallel over j): per-DP checks, int32 conversion.  Each chunk
     // keeps its first offending j; the smallest one is reported.
