@@ -63,10 +63,14 @@ def main():
         d[r[col["Metric Name"]]] = val * scale
     seq = list(launches.values())
     ticks = [i for i, d in enumerate(seq) if "k_tick" in d["name"]]
-    if len(ticks) >= 3:
-        seq = seq[ticks[-3] + 1:ticks[-2] + 1]
-    elif len(ticks) >= 2:
-        seq = seq[ticks[-2] + 1:ticks[-1] + 1]
+    # the last tick-to-tick window holding only iteration kernels (creates,
+    # reads and checks run other kernels between iterations)
+    for a, b in reversed(list(zip(ticks, ticks[1:]))):
+        win = seq[a + 1:b + 1]
+        if all("k_level" in d["name"] or "k_tick" in d["name"] or "k_spmv" in d["name"]
+               or "k_avg0" in d["name"] for d in win):
+            seq = win
+            break
     pred = args.variant in ("pcfr", "pcfr+")
     agg: dict = {}
     for d in seq:
