@@ -280,6 +280,8 @@ struct scfr_handle {
     bool pdl = true;   // programmatic dependent launch between level kernels
     bool fuse = true;  // payoff SpMV fused into the observe pass (level engine)
     bool affine_rows = true;  // fused SpMV indexes equal-length level rows without indptr (SCFR_NO_ROW_SHAPE)
+    bool small_warp = true;   // warp-per-DP on small multi-action levels (SCFR_NO_SMALL_WARP=1: off)
+    int64_t warp_nj = 4096;  // size limit of the fat / small warp rules (SCFR_WARP_NJ)
     bool group = true;
     int64_t group_nj = 4096;  // group mode only above this many DPs per level (SCFR_GROUP_NJ)  // big affine 2..16-action levels run G = 32/n DPs per warp (SCFR_NO_GROUP=1: off)
     bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)

@@ -217,16 +217,9 @@ using LevelKernel = LevelKernelT<double>;
 // too: their launch time is one DP's latency chain, and the thread path
 // serialises the actions' fused payoff rows (Liar's dice: a 1320-DP level
 // with 4 actions took 16 µs as 11 CTAs of threads).
-static bool warp_level(const Player& P, int l) {
-    static const bool small_warp = [] {
-        const char* e = std::getenv("SCFR_NO_SMALL_WARP");
-        return !(e && e[0] == '1');
-    }();
-    static const int64_t max_nj = [] {
-        const char* e = std::getenv("SCFR_WARP_NJ");
-        return e ? std::atoll(e) : 4096;
-    }();
-    return (P.lvl_nj[l] <= max_nj && (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (small_warp && P.lvl_maxa[l] >= 2))) ||
+static bool warp_level(const scfr_handle* h, const Player& P, int l) {
+    return (P.lvl_nj[l] <= h->warp_nj &&
+            (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (h->small_warp && P.lvl_maxa[l] >= 2))) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
@@ -392,10 +385,8 @@ static void trace_stage(const char* what) {
 // (sequence s belongs to a DP >= start iff s >= seq_ptr[start]).
 // SCFR_NO_LEVEL_MERGE=1 keeps the node-depth levels.
 static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::vector<int>& dp_parent) {
-    static const bool off = [] {
-        const char* e = std::getenv("SCFR_NO_LEVEL_MERGE");
-        return e && e[0] == '1';
-    }();
+    const char* e = std::getenv("SCFR_NO_LEVEL_MERGE");  // per create (tests toggle it)
+    const bool off = e && e[0] == '1';
     const int L = (int)P.lvl.size() - 1;
     if (off || L < 2) return;
     const int T = host_threads();
@@ -1018,8 +1009,8 @@ struct Launcher : LaunchBase {
     static bool wide(const Player& P, int l) {
         return l >= 0 && l < P.levels() && P.lvl_maxa[l] >= kWideActions;
     }
-    static bool fat(const Player& P, int l) {
-        return l >= 0 && l < P.levels() && warp_level(P, l);
+    bool fat(const Player& P, int l) const {
+        return l >= 0 && l < P.levels() && warp_level(h, P, l);
     }
 
     // Rows of level l all of one length: index them without indptr.
@@ -1350,7 +1341,7 @@ static double best_response(scfr_handle* h, int player, const double* x_opp) {
     solve_spmv(h, player == 1 ? h->U : h->UT, x_opp, P.g.p, player == 2);
     for (int l = P.levels() - 1; l >= 0; --l) {
         const int lo = P.lvl[l], hi = P.lvl[l + 1];
-        if (warp_level(P, l))
+        if (warp_level(h, P, l))
             k_br_warp<<<(hi - lo + TPB / 32 - 1) / (TPB / 32), TPB, 0, h->stream>>>(shaped_tree(P, l), lo, hi, P.g.p, P.W.p);
         else
             k_br<<<grid_for(hi - lo), TPB, 0, h->stream>>>(shaped_tree(P, l), lo, hi, P.g.p, P.W.p);
@@ -1546,6 +1537,9 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         const char* ngr = std::getenv("SCFR_NO_GROUP");
         h->group = !(ngr && ngr[0] == '1');
         if (const char* gnj = std::getenv("SCFR_GROUP_NJ")) h->group_nj = std::atoll(gnj);
+        const char* nsw = std::getenv("SCFR_NO_SMALL_WARP");
+        h->small_warp = !(nsw && nsw[0] == '1');
+        if (const char* wnj = std::getenv("SCFR_WARP_NJ")) h->warp_nj = std::atoll(wnj);
         const char* nar = std::getenv("SCFR_NO_ROW_SHAPE");
         h->affine_rows = !(nar && nar[0] == '1');
         const char* ntw = std::getenv("SCFR_NO_TD_WARP");
