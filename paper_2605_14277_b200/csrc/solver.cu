@@ -684,8 +684,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
 
 // Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
 // last shard may hold fewer), re-based so local row i is global row0 + i.
-static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Player& rowP, bool f32,
-                       int world = 1, int rank = 0) {
+static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, int world = 1, int rank = 0) {
     if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
     if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
     if (m->indptr[0] != 0 || m->indptr[m->rows] != m->nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
@@ -715,47 +714,9 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Playe
         ix = ixv.data();
         dv = nullptr;
     }
-    D.h_rows.clear();  // level boundaries of the row player (global rows)
-    D.h_ptr.clear();
-    for (int l = 0; l <= rowP.levels(); ++l) {
-        const int r = l < rowP.levels() ? rowP.lvl_s0[l] : rowP.S;
-        if (r >= 0 && r <= m->rows && (D.h_rows.empty() || D.h_rows.back() < r)) {
-            D.h_rows.push_back(r);
-            D.h_ptr.push_back(m->indptr[r]);
-        }
-    }
-    const int L = rowP.levels();
-    const bool rowc = world == 1 && L > 0;
-    std::vector<std::vector<int>> cmn(host_threads()), cmx(host_threads());
-    parallel_chunks(D.rows + 1, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
+    parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
         for (int64_t i = lo; i < hi; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
-        if (!rowc) return;
-        // per-level min / max row length (rows of level l: [lvl_s0[l], next level's))
-        std::vector<int> mn(L, INT32_MAX), mx(L, -1);
-        const int64_t e = std::min<int64_t>(hi, D.rows);
-        if (lo < e) {
-            int l = (int)(std::upper_bound(rowP.lvl_s0.begin(), rowP.lvl_s0.end(), (int)lo) - rowP.lvl_s0.begin()) - 1;
-            for (int64_t i = lo; i < e; ++i) {
-                while (l + 1 < L && i >= rowP.lvl_s0[l + 1]) ++l;
-                if (l < 0 || i >= (int64_t)rowP.lvl_s0[l] + rowP.lvl_ns[l]) continue;
-                const int n = (int)(m->indptr[i + 1] - m->indptr[i]);
-                mn[l] = std::min(mn[l], n);
-                mx[l] = std::max(mx[l], n);
-            }
-        }
-        cmn[c] = std::move(mn);
-        cmx[c] = std::move(mx);
     });
-    D.lvl_rowc.assign(rowc ? L : 0, -1);
-    for (int l = 0; l < (int)D.lvl_rowc.size(); ++l) {
-        int mn = INT32_MAX, mx = -1;
-        for (size_t c = 0; c < cmn.size(); ++c)
-            if (!cmn[c].empty()) {
-                mn = std::min(mn, cmn[c][l]);
-                mx = std::max(mx, cmx[c][l]);
-            }
-        if (mx >= 1 && mn == mx) D.lvl_rowc[l] = mx;
-    }
     std::vector<int> badcol(host_threads(), 0);
     parallel_chunks(D.nnz, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; ++k) {
@@ -784,6 +745,68 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, const Playe
     }
     CUDA_OK(cudaStreamSynchronize(s));
     trace_stage("csr copies+sync");
+}
+
+// Per-level bookkeeping of a CSR whose rows are rowP's sequences: indptr at
+// the level boundaries (byte accounting, empty-row detection) and, for an
+// unsharded matrix, the row length every row of a level shares (FuseUT::rc),
+// reduced on the device from the uploaded int32 indptr.
+__global__ void k_row_len_stats(int rows, int L, const int* __restrict__ lvl_s0, const int* __restrict__ lvl_end,
+                                const int* __restrict__ indptr, int* __restrict__ mn, int* __restrict__ mx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int l = -1, n = 0;
+    if (i < rows && i >= lvl_s0[0]) {
+        l = find_level(lvl_s0, L, i);
+        if (i >= lvl_end[l]) l = -1;
+        else n = indptr[i + 1] - indptr[i];
+    }
+    const unsigned full = 0xffffffffu;
+    const int l0 = __shfl_sync(full, l, 0);
+    if (__all_sync(full, l == l0)) {
+        if (l0 < 0) return;
+        const int a = (int)__reduce_min_sync(full, (unsigned)n), b = (int)__reduce_max_sync(full, (unsigned)n);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(mn + l0, a);
+            atomicMax(mx + l0, b);
+        }
+    } else if (l >= 0) {
+        atomicMin(mn + l, n);
+        atomicMax(mx + l, n);
+    }
+}
+
+static void csr_level_info(const scfr_csr* m, DevCsr& D, const Player& rowP, cudaStream_t s, bool unsharded) {
+    const int L = rowP.levels();
+    D.h_rows.clear();  // level boundaries of the row player (global rows)
+    D.h_ptr.clear();
+    for (int l = 0; l <= L; ++l) {
+        const int r = l < L ? rowP.lvl_s0[l] : rowP.S;
+        if (r >= 0 && r <= m->rows && (D.h_rows.empty() || D.h_rows.back() < r)) {
+            D.h_rows.push_back(r);
+            D.h_ptr.push_back(m->indptr[r]);
+        }
+    }
+    D.lvl_rowc.assign(unsharded ? L : 0, -1);
+    if (!unsharded || L == 0 || D.rows == 0) return;
+    std::vector<int> meta(4 * L);  // lvl_s0, level ends, min (init), max (init)
+    for (int l = 0; l < L; ++l) {
+        meta[l] = rowP.lvl_s0[l];
+        meta[L + l] = rowP.lvl_s0[l] + (int)rowP.lvl_ns[l];
+        meta[2 * L + l] = INT32_MAX;
+        meta[3 * L + l] = -1;
+    }
+    DevBuf<int> dm;
+    dm.alloc(meta.size());
+    CUDA_OK(copy_async(dm.p, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    k_row_len_stats<<<grid_for(D.rows), TPB, 0, s>>>(D.rows, L, dm.p, dm.p + L, D.indptr.p, dm.p + 2 * L,
+                                                    dm.p + 3 * L);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(copy_async(meta.data(), dm.p, meta.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    for (int l = 0; l < L; ++l) {
+        const int mn = meta[2 * L + l], mx = meta[3 * L + l];
+        if (mx >= 1 && mn == mx) D.lvl_rowc[l] = mx;
+    }
 }
 
 // --- NCCL (loaded at run time; only the row-sharded mode needs it) -------
@@ -1474,31 +1497,33 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // two independent pipelines, each on half the host threads:
             // player 1 then U (its rows are player 1's sequences), and
             // player 2 then Uᵀ on a second thread
-            const int half = std::max(1, host_threads() / 2);
-            std::exception_ptr err_b;
-            std::thread tb([&] {
+            const int quarter = std::max(1, host_threads() / 4);
+            std::exception_ptr err[4];
+            auto task = [&](int k) {
                 try {
-                    tl_host_threads = half;
-                    AllocStream alloc_b(h->stream);
-                    upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32);
-                    upload_csr(UT, h->UT, h->stream, h->P[1], h->f32, w, rk);
+                    tl_host_threads = quarter;
+                    AllocStream alloc_k(h->stream);
+                    switch (k) {
+                        case 0: upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32); break;
+                        case 1: upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32); break;
+                        case 2: upload_csr(U, h->U, h->stream, h->f32, w, rk); break;
+                        default: upload_csr(UT, h->UT, h->stream, h->f32, w, rk); break;
+                    }
                 } catch (...) {
-                    err_b = std::current_exception();
+                    err[k] = std::current_exception();
                 }
-            });
-            std::exception_ptr err_a;
+            };
+            std::thread t1(task, 1), t2(task, 2), t3(task, 3);
             const int saved = tl_host_threads;
-            try {
-                tl_host_threads = half;
-                upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32);
-                upload_csr(U, h->U, h->stream, h->P[0], h->f32, w, rk);
-            } catch (...) {
-                err_a = std::current_exception();
-            }
+            task(0);
             tl_host_threads = saved;
-            tb.join();
-            if (err_a) std::rethrow_exception(err_a);
-            if (err_b) std::rethrow_exception(err_b);
+            t1.join();
+            t2.join();
+            t3.join();
+            for (auto& e : err)
+                if (e) std::rethrow_exception(e);
+            csr_level_info(U, h->U, h->P[0], h->stream, w == 1);  // U's rows: player 1's sequences
+            csr_level_info(UT, h->UT, h->P[1], h->stream, w == 1);
             CUDA_OK(cudaStreamSynchronize(h->stream));
         }
         stage("players+payoff");
