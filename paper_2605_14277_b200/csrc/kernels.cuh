@@ -280,7 +280,10 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
                                        R* __restrict__ r, R* __restrict__ b,
                                        R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
                                        bool do_rm, int* nonfinite, FuseUT<R> fuse = FuseUT<R>{},
-                                       const R* Vc = nullptr, bool skip_v = false) {
+                                       const R* Vc = nullptr, bool skip_v = false, R* bw = nullptr) {
+    // bw: where regret matching writes (default b; CUR's matched strategy in
+    // the predictive alt mode, solver.cu bcur)
+    R* const bo = bw ? bw : b;
     // Vc: where child values are read (default V; the level engine points it
     // at u when the child level is a forced leaf level, kernels.cuh
     // leaf_note).  skip_v: that leaf level itself, whose V nobody reads.
@@ -325,7 +328,7 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
         if (do_rm) {
 #pragma unroll
             for (int a = 0; a < MAXA; ++a)
-                if (a < n) b[s0 + a] = rm_prob(rr[a], S, n);
+                if (a < n) bo[s0 + a] = rm_prob(rr[a], S, n);
         }
     } else {
         if (fuse.ip)  // wide DP: materialise u first, then the generic path re-reads it
@@ -344,7 +347,7 @@ __device__ __forceinline__ void obs_dp(const DevTree& T, int j, const R* __restr
             S = dadd(S, rv > R(0) ? rv : R(0));
         }
         if (do_rm)
-            for (int s = s0; s < s0 + n; ++s) b[s] = rm_prob(Ld::ld(r + s), S, n);
+            for (int s = s0; s < s0 + n; ++s) bo[s] = rm_prob(Ld::ld(r + s), S, n);
     }
     if (bad) atomicOr(nonfinite, 1);
 }
@@ -567,7 +570,7 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
                                              const R* __restrict__ u, R* __restrict__ r, R* __restrict__ b,
                                              R* __restrict__ V, int post, typename nd<R>::type pf,
                                              typename nd<R>::type nf, bool do_rm, int* nonfinite,
-                                             FuseUT<R> fuse, const R* Vc) {
+                                             FuseUT<R> fuse, const R* Vc, R* bw = nullptr) {
     const R* Vr = Vc ? Vc : V;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
     R q = R(0), bb = R(0), rr = R(0);
@@ -590,7 +593,7 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
         r[s] = rv;
     }
     const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
-    if (do_rm && valid) b[s] = rm_prob(rv, S, n);
+    if (do_rm && valid) (bw ? bw : b)[s] = rm_prob(rv, S, n);
     if (bad) atomicOr(nonfinite, 1);
 }
 
@@ -649,8 +652,8 @@ template <class Ld, class R>
 __device__ __noinline__ void obs_dp_wide(const DevTree& T, int j, const R* __restrict__ u, R* __restrict__ r,
                                          R* __restrict__ b, R* __restrict__ V, int post,
                                          typename nd<R>::type pf, typename nd<R>::type nf, bool do_rm,
-                                         int* nonfinite, FuseUT<R> fuse, const R* Vc) {
-    obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
+                                         int* nonfinite, FuseUT<R> fuse, const R* Vc, R* bw) {
+    obs_dp<1, Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc, false, bw);
 }
 template <class Ld, class R>
 __device__ __noinline__ void pred_dp_wide(const DevTree& T, int j, const R* __restrict__ m,
@@ -664,12 +667,13 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
                                             R* __restrict__ r, R* __restrict__ b,
                                             R* __restrict__ V, int post, typename nd<R>::type pf, typename nd<R>::type nf,
                                             bool do_rm, int* nonfinite, int lane,
-                                            FuseUT<R> fuse = FuseUT<R>{}, const R* Vc = nullptr) {
+                                            FuseUT<R> fuse = FuseUT<R>{}, const R* Vc = nullptr,
+                                            R* bw = nullptr) {
     const R* Vr = Vc ? Vc : V;
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     if (n > 32) {  // wider than a warp: single-lane generic path
-        if (lane == 0) obs_dp_wide<Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc);
+        if (lane == 0) obs_dp_wide<Ld>(T, j, u, r, b, V, post, pf, nf, do_rm, nonfinite, fuse, Vc, bw);
         return;
     }
     R q = R(0), bb = R(0), rr = R(0);
@@ -693,7 +697,7 @@ __device__ __forceinline__ void obs_dp_warp(const DevTree& T, int j, const R* __
         r[s0 + lane] = rv;
     }
     const R S = lane_seq_sum(rv > R(0) ? rv : R(0), n);
-    if (do_rm && lane < n) b[s0 + lane] = rm_prob(rv, S, n);
+    if (do_rm && lane < n) (bw ? bw : b)[s0 + lane] = rm_prob(rv, S, n);
     if (__any_sync(kFullMask, bad) && lane == 0) atomicOr(nonfinite, 1);
 }
 

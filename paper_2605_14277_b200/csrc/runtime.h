@@ -122,6 +122,7 @@ struct Player {
     DevBuf<double> r, b, x, xpost, avg, u, V;  // batched [B][...]
     DevBuf<double> g, W, xbar;                 // best-response scratch, one solve
     DevBuf<double> wide;                       // fp32 mode: a widened read of one vector
+    DevBuf<double> bcur;                       // player 1, predictive alt mode: OBS's regret matching, read by CUR
     DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
     int levels() const { return (int)lvl.size() - 1; }
 };
@@ -282,6 +283,7 @@ struct scfr_handle {
     bool affine_rows = true;  // fused SpMV indexes equal-length level rows without indptr (SCFR_NO_ROW_SHAPE)
     bool small_warp = true;   // warp-per-DP on small multi-action levels (SCFR_NO_SMALL_WARP=1: off)
     int64_t warp_nj = 4096;  // size limit of the fat / small warp rules (SCFR_WARP_NJ)
+    bool bcur_on = false;  // predictive alt: OBS P1 writes RM(r) to P[0].bcur, CUR is a plain TD (SCFR_NO_BCUR=1: off)
     bool group = true;
     int64_t group_nj = 4096;  // group mode only above this many DPs per level (SCFR_GROUP_NJ)  // big affine 2..16-action levels run G = 32/n DPs per warp (SCFR_NO_GROUP=1: off)
     bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)

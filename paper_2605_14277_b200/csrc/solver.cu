@@ -69,6 +69,7 @@ struct TaskT {
     int fu_sx;     // per-solve stride of fu.x
     const R* Vc;   // OBS / PRED: child values read from here (u / the prediction; kernels.cuh leaf_note), per-solve stride S
     int skip_v;    // OBS on a forced leaf level whose V nobody reads
+    R* bw;         // OBS: regret matching writes here instead of b (bcur)
 };
 using Task = TaskT<double>;
 
@@ -120,10 +121,11 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
             const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
                 obs_dp_warp<LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post, pf, nf,
-                                  kp.do_rm != 0, kp.nonfinite, lane, fu, Vc);
+                                  kp.do_rm != 0, kp.nonfinite, lane, fu, Vc, t.bw ? t.bw + so : nullptr);
             else
                 obs_dp<MAXA, LdL1>(t.T, j, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post, pf, nf,
-                                   kp.do_rm != 0, kp.nonfinite, fu, Vc, t.skip_v != 0);
+                                   kp.do_rm != 0, kp.nonfinite, fu, Vc, t.skip_v != 0,
+                                   t.bw ? t.bw + so : nullptr);
         } else {
             const R* Vc = t.Vc ? t.Vc + so : nullptr;
             if constexpr (WARP)
@@ -167,7 +169,7 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
             cur_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
             obs_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post,
-                               pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc);
+                               pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc, t.bw ? t.bw + so : nullptr);
         } else {
             pred_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
                                 kp.plus != 0, Vc);
@@ -978,6 +980,9 @@ KParams LaunchBase::kparams(bool do_rm) const {
 
 struct Launcher : LaunchBase {
     explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
+    // predictive alt mode: player 1's OBS regret-matches into bcur (instead
+    // of b, which PRED still needs) and CUR reads it as a plain TD
+    void* bcur_ = nullptr;
 
 
     // Task for level l of player P (l outside [0, L) -> empty task).
@@ -1061,6 +1066,10 @@ struct Launcher : LaunchBase {
         TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
         t0.Vc = vca;
         t1.Vc = vcb;
+        if (bcur_ && A == &h->P[0]) {
+            if (lk == LK_OBS) t0.bw = static_cast<R*>(bcur_);
+            else if (lk == LK_TD) t0.b = static_cast<R*>(bcur_);
+        }
         t0.skip_v = skipa;
         t1.skip_v = skipb;
         const bool fused_here = lk == LK_OBS && fuse_spmv();
@@ -1225,14 +1234,18 @@ struct Launcher : LaunchBase {
                          !pr, oa && k == 1 ? leaf_u(A, Au) : nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr,
                          oa && k == 0, ob && k == 0);
         } else {
+            const bool bc = pr && h->bcur_on;
+            if (bc) bcur_ = vals<R>(A.bcur);
             for (int k = 0; k < LA; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, Au, nullptr, Ax,
-                         nullptr, !pr, oa && k == 1 ? leaf_u(A, Au) : nullptr, nullptr, oa && k == 0, 0);
-            // current_strategy of player 1 into xpost: RM on the fly
-            // (predictive) or TD of the b that OBS already regret-matched
+                         nullptr, !pr || bc, oa && k == 1 ? leaf_u(A, Au) : nullptr, nullptr, oa && k == 0, 0);
+            // current_strategy of player 1 into xpost: TD of the b that OBS
+            // already regret-matched (into b, or into bcur for the predictive
+            // variants), or RM on the fly (SCFR_NO_BCUR=1)
             for (int k = 0; k < LA; ++k)
-                level<R>(pr ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : k, nullptr, -1,
-                         nullptr, nullptr, Axp, nullptr, false);
+                level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : k, nullptr,
+                         -1, nullptr, nullptr, Axp, nullptr, false);
+            bcur_ = nullptr;
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
@@ -1598,6 +1611,11 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                     const int s0 = l == 0 ? 0 : P2.lvl_s0[l];
                     h->neg_zero_rows.emplace_back(s0, P2.lvl_s0[l] + (int)P2.lvl_ns[l] - s0);
                 }
+        }
+        if (h->engine == SCFR_ENGINE_LEVELS && predictive(h->variant) && h->mode == SCFR_MODE_ALT) {
+            const char* nb = std::getenv("SCFR_NO_BCUR");
+            h->bcur_on = !(nb && nb[0] == '1');
+            if (h->bcur_on) h->P[0].bcur.alloc(val_slots((size_t)h->P[0].S * h->B, h->f32));
         }
         if (h->engine == SCFR_ENGINE_LEVELS && !h->comm) {
             // forced leaf levels: skip their top-down launches (k_expand_leaf)
