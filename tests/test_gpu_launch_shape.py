@@ -46,3 +46,24 @@ def test_group_mode_same_launches_same_bits(gpu, monkeypatch):
     plain, r_p = _launches(b, cfg)
     assert grouped == plain
     np.testing.assert_array_equal(r_g, r_p)
+
+
+def test_batched_level_engine_group_and_bcur(gpu, monkeypatch):
+    """A batch of PCFR+ alt solves on the level engine, group mode forced onto
+    every eligible level: each solve equals the same solve run alone (the
+    batch offsets of the group kernels and of bcur)."""
+    from conftest import bundle
+    monkeypatch.setenv("SCFR_GROUP_NJ", "0")
+    monkeypatch.setenv("SCFR_NO_SMALL_WARP", "1")
+    b = bundle("goof4")
+    params = [(1.5, 0.0, 2.0), (1.5, 0.0, 1.0), (1.5, 0.0, 0.0)]
+    s = Solver(b, SolverConfig("pcfr+"), engine="levels", batch_params=params)
+    s.step(7)
+    for k, (a, be, g) in enumerate(params):
+        one = Solver(b, SolverConfig("pcfr+", alpha=a, beta=be, gamma=g), engine="levels")
+        one.step(7)
+        for pl in (1, 2):
+            np.testing.assert_array_equal(s.regrets(pl, k), one.regrets(pl))
+            np.testing.assert_array_equal(s.average(pl, k), one.average(pl))
+        one.close()
+    s.close()
