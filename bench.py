@@ -1,23 +1,29 @@
 #!/usr/bin/env python
-"""Benchmark: CFR iterations/sec on the largest single-GPU config.
+"""Benchmark: CFR iterations/sec on the largest config (BASELINE.json configs[3]).
 
 Workload (default): Goofspiel-5 (bids revealed, random prize order, win/loss;
 8 530 656 game nodes, |Σ| = 2 666 026 per player, nnz(U) = 1 728 000), PCFR+
-alternating, gamma = 2, fp64 — BASELINE.json configs[3] on one GPU.  A step is
-one full CFR iteration (reference ``_step``, pkg/solvers.py:351-372).  The
-working set (~1 GB/iteration) is far above the 126 MB L2, so no L2 flush is
-needed between iterations.
+alternating, gamma = 2, fp64.  A step is one full CFR iteration (reference
+``_step``, pkg/solvers.py:351-372).  The working set (~0.4 GB moved per
+iteration) is far above the 126 MB L2, so no L2 flush is needed between
+iterations.  Iterates at 1/2/10/30/50 iterations are bit-identical to the
+reference's own (tests/test_gpu_goof5.py).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload ...]
 
-N > 1 (torchrun, one rank per GPU): every rank runs an independent replica of
-the solve (no collective on the data path; weak scaling), value = all ranks'
-iterations / max-over-ranks device time.
+N = 1: the Goofspiel-5 solve on one GPU.  N > 1 (torchrun, one rank per GPU):
+config 4 — the SAME single solve with the payoff SpMV row-sharded over the
+ranks and an NCCL all-gather of u each iteration (strong scaling; value =
+that solve's iterations/s over the max-over-ranks device time).  Every line
+also carries ``sweep``: config 5, 256 distinct Leduc DCFR(alpha, beta, gamma)
+solves split over the N ranks (no collective), in solve-iterations/s.
 
 ``--impl reference`` times the reference algorithm's CPU implementation on the
-host cores: the C oracle (a port of the reference's per-iteration path,
-oracle/seqcfr_oracle.c, pinned bit-exact to the reference by tests/) with all
-host threads; rank 0 only.
+host cores: the C oracle (oracle/seqcfr_oracle.c, a port of the reference's
+per-iteration path, pinned bit-exact to the reference by tests/) over a bundle
+built by the oracle's own compile step (oracle/seqcfr_tree.c) — no product
+code is loaded.  Serial and all-core runs are both timed and the better one
+is reported; rank 0 only.
 """
 
 from __future__ import annotations
@@ -63,6 +69,46 @@ def make_bundle(kind: str):
     if kind == "leduc":
         return GameBundle(leduc_poker())
     return GameBundle(kuhn_poker())
+
+
+def oracle_bundle(kind: str):
+    """The same game compiled by the oracle's C restatement of the reference
+    compile step (oracle/seqcfr_tree.c): the CPU legs never load the product
+    library.  Kuhn / Leduc trees come from the pure-Python game builders."""
+    from oracle import tree
+    if kind == "goof":
+        return tree.native_bundle("goofspiel", 5)
+    if kind == "liars":
+        return tree.native_bundle("liars_dice", 6)
+    from paper_2605_14277_b200 import games as G  # pure Python (no native code)
+    g = G.leduc_poker() if kind == "leduc" else G.kuhn_poker()
+    return tree.compile_native(g.flatten())
+
+
+def loaded_native_libs() -> list:
+    """Shared objects from this repo mapped into the process (self-check of
+    which native code a leg actually ran)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                p = line.split()[-1]
+                if p.endswith(".so") and p.startswith(ROOT):
+                    out.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -183,28 +229,53 @@ def cpu_oracle_rate(bundle, variant: str, steps: int, warmup: int, budget_s: flo
     return steps / dt, steps, dt
 
 
+def cpu_best_rate(bundle, variant: str, steps: int, warmup: int, budget_s: float | None,
+                  dtype: str = "f64") -> dict:
+    """Serial and all-core runs of the oracle port; the better is the
+    baseline ('the better of serial and parallel[cores]')."""
+    cores = os.cpu_count() or 1
+    runs = {}
+    for th in sorted({1, cores}):
+        rate, n, dt = cpu_oracle_rate(bundle, variant, steps, warmup, budget_s, th, dtype)
+        runs[th] = {"iterations_per_s": rate, "steps": n, "seconds": dt}
+    best = max(runs, key=lambda k: runs[k]["iterations_per_s"])
+    return {"value": runs[best]["iterations_per_s"], "cores": best, "runs": runs,
+            "steps": runs[best]["steps"], "seconds": runs[best]["seconds"]}
+
+
+def sweep_grid():
+    """Config 5: 256 DISTINCT DCFR (alpha, beta, gamma) triples on a fixed
+    grid (gamma refined to reach 256)."""
+    return [(a, b, g) for a in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 8.0)
+            for b in (-1.0, -0.5, 0.0, 0.5) for g in (0.0, 0.5, 1.0, 1.5, 2.0, 2.5, 3.0, 4.0)]
+
+
 def per_game_suite(device: int, cpu: bool) -> dict:
     """BASELINE.json configs on one GPU: iterations/s and time to
     exploitability 1e-4 (the exact first iteration, found by a coarse-to-fine
-    search over device-side snapshots), the 256-solve Leduc DCFR sweep, and the CPU
-    oracle on the same small configs for context."""
+    search over device-side snapshots) for Leduc, Liar's dice and the bench
+    config Goofspiel-5, Kuhn @1000, and the CPU oracle on the same small
+    configs for context (built product-free)."""
     from paper_2605_14277_b200 import Solver, SolverConfig, solve_to_target
 
     out = {}
     for name, kind, variant, check in (("kuhn_cfr", "kuhn", "cfr", None),
                                         ("leduc_cfr+", "leduc", "cfr+", 1),
-                                        ("liars_dice_dcfr", "liars", "dcfr", 1)):
+                                        ("liars_dice_dcfr", "liars", "dcfr", 1),
+                                        ("goofspiel5_pcfr+", "goof", "pcfr+", 1)):
         b = make_bundle(kind)
         cfg = SolverConfig(variant)
         s = Solver(b, cfg, device=device)
         s.step(20)
         s.synchronize()
-        s.step(500)
-        rate = 500 / (s.last_step_ms() / 1e3)
+        n = 100 if kind == "goof" else 500
+        s.step(n)
+        rate = n / (s.last_step_ms() / 1e3)
         rec = {"engine": s.engine, "iterations_per_s": rate}
         s.close()
         if check:
-            r = solve_to_target(b, cfg, 1e-4, check_every=check, device=device)
+            r = solve_to_target(b, cfg, 1e-4, check_every=check, device=device,
+                                max_iterations=20000)
             rec.update({"target": 1e-4, "reached": r.reached, "iterations": r.iterations,
                         "exploitability": r.exploitability, "seconds_wall": r.seconds,
                         "seconds_solve_only": r.solve_seconds, "check_every": check,
@@ -214,24 +285,10 @@ def per_game_suite(device: int, cpu: bool) -> dict:
             s.step(1000)
             rec["exploitability_at_1000"] = s.exploitability("average")[0]
             s.close()
-        if cpu:
-            threads = 1  # small trees: the port is latency-bound, one thread is fastest
-            crate, _, _ = cpu_oracle_rate(b, variant, 200, 3, 5.0, threads)
-            rec["cpu_oracle_iterations_per_s"] = crate
+        if cpu and kind != "goof":
+            crate, _, _ = cpu_oracle_rate(oracle_bundle(kind), variant, 200, 3, 5.0, 1)
+            rec["cpu_oracle_iterations_per_s"] = crate  # small trees: one thread is fastest
         out[name] = rec
-    # config 5: 256 DCFR(alpha, beta, gamma) Leduc solves, one handle
-    grid = [(a, bb, g) for a in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 5.0, 8.0)
-            for bb in (-1.0, -0.5, 0.0, 0.5) for g in (0.0, 1.0, 2.0, 3.0)] * 2
-    b = make_bundle("leduc")
-    s = Solver(b, SolverConfig("dcfr"), device=device, batch_params=grid)
-    s.step(5)
-    s.synchronize()
-    s.step(1000)
-    ms = s.last_step_ms()
-    out["leduc_dcfr_sweep_256"] = {"engine": s.engine, "solves": len(grid), "iterations": 1000,
-                                   "seconds": ms / 1e3,
-                                   "solve_iterations_per_s": len(grid) * 1000 / (ms / 1e3)}
-    s.close()
     return out
 
 
@@ -247,22 +304,60 @@ def run_reference(args):
     if rank != 0:
         return
     desc, kind, variant = WORKLOADS[args.workload]
-    bundle = make_bundle(kind)
-    threads = os.cpu_count() or 1
-    rate, steps, dt = cpu_oracle_rate(bundle, variant, args.steps, args.warmup, None, threads)
+    t0 = time.perf_counter()
+    bundle = oracle_bundle(kind)
+    build_s = time.perf_counter() - t0
+    best = cpu_best_rate(bundle, variant, args.steps, args.warmup, None)
+    rate = best["value"]
     line = {
         "impl": "reference", "metric": "cfr_iterations_per_sec", "value": rate,
-        "unit": "iterations/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "unit": "iterations/s", "n_gpus": args.gpus, "steps": best["steps"], "warmup": args.warmup,
+        "ms_per_step": 1e3 * best["seconds"] / best["steps"], "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated game tree)",
         "config": {"workload": desc, "variant": variant, "parallelism": "host threads"},
-        "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} {args.workload} iterations after {args.warmup} warm-up "
-                                   f"(oracle/seqcfr_oracle.c, bit-exact port of the reference path)"},
+        "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": best["cores"], "kind": "port",
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                         "serial_vs_parallel": {str(k): v["iterations_per_s"] for k, v in best["runs"].items()},
+                         "sample": f"{best['steps']} {args.workload} iterations after {args.warmup} warm-up, "
+                                   f"better of 1 and {os.cpu_count()} threads (oracle/seqcfr_oracle.c, "
+                                   f"bit-exact port of the reference path; bundle by oracle/seqcfr_tree.c "
+                                   f"in {build_s:.1f}s)"},
         "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_so_loaded": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
+
+
+def sweep_measure(device: int, ws: int, rank: int, dist, iters: int) -> dict:
+    """Config 5 over the ranks: rank k solves its contiguous slice of the
+    256-point DCFR grid as one batched handle (no collective)."""
+    import torch
+    from paper_2605_14277_b200 import Solver, SolverConfig
+    from paper_2605_14277_b200.distributed import sweep_slice
+    grid = sweep_grid()
+    mine, lo = sweep_slice(grid, ws, rank)
+    b = make_bundle("leduc")
+    s = Solver(b, SolverConfig("dcfr"), device=device, batch_params=mine)
+    s.step(5)
+    s.synchronize()
+    if dist:
+        dist.barrier()
+    s.step(iters)
+    ms = s.last_step_ms()
+    eng = s.engine
+    s.close()
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t[0])
+    return {"config": "256 distinct Leduc DCFR(alpha, beta, gamma) alt solves, "
+                      f"{iters} iterations each, split over {ws} rank(s), no collective",
+            "solves": len(grid), "solves_per_rank": len(mine), "engine": eng,
+            "iterations": iters, "seconds": ms_max / 1e3,
+            "solve_iterations_per_s": len(grid) * iters / (ms_max / 1e3)}
 
 
 def run_ours(args):
@@ -271,6 +366,8 @@ def run_ours(args):
     dist = None
     if ws > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # comm_nranks in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     device = local
@@ -279,7 +376,7 @@ def run_ours(args):
     desc, kind, variant = WORKLOADS[args.workload]
     bundle = make_bundle(kind)
     cfg = SolverConfig(variant)
-    sharded = args.mode == "sharded" and ws > 1
+    sharded = ws > 1 and args.mode == "sharded"
 
     def make_solver():
         if sharded:  # config 4: one solve, payoff SpMV rows split over the ranks
@@ -347,7 +444,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max, e2e_max = float(t[0]), float(t[1])
 
-    # --- per-kernel roofline (CUDA events around every launch, same stream)
+    # --- per-kernel roofline: CUDA events recorded inside a replay of the
+    # iteration graph (the timed configuration), on the handle's stream
     prof = s.profile(args.profile_iters)
     peak, peak_kind = _peaks()
     dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
@@ -370,8 +468,7 @@ def run_ours(args):
     survey_bytes = survey_step_bytes(bundle, cfg, 4 if args.dtype == "f32" else 8)
     survey_gbs = survey_bytes / (ms_max / args.steps / 1e3) / 1e9
 
-    solves = 1 if sharded else ws  # sharded: all ranks advance ONE solve
-    value = solves * args.steps / (ms_max / 1e3)
+    value = args.steps / (ms_max / 1e3) * (1 if sharded else ws)
     line = {
         "metric": "cfr_iterations_per_sec", "value": value, "unit": "iterations/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -380,13 +477,14 @@ def run_ours(args):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (generated game tree)",
         "config": {"workload": desc, "variant": variant, "mode": cfg.mode, "gamma": cfg.gamma,
                    "seqs_per_player": [p.num_seqs for p in bundle.procs],
-                   "nnz_U": bundle.payoff.nnz, "parallelism": (f"row-sharded payoff SpMV + NCCL all-gather x{ws}" if sharded
+                   "nnz_U": bundle.payoff.nnz,
+                   "parallelism": (f"row-sharded payoff SpMV + NCCL all-gather x{ws} (config 4)" if sharded
                                    else f"independent replicas x{ws}" if ws > 1 else "1 gpu"),
                    "l2": "working set > L2 (no flush needed)",
                    "engine": s.engine},
         "gpu_launches": launches,
         "clocks": clocks,
-        "e2e": {"value": solves * args.steps / e2e_max, "unit": "iterations/s",
+        "e2e": {"value": (1 if sharded else ws) * args.steps / e2e_max, "unit": "iterations/s",
                 "h2d_bytes_per_step": (h2d1 - h2d0) / E2E_REPS / args.steps,
                 "d2h_bytes_per_step": (d2h1 - d2h0) / E2E_REPS / args.steps,
                 "includes": "scfr_create upload + K iterations + average-strategy readback, wall clock; "
@@ -397,6 +495,7 @@ def run_ours(args):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,
                      "step": {"algorithmic_bytes": step_bytes, "profiled_ms": prof_ms,
+                              "graph_ms_per_step": ms_max / args.steps,
                               "achieved_gbs": step_bytes / (prof_ms / 1e3) / 1e9,
                               "frac": step_bytes / (prof_ms / 1e3) / 1e9 / peak},
                      "survey_8d": {"algorithmic_bytes_per_step": survey_bytes,
@@ -410,17 +509,22 @@ def run_ours(args):
                                      "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
                                  for k, v in prof.items()}},
     }
-    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, steps, dt = cpu_oracle_rate(bundle, variant, 50, 1, args.cpu_budget, threads, args.dtype)
-        line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": threads,
-                                "kind": "port",
-                                "sample": f"{steps} {args.workload} iterations after 1 warm-up, "
-                                          f"{dt:.1f}s (oracle/seqcfr_oracle.c)"}
     s.close()
-    if rank == 0 and not args.no_suite:
-        line["per_game"] = per_game_suite(device, ws == 1 and not args.no_cpu_baseline)
+    if not args.no_sweep:
+        line["sweep"] = sweep_measure(device, ws, rank, dist, args.sweep_iters)
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        best = cpu_best_rate(oracle_bundle(kind), variant, 50, 1, args.cpu_budget, args.dtype)
+        line["cpu_baseline"] = {"value": best["value"], "unit": "iterations/s", "cores": best["cores"],
+                                "kind": "port", "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                                "serial_vs_parallel": {str(k): v["iterations_per_s"]
+                                                       for k, v in best["runs"].items()},
+                                "sample": f"{best['steps']} {args.workload} iterations after 1 warm-up, "
+                                          f"{best['seconds']:.1f}s, better of 1 and {os.cpu_count()} threads "
+                                          f"(oracle/seqcfr_oracle.c over an oracle-compiled bundle)"}
+    if rank == 0 and ws == 1 and not args.no_suite:
+        line["per_game"] = per_game_suite(device, not args.no_cpu_baseline)
     if rank == 0:
+        line["native_so_loaded"] = loaded_native_libs()
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -440,8 +544,10 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-suite", action="store_true", help="skip the per-game section")
-    ap.add_argument("--mode", choices=("replicas", "sharded"), default="replicas",
-                    help="N>1: independent replicas (weak) or one row-sharded solve (strong)")
+    ap.add_argument("--mode", choices=("sharded", "replicas"), default="sharded",
+                    help="N>1: one row-sharded solve (config 4, strong; default) or independent replicas")
+    ap.add_argument("--no-sweep", action="store_true", help="skip config 5 (the 256-solve sweep)")
+    ap.add_argument("--sweep-iters", type=int, default=1000)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -52,6 +52,9 @@ extern "C" {
 #define SCFR_ECUDA (-4)      /* CUDA runtime failure / no device */
 #define SCFR_ENOMEM (-5)
 #define SCFR_ENCCL (-6)
+/* a schedule value float(t)**gamma overflowed (the reference raises
+ * OverflowError from Python's float power, pkg/solvers.py:172) */
+#define SCFR_EOVERFLOW (-7)
 
 /* Variants (pkg/solvers.py:35) and update modes (pkg/solvers.py:38-44). */
 #define SCFR_CFR 0

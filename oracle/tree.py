@@ -160,3 +160,149 @@ def compile_flat(flat):
     p1, p2 = extract(flat, 1), extract(flat, 2)
     U, UT = payoff(flat, p1, p2)
     return SimpleNamespace(procs=(p1, p2), payoff=U, payoff_t=UT)
+
+
+# ---------------------------------------------------------------------------
+# The same compile step in C (oracle/seqcfr_tree.c), plus the fixture-game
+# generators, so the checker side can build Goofspiel-5 (8.5 M nodes) without
+# the product library.  Pinned to the reference by tests/test_oracle_tree.py.
+
+import ctypes as _C  # noqa: E402
+import os as _os  # noqa: E402
+
+_TREE_LIB = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "_build",
+                          "libseqcfr_tree.so")
+_tl = None
+
+
+class _Game(_C.Structure):
+    _fields_ = [("n", _C.c_int64), ("num_infosets", _C.c_int64),
+                ("kind", _C.POINTER(_C.c_int8)), ("player", _C.POINTER(_C.c_int8)),
+                ("parent", _C.POINTER(_C.c_int64)), ("child_ptr", _C.POINTER(_C.c_int64)),
+                ("child_idx", _C.POINTER(_C.c_int64)), ("infoset", _C.POINTER(_C.c_int64)),
+                ("prob", _C.POINTER(_C.c_double)), ("payoff", _C.POINTER(_C.c_double))]
+
+
+class _Proc(_C.Structure):
+    _fields_ = [(f, _C.c_int64) for f in ("num_nodes", "num_decisions", "num_seqs", "height",
+                                          "degree")] + \
+        [("kind", _C.POINTER(_C.c_int8))] + \
+        [(f, _C.POINTER(_C.c_int64)) for f in ("depth", "parent", "node_seq", "seq_node",
+                                              "dp_node", "dp_first_seq", "dp_num_actions",
+                                              "dp_parent_seq", "level_starts", "game_seq")]
+
+
+class _Csr(_C.Structure):
+    _fields_ = [("rows", _C.c_int64), ("cols", _C.c_int64), ("nnz", _C.c_int64),
+                ("indptr", _C.POINTER(_C.c_int64)), ("indices", _C.POINTER(_C.c_int64)),
+                ("data", _C.POINTER(_C.c_double))]
+
+
+def _tree_lib():
+    global _tl
+    if _tl is None:
+        if not _os.path.exists(_TREE_LIB):
+            import subprocess
+            subprocess.run(["make", "-s", "-C", _os.path.dirname(_TREE_LIB) + "/.."], check=True)
+        L = _C.CDLL(_TREE_LIB)
+        P = _C.POINTER
+        L.ot_goofspiel.restype = P(_Game)
+        L.ot_goofspiel.argtypes = [_C.c_int]
+        L.ot_liars_dice.restype = P(_Game)
+        L.ot_liars_dice.argtypes = [_C.c_int]
+        L.ot_game_free.argtypes = [P(_Game)]
+        L.ot_extract.restype = P(_Proc)
+        L.ot_extract.argtypes = [_C.c_int64, P(_C.c_int8), P(_C.c_int64), P(_C.c_int64),
+                                 P(_C.c_int64), P(_C.c_int8), P(_C.c_int64), _C.c_int,
+                                 P(_C.c_int)]
+        L.ot_proc_free.argtypes = [P(_Proc)]
+        L.ot_payoff.restype = _C.c_int
+        L.ot_payoff.argtypes = [_C.c_int64, P(_C.c_int8), P(_C.c_int64), P(_C.c_double),
+                                P(_C.c_double), P(_Proc), P(_Proc), P(P(_Csr)), P(P(_Csr))]
+        L.ot_csr_free.argtypes = [P(_Csr)]
+        _tl = L
+    return _tl
+
+
+def _np(ptr, n, dt):
+    return np.ctypeslib.as_array(ptr, shape=(int(n),)).astype(dt, copy=True) if n else \
+        np.zeros(0, dtype=dt)
+
+
+def native_game(name: str, size: int) -> SimpleNamespace:
+    """Flat arrays of ``goofspiel(size)`` or ``liars_dice(size)`` from the C
+    generators (same trees as the product's games.py generators)."""
+    L = _tree_lib()
+    gp = {"goofspiel": L.ot_goofspiel, "liars_dice": L.ot_liars_dice}[name](int(size))
+    if not gp:
+        raise ValueError(f"oracle generator refused {name}({size})")
+    g = gp.contents
+    n = g.n
+    try:
+        flat = SimpleNamespace(
+            num_nodes=int(n), kind=_np(g.kind, n, np.int8), player=_np(g.player, n, np.int8),
+            parent=_np(g.parent, n, np.int64), child_ptr=_np(g.child_ptr, n + 1, np.int64),
+            child_idx=_np(g.child_idx, max(n - 1, 0), np.int64),
+            infoset=_np(g.infoset, n, np.int64), prob=_np(g.prob, n, np.float64),
+            payoff=_np(g.payoff, n, np.float64))
+    finally:
+        L.ot_game_free(gp)
+    return flat
+
+
+def compile_native(flat) -> SimpleNamespace:
+    """Reference compile step (DecisionProcess x2, U, U^T) on flat arrays, in C."""
+    L = _tree_lib()
+    P = _C.POINTER
+    a = {f: np.ascontiguousarray(getattr(flat, f), dtype=dt) for f, dt in
+         (("kind", np.int8), ("parent", np.int64), ("child_ptr", np.int64),
+          ("child_idx", np.int64), ("player", np.int8), ("infoset", np.int64),
+          ("prob", np.float64), ("payoff", np.float64))}
+    ptr = {f: v.ctypes.data_as(P(_C.c_int8 if v.dtype == np.int8 else
+                                  _C.c_double if v.dtype == np.float64 else _C.c_int64))
+           for f, v in a.items()}
+    n = int(a["kind"].shape[0])
+    procs, raw = [], []
+    try:
+        for pl in (1, 2):
+            err = _C.c_int(0)
+            pp = L.ot_extract(n, ptr["kind"], ptr["parent"], ptr["child_ptr"], ptr["child_idx"],
+                              ptr["player"], ptr["infoset"], pl, _C.byref(err))
+            if not pp:
+                raise ValueError(f"oracle compile failed for player {pl} (code {err.value})")
+            raw.append(pp)
+            p = pp.contents
+            nn, nj, ns, h = p.num_nodes, p.num_decisions, p.num_seqs, p.height
+            procs.append(SimpleNamespace(
+                num_nodes=int(nn), num_decisions=int(nj), num_seqs=int(ns), height=int(h),
+                degree=int(p.degree), kind=_np(p.kind, nn, np.int8),
+                depth=_np(p.depth, nn, np.int64), parent=_np(p.parent, nn, np.int64),
+                node_seq=_np(p.node_seq, nn, np.int64), seq_node=_np(p.seq_node, ns, np.int64),
+                dp_node=_np(p.dp_node, nj, np.int64),
+                dp_first_seq=_np(p.dp_first_seq, nj, np.int64),
+                dp_num_actions=_np(p.dp_num_actions, nj, np.int64),
+                dp_parent_seq=_np(p.dp_parent_seq, nj, np.int64),
+                level_starts=_np(p.level_starts, h + 2, np.int64),
+                game_seq=_np(p.game_seq, n, np.int64)))
+        U, UT = P(_Csr)(), P(_Csr)()
+        if L.ot_payoff(n, ptr["kind"], ptr["parent"], ptr["prob"], ptr["payoff"], raw[0], raw[1],
+                       _C.byref(U), _C.byref(UT)):
+            raise MemoryError("oracle payoff build failed")
+        mats = []
+        for m in (U, UT):
+            c = m.contents
+            mats.append(SimpleNamespace(rows=int(c.rows), cols=int(c.cols), nnz=int(c.nnz),
+                                        indptr=_np(c.indptr, c.rows + 1, np.int64),
+                                        indices=_np(c.indices, c.nnz, np.int64),
+                                        data=_np(c.data, c.nnz, np.float64)))
+            L.ot_csr_free(m)
+    finally:
+        for pp in raw:
+            L.ot_proc_free(pp)
+    return SimpleNamespace(procs=tuple(procs), payoff=mats[0], payoff_t=mats[1])
+
+
+def native_bundle(name: str, size: int) -> SimpleNamespace:
+    """Product-free bundle of a generated fixture game (the bench's reference
+    arm and CPU baseline use this; no paper_2605_14277_b200 code runs)."""
+    return compile_native(native_game(name, size))

@@ -68,10 +68,18 @@ static void check_game(const scfr_game* g) {
         if (g->child_ptr[i + 1] < g->child_ptr[i]) fail(SCFR_EINVAL, "child_ptr must be non-decreasing");
         if (g->kind[i] < 0 || g->kind[i] > 2) fail(SCFR_EGAME, "node %lld: unknown kind", (long long)i);
         if (i && (g->parent[i] < 0 || g->parent[i] >= n)) fail(SCFR_EGAME, "node %lld: invalid parent id", (long long)i);
+        // decision and chance nodes need children (the reference's
+        // validate_game rejects them, pkg/games.py:158-284)
+        if (g->kind[i] != SCFR_NODE_TERMINAL && g->child_ptr[i + 1] == g->child_ptr[i])
+            fail(SCFR_EGAME, "node %lld: non-terminal node without children", (long long)i);
     }
     const int64_t m = g->child_ptr[n];
     for (int64_t k = 0; k < m; ++k)
         if (g->child_idx[k] <= 0 || g->child_idx[k] >= n) fail(SCFR_EGAME, "child id out of range");
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = g->child_ptr[i]; k < g->child_ptr[i + 1]; ++k)
+            if (g->parent[g->child_idx[k]] != i)
+                fail(SCFR_EGAME, "node %lld: child list and parent ids disagree", (long long)i);
 }
 
 // DecisionProcess._extract for one player (pkg/decision_process.py:76-242).
@@ -117,6 +125,10 @@ static void extract(const scfr_game* g, int player, Tfsdp& P) {
             } else if (parent_key[pid] != key) {
                 fail(SCFR_EGAME, "node %lld: perfect recall violated in infoset %lld", (long long)v,
                      (long long)g->infoset[v]);
+            } else if (cp[v + 1] - cp[v] != nact[pid]) {
+                // every node of an infoset offers the same actions
+                fail(SCFR_EGAME, "node %lld: infoset %lld has nodes with different action counts",
+                     (long long)v, (long long)g->infoset[v]);
             }
         }
         for (int64_t k = cp[v]; k < cp[v + 1]; ++k) {
@@ -226,7 +238,10 @@ static void extract(const scfr_game* g, int player, Tfsdp& P) {
         for (int64_t a = 0; a < nact[pid]; ++a) final_of_key[first_key[pid] + a] = P.dp_first_seq[j] + a;
     }
     P.game_seq.resize(n);
-    for (int64_t v = 0; v < n; ++v) P.game_seq[v] = final_of_key[prov[v]];
+    for (int64_t v = 0; v < n; ++v) {
+        if (prov[v] < 0 || prov[v] >= next_key) fail(SCFR_EGAME, "node %lld: sequence key out of range", (long long)v);
+        P.game_seq[v] = final_of_key[prov[v]];
+    }
 }
 
 // build_payoff_matrix + CsrMatrix.from_coo + transposed.

@@ -310,7 +310,14 @@ struct scfr_handle {
     int tile_staged = 1;     // SCFR_TILE_STAGE=0: no shared-memory staging (A/B)
     size_t tile_smem_up = 0, tile_smem_down = 0;
     std::vector<std::pair<const void*, int>> tile_occ;  // resident CTAs per SM, per tile kernel
+    void (*comm_destroy)(void*) = nullptr;  // set with comm (NCCL is dlopen'ed)
     ~scfr_handle() {
+        // in-flight async copies / kernels may still use buffers that the
+        // member destructors free: drain the stream first (also on a failed
+        // create, where this destructor runs from the unique_ptr)
+        if (stream) cudaStreamSynchronize(stream);
+        if (comm && comm_destroy) comm_destroy(comm);
+        comm = nullptr;
         if (exec) cudaGraphExecDestroy(exec);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);

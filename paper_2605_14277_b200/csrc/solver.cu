@@ -1357,6 +1357,14 @@ static void check_player(const scfr_handle* h, int player, int solve) {
 
 static void add_weights(scfr_handle* h, int64_t n) {
     ensure_schedule(h, h->t + n);
+    // float(t)**gamma must be finite for every iteration about to run: the
+    // reference's Python float power raises OverflowError there (and an
+    // infinite weight would turn the average into NaN)
+    for (int k = 0; k < h->B; ++k)
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(h->w_host[(size_t)k * h->cap + h->t + i]))
+                fail(SCFR_EOVERFLOW, "t**gamma overflows at iteration %lld (solve %d, gamma %g)",
+                     (long long)(h->t + i + 1), k, h->gamma[k]);
     for (int k = 0; k < h->B; ++k)
         for (int64_t i = 0; i < n; ++i) h->avg_weight[k] += h->w_host[(size_t)k * h->cap + h->t + i];
 }
@@ -1556,6 +1564,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             ncclComm_t comm;
             NCCL_OK(nccl().CommInitRank(&comm, w, id, rk));
             h->comm = comm;
+            h->comm_destroy = [](void* c) { nccl().CommDestroy((ncclComm_t)c); };
             h->world = w;
             h->rank = rk;
         }
@@ -1982,9 +1991,7 @@ int scfr_destroy(scfr_handle* h) {
     return guarded([&] {
         if (!h) return;
         cudaSetDevice(h->device);
-        if (h->stream) cudaStreamSynchronize(h->stream);
-        if (h->comm) nccl().CommDestroy((ncclComm_t)h->comm);
-        delete h;
+        delete h;  // ~scfr_handle drains the stream and destroys the communicator
     });
 }
 

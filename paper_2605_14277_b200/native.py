@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libseqcfr_b200.so")
 
-OK, EINVAL, EGAME, ENONFINITE, ECUDA, ENOMEM, ENCCL = 0, -1, -2, -3, -4, -5, -6
+OK, EINVAL, EGAME, ENONFINITE, ECUDA, ENOMEM, ENCCL, EOVERFLOW = 0, -1, -2, -3, -4, -5, -6, -7
 VARIANT_CODE = {"cfr": 0, "cfr+": 1, "dcfr": 2, "pcfr": 3, "pcfr+": 4}
 MODE_CODE = {"sim": 0, "alt": 1}
 ENGINE_CODE = {"auto": 0, "levels": 1, "persistent": 2, "persistent_grid": 3, "tiled": 4,
@@ -154,6 +154,8 @@ def check(status: int) -> None:
         raise MemoryError(msg)
     if status == ENCCL:
         raise NcclError(msg)
+    if status == EOVERFLOW:
+        raise OverflowError(msg)
     raise CudaError(f"[{status}] {msg}")
 
 

@@ -450,7 +450,8 @@ class IterationBenchmark:
     workers: int
     times: list[float]
     work_per_iteration: int
-    state_bytes: int
+    state_bytes: int          # the reference's figure: bundle.nbytes() + both RegretState.state_bytes()
+    device_bytes: int = 0     # what this handle holds in HBM (structure, state, schedules)
 
     @property
     def mean_seconds(self) -> float:
@@ -481,7 +482,8 @@ def benchmark_iterations(bundle: GameBundle, config: SolverConfig, backend=None,
         times.append(s.last_step_ms() / 1e3)
     out = IterationBenchmark(proc_nodes=bundle.num_proc_nodes, backend_kind="cuda", workers=1,
                              times=times, work_per_iteration=work_per_iteration(bundle, config),
-                             state_bytes=s.device_bytes())
+                             state_bytes=bundle.reference_nbytes() + bundle.reference_state_bytes(),
+                             device_bytes=s.device_bytes())
     s.close()
     return out
 

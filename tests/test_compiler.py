@@ -80,14 +80,27 @@ def test_native_generators_match_python(size):
         np.testing.assert_array_equal(a.payoff, b.payoff)
 
 
-def test_goofspiel5_sizes():
-    # SURVEY.md §8 sizes table
+def test_goofspiel5_matches_reference():
+    """The bench workload: every structure array of the native compile equals
+    the reference's own GameBundle (digests by scripts/make_golden_goof5.py)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "goof5_meta.json")) as fh:
+        info = json.load(fh)["structure"]["goof5"]
     flat = flat_goofspiel(5)
-    assert flat.num_nodes == 8_530_656
+    assert flat.num_nodes == info["num_game_nodes"] == 8_530_656
     b = GameBundle(flat)
     for p in b.procs:
         assert (p.num_nodes, p.num_seqs, p.num_decisions) == (4_850_531, 2_666_026, 2_184_505)
     assert b.payoff.nnz == 1_728_000
+    for pl in (1, 2):
+        for f, d in info[f"p{pl}"]["digests"].items():
+            assert digest(getattr(b.procs[pl - 1], f)) == d, (pl, f)
+    for tag, m in (("U", b.payoff), ("UT", b.payoff_t)):
+        for f, d in info[tag]["digests"].items():
+            assert digest(getattr(m, f)) == d, (tag, f)
+    assert b.reference_nbytes() == info["bundle_nbytes"]
 
 
 def test_perfect_recall_violation_is_rejected():
