@@ -249,7 +249,8 @@ __device__ __forceinline__ R post_op(R rv, int post, R pf, R nf) {
 template <class R>
 __device__ __forceinline__ R rm_prob(R rv, R S, int n) {
     const R p = rv > R(0) ? rv : R(0);
-    return S != R(0) ? ddiv(p, S) : ddiv(R(1), R(n));
+    const bool z = S == R(0);  // one division either way: p / S, or 1.0 / n
+    return ddiv(z ? R(1) : p, z ? R(n) : S);
 }
 
 
@@ -420,14 +421,16 @@ __device__ __forceinline__ void pred_dp(const DevTree& T, int j, const R* __rest
 
 // TD: x[(j,a)] = b[(j,a)] * x[parent(j)] (pkg/solvers.py:163-170), with the
 // fused average update avg = w*x + avg (pkg/solvers.py:172-174).
+// xp_in: the parent sequence's x when the caller already has it (the level
+// engine's top: recomputed from the ancestor chain), else loaded from x.
 template <class Ld, class R>
 __device__ __forceinline__ void td_dp(const DevTree& T, int j, const R* __restrict__ b,
                                       R* __restrict__ x, typename nd<R>::type* __restrict__ avg,
-                                      typename nd<R>::type w) {
+                                      typename nd<R>::type w, const R* xp_in = nullptr) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
     const int s1 = s0 + n;
-    const R xp = Ld::ld(x + parent_of<Ld>(T, j));
+    const R xp = xp_in ? *xp_in : Ld::ld(x + parent_of<Ld>(T, j));
     if (T.un == 1) {  // single-action level: b == R(1), so x = R(1) * xp (single_action_note)
         const R xa = dmul(R(1), xp);
         x[s0] = xa;
@@ -447,10 +450,10 @@ __device__ __forceinline__ void td_dp(const DevTree& T, int j, const R* __restri
 template <class Ld, class R>
 __device__ __forceinline__ void td_dp_warp(const DevTree& T, int j, const R* __restrict__ b,
                                            R* __restrict__ x, typename nd<R>::type* __restrict__ avg,
-                                           typename nd<R>::type w, int lane) {
+                                           typename nd<R>::type w, int lane, const R* xp_in = nullptr) {
     int s0, n;
     dp_range<Ld>(T, j, s0, n);
-    const R xp = Ld::ld(x + parent_of<Ld>(T, j));
+    const R xp = xp_in ? *xp_in : Ld::ld(x + parent_of<Ld>(T, j));
     for (int a = lane; a < n; a += 32) {
         const int s = s0 + a;
         const R xa = T.un == 1 ? dmul(R(1), xp) : dmul(Ld::ld(b + s), xp);
@@ -558,19 +561,28 @@ __device__ __forceinline__ R lane_seq_sum(R v, int n) {
 // shuffles (n is warp-uniform); `valid` masks the lanes past the level's end
 // and the 32 - G*n idle lanes.
 
-template <class R>
+// N > 0: the group width is a compile-time constant (the common 2..4-action
+// levels), so the shuffles unroll with no loop around them; N == 0: width n
+// at run time.
+template <int N = 0, class R>
 __device__ __forceinline__ R group_seq_sum(R v, int gb, int n) {
     R acc = R(0);
-    for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, gb + a));
+    if constexpr (N > 0) {
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, gb + a));
+    } else {
+        for (int a = 0; a < n; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, gb + a));
+    }
     return acc;
 }
 
-template <class Ld, class R>
+template <class Ld, int N = 0, class R>
 __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
                                              const R* __restrict__ u, R* __restrict__ r, R* __restrict__ b,
                                              R* __restrict__ V, int post, typename nd<R>::type pf,
                                              typename nd<R>::type nf, bool do_rm, int* nonfinite,
                                              FuseUT<R> fuse, const R* Vc, R* bw = nullptr) {
+    if constexpr (N > 0) n = N;
     const R* Vr = Vc ? Vc : V;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
     R q = R(0), bb = R(0), rr = R(0);
@@ -582,7 +594,7 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
         rr = Ld::ld(r + s);
         q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, Vr));
     }
-    const R E = group_seq_sum(dmul(bb, q), gb, n);
+    const R E = group_seq_sum<N>(dmul(bb, q), gb, n);
     if (valid && a == 0) V[j] = E;
     const R negE = dmul(R(-1), dadd(R(0), E));
     R rv = R(0);
@@ -592,15 +604,16 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
         bad |= !isfinite(rv);
         r[s] = rv;
     }
-    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
     if (do_rm && valid) (bw ? bw : b)[s] = rm_prob(rv, S, n);
     if (bad) atomicOr(nonfinite, 1);
 }
 
-template <class Ld, class R>
+template <class Ld, int N = 0, class R>
 __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
                                               const R* __restrict__ m, const R* __restrict__ r,
                                               R* __restrict__ b, R* __restrict__ V, bool plus, const R* Vc) {
+    if constexpr (N > 0) n = N;
     const R* Vr = Vc ? Vc : V;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
     R q = R(0), bb = R(0), rr = R(0);
@@ -611,7 +624,7 @@ __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool vali
         rr = Ld::ld(r + s);
         q = dadd(dadd(R(0), mm), lane_child_value<Ld>(c, Vr));
     }
-    const R E = group_seq_sum(dmul(bb, q), gb, n);
+    const R E = group_seq_sum<N>(dmul(bb, q), gb, n);
     if (valid && a == 0) V[j] = E;
     const R negE = dmul(R(-1), dadd(R(0), E));
     R rv = R(0);
@@ -619,7 +632,7 @@ __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool vali
         rv = dadd(rr, dadd(negE, q));
         if (plus) rv = rv > R(0) ? rv : R(0);
     }
-    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
     if (valid) b[s] = rm_prob(rv, S, n);
 }
 
@@ -627,21 +640,23 @@ __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool vali
 template <class Ld, class R>
 __device__ __forceinline__ void td_dp_group(const DevTree& T, int j, bool valid, int a, int n,
                                             const R* __restrict__ b, R* __restrict__ x,
-                                            typename nd<R>::type* __restrict__ avg, typename nd<R>::type w) {
+                                            typename nd<R>::type* __restrict__ avg, typename nd<R>::type w,
+                                            const R* xp_in = nullptr) {
     if (!valid) return;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
-    const R xa = dmul(Ld::ld(b + s), Ld::ld(x + parent_of<Ld>(T, j)));
+    const R xa = dmul(Ld::ld(b + s), xp_in ? *xp_in : Ld::ld(x + parent_of<Ld>(T, j)));
     x[s] = xa;
     if (avg) avg[s] = dadd(dmul(w, xa), Ld::ld(avg + s));
 }
 
 // CUR: regret matching on the fly, then the top-down product.
-template <class Ld, class R>
+template <class Ld, int N = 0, class R>
 __device__ __forceinline__ void cur_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
                                              const R* __restrict__ r, R* __restrict__ x) {
+    if constexpr (N > 0) n = N;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
     const R rv = valid ? Ld::ld(r + s) : R(0);
-    const R S = group_seq_sum(rv > R(0) ? rv : R(0), gb, n);
+    const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
     if (valid) x[s] = dmul(rm_prob(rv, S, n), Ld::ld(x + parent_of<Ld>(T, j)));
 }
 

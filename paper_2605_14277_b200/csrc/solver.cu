@@ -70,10 +70,51 @@ struct TaskT {
     const R* Vc;   // OBS / PRED: child values read from here (u / the prediction; kernels.cuh leaf_note), per-solve stride S
     int skip_v;    // OBS on a forced leaf level whose V nobody reads
     R* bw;         // OBS: regret matching writes here instead of b (bcur)
+    // Top-down launch of level ls of a player with a top (prepare_top): the
+    // parents' x come from their ancestor chains, and the launch also writes
+    // the top's x (and average).
+    const TopInfo* top;
 };
 using Task = TaskT<double>;
 
-enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
+// --- the top: last-arrival completion, ancestor-chain x -----------------
+
+// x of top sequence p from its ancestor chain: b_a0·1.0, then b_a1·that, ...
+// (x[s] = b[s]·x[parent] with x[0] = 1.0; a forced level's b is 1.0 and is
+// not read).  src: b (or bcur) of this solve.
+template <class R>
+__device__ __forceinline__ R top_x(const TopInfo* tp, const R* src, int p) {
+    if (p == 0) return R(1);
+    const int ls = tp->ls;
+    const int* an = tp->anc + (size_t)p * ls;
+    int a[kTopMax];
+    R bv[kTopMax];
+#pragma unroll
+    for (int l = 0; l < kTopMax; ++l) a[l] = l < ls ? __ldg(an + l) : -1;
+#pragma unroll
+    for (int l = 0; l < kTopMax; ++l) bv[l] = a[l] >= 0 && !(a[l] & (1 << 30)) ? src[a[l]] : R(1);
+    R x = R(1);
+#pragma unroll
+    for (int l = 0; l < kTopMax; ++l)
+        if (a[l] >= 0) x = dmul(bv[l], x);
+    return x;
+}
+
+// Work of a top-down level-ls launch before its DPs: the top's x (and
+// average), once per solve across the task's CTAs.
+template <int KIND, class R>
+__device__ __forceinline__ void top_prologue(const TaskT<R>& t, int blk, R w) {
+    const size_t so = (size_t)blockIdx.y * t.S;
+    const TopInfo* tp = t.top;
+    const R* src = t.b + so;
+    for (int s = 1 + blk * TPB + (int)threadIdx.x; s < tp->Stop; s += t.nblk * TPB) {
+        const R xa = top_x(tp, src, s);
+        t.x[so + s] = xa;
+        if (KIND == LK_TD_AVG) t.avg[so + s] = dadd(dmul(w, xa), t.avg[so + s]);
+    }
+    if (KIND == LK_TD_AVG && blk == 0 && threadIdx.x == 0)  // the reference axpy also covers x[0] = 1
+        t.avg[so] = dadd(dmul(w, t.x[so]), t.avg[so]);
+}
 
 // The task's blocks stride over its DPs (grid-stride): a launch is capped at
 // about one resident wave, so the deep levels (10^6 DPs of a few loads each)
@@ -107,14 +148,16 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
         fused_u<LdL1>(f0, const_cast<R*>(t.u) + so, 0, bad);
         if (bad) atomicOr(kp.nonfinite, 1);
     }
+    if ((KIND == LK_TD_AVG || KIND == LK_TD) && t.top) top_prologue<KIND, R>(t, blk, w);
     for (int item = first; item < t.n; item += stride) {  // warp-uniform in warp mode
         const int j = t.lo + item;
-        if constexpr (KIND == LK_TD_AVG) {
-            if constexpr (WARP) td_dp_warp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w, lane);
-            else td_dp<LdL1>(t.T, j, t.b + so, t.x + so, t.avg + so, w);
-        } else if constexpr (KIND == LK_TD) {
-            if constexpr (WARP) td_dp_warp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0), lane);
-            else td_dp<LdL1>(t.T, j, t.b + so, t.x + so, nullptr, R(0));
+        if constexpr (KIND == LK_TD_AVG || KIND == LK_TD) {
+            R xp;  // the top's x is recomputed from the ancestor chain
+            if (t.top) xp = top_x(t.top, t.b + so, parent_of<LdL1>(t.T, j));
+            const R* xpp = t.top ? &xp : nullptr;
+            R* avg = KIND == LK_TD_AVG ? t.avg + so : nullptr;
+            if constexpr (WARP) td_dp_warp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w, lane, xpp);
+            else td_dp<LdL1>(t.T, j, t.b + so, t.x + so, avg, w, xpp);
         } else if constexpr (KIND == LK_CUR) {
             cur_dp<MAXA, LdL1>(t.T, j, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
@@ -140,12 +183,12 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
 // big affine levels with n = T.un actions.  The task's warps stride over
 // groups of G DPs; the loop bound is warp-uniform so every lane reaches the
 // shuffles.  Never used on level 0 (the empty sequence's extra work).
-template <int KIND, class R>
+template <int KIND, int N, class R>
 __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, const KParams& kp) {
     constexpr int W = TPB / 32;
     const size_t so = (size_t)blockIdx.y * t.S;
     R* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
-    const int n = t.T.un, G = 32 / n;
+    const int n = N > 0 ? N : t.T.un, G = 32 / n;
     const int lane = threadIdx.x & 31, g = lane / n, a = lane - g * n, gb = g * n;
     R w = R(0), pf = R(1), nf = R(1);
     if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
@@ -157,34 +200,36 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
     FuseUT<R> fu = t.fu;
     if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
     const R* Vc = t.Vc ? t.Vc + so : nullptr;
+    if ((KIND == LK_TD_AVG || KIND == LK_TD) && t.top) top_prologue<KIND, R>(t, blk, w);
     for (int wi = blk * W + (int)(threadIdx.x >> 5); wi * G < t.n; wi += t.nblk * W) {
         const int item = wi * G + g;
         const bool valid = g < G && item < t.n;
         const int j = t.lo + (valid ? item : 0);
-        if constexpr (KIND == LK_TD_AVG) {
-            td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, t.avg + so, w);
-        } else if constexpr (KIND == LK_TD) {
-            td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, nullptr, R(0));
+        if constexpr (KIND == LK_TD_AVG || KIND == LK_TD) {
+            R xp;  // the top's x is recomputed from the ancestor chain
+            if (t.top && valid) xp = top_x(t.top, t.b + so, parent_of<LdL1>(t.T, j));
+            td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, KIND == LK_TD_AVG ? t.avg + so : nullptr, w,
+                               t.top ? &xp : nullptr);
         } else if constexpr (KIND == LK_CUR) {
-            cur_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.r + so, t.x + so);
+            cur_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
-            obs_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post,
+            obs_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post,
                                pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc, t.bw ? t.bw + so : nullptr);
         } else {
-            pred_dp_group<LdL1s>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
+            pred_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
                                 kp.plus != 0, Vc);
         }
     }
 }
 
-template <int KIND, class R>
+template <int KIND, int N, class R>
 __global__ void __launch_bounds__(TPB, 8) k_level_g(const __grid_constant__ TaskT<R> t0,
                                                     const __grid_constant__ TaskT<R> t1,
                                                     const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
     pdl_wait();
-    if ((int)blockIdx.x < t0.nblk) level_body_group<KIND, R>(t0, blockIdx.x, kp);
-    else level_body_group<KIND, R>(t1, blockIdx.x - t0.nblk, kp);
+    if ((int)blockIdx.x < t0.nblk) level_body_group<KIND, N, R>(t0, blockIdx.x, kp);
+    else level_body_group<KIND, N, R>(t1, blockIdx.x - t0.nblk, kp);
 }
 
 // Narrow variants (<= 2 actions in registers: the deep, bandwidth-bound
@@ -219,20 +264,31 @@ using LevelKernel = LevelKernelT<double>;
 // too: their launch time is one DP's latency chain, and the thread path
 // serialises the actions' fused payoff rows (Liar's dice: a 1320-DP level
 // with 4 actions took 16 µs as 11 CTAs of threads).
-static bool warp_level(const scfr_handle* h, const Player& P, int l) {
+bool warp_level(const scfr_handle* h, const Player& P, int l) {
     return (P.lvl_nj[l] <= h->warp_nj &&
             (P.lvl_nc[l] >= 8.0 * P.lvl_nj[l] || (h->small_warp && P.lvl_maxa[l] >= 2))) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
 
-template <class R>
-static LevelKernelT<R> pick_group_kernel(int kind) {
+// Group kernels specialised on the common widths (2..4 actions: the
+// shuffled in-order sums unroll), else the width is read at run time.
+template <int N, class R>
+static LevelKernelT<R> pick_group_kernel_n(int kind) {
     switch (kind) {
-        case LK_TD_AVG: return k_level_g<LK_TD_AVG, R>;
-        case LK_TD: return k_level_g<LK_TD, R>;
-        case LK_CUR: return k_level_g<LK_CUR, R>;
-        case LK_OBS: return k_level_g<LK_OBS, R>;
-        default: return k_level_g<LK_PRED, R>;
+        case LK_TD_AVG: return k_level_g<LK_TD_AVG, N, R>;
+        case LK_TD: return k_level_g<LK_TD, N, R>;
+        case LK_CUR: return k_level_g<LK_CUR, N, R>;
+        case LK_OBS: return k_level_g<LK_OBS, N, R>;
+        default: return k_level_g<LK_PRED, N, R>;
+    }
+}
+template <class R>
+static LevelKernelT<R> pick_group_kernel(int kind, int un) {
+    switch (un) {
+        case 2: return pick_group_kernel_n<2, R>(kind);
+        case 3: return pick_group_kernel_n<3, R>(kind);
+        case 4: return pick_group_kernel_n<4, R>(kind);
+        default: return pick_group_kernel_n<0, R>(kind);
     }
 }
 
@@ -885,7 +941,7 @@ static DevTree shaped_tree(const Player& P, int l) {
 
 // The deepest level is single-action DPs into end nodes (affine, no child
 // DPs) and all its DPs hang under the level above (kernels.cuh leaf_note).
-static bool leaf_single(const scfr_handle* h, const Player& P) {
+bool leaf_single(const scfr_handle* h, const Player& P) {
     const int L = P.levels();
     if (!h->leaf_skip || L < 2) return false;
     const DevTree& sh = P.lvl_shape[L - 1];
@@ -983,6 +1039,11 @@ struct Launcher : LaunchBase {
     // predictive alt mode: player 1's OBS regret-matches into bcur (instead
     // of b, which PRED still needs) and CUR reads it as a plain TD
     void* bcur_ = nullptr;
+    // first level of player P that top-down passes launch (the top's are not)
+    int first_level(const Player& P) const {
+        const int k = &P == &h->P[0] ? 0 : 1;
+        return h->top[k].on ? h->top[k].ls : 0;
+    }
 
 
     // Task for level l of player P (l outside [0, L) -> empty task).
@@ -1072,6 +1133,14 @@ struct Launcher : LaunchBase {
         }
         t0.skip_v = skipa;
         t1.skip_v = skipb;
+        // the top-down launch of level ls of a player with a top recomputes the top
+        auto attach_top = [&](TaskT<R>& t, Player* P, int l) {
+            if (!P || (lk != LK_TD_AVG && lk != LK_TD)) return;
+            const TopPlayer& tp = h->top[P == &h->P[0] ? 0 : 1];
+            if (tp.on && l == tp.ls) t.top = tp.info.p;
+        };
+        attach_top(t0, A, la);
+        attach_top(t1, Bp, lb);
         const bool fused_here = lk == LK_OBS && fuse_spmv();
         if (t0.n == 0 && t1.n == 0) return;
         const bool fused = fused_here;
@@ -1149,7 +1218,14 @@ struct Launcher : LaunchBase {
                 bytes += (shaped ? 0.0 : 4.0 * (s1 - s0 + 1)) + (4.0 + v) * nnz + v * nnz;
             }
         }
-        const LevelKernelT<R> kern = group ? pick_group_kernel<R>(lk) : pick_level_kernel<R>(lk, maxa, warp);
+        // both tasks of a group launch share one width, or the kernel reads it
+        int gun = 0;
+        if (group) {
+            const int ua = A && la >= 0 && la < A->levels() ? A->lvl_shape[la].un : -1;
+            const int ub = Bp && lb >= 0 && lb < Bp->levels() ? Bp->lvl_shape[lb].un : -1;
+            gun = ua < 0 ? ub : ub < 0 ? ua : ua == ub ? ua : 0;
+        }
+        const LevelKernelT<R> kern = group ? pick_group_kernel<R>(lk, gun) : pick_level_kernel<R>(lk, maxa, warp);
         // grid-stride tasks: cap each at one resident wave of this kernel
         const int wave = resident_ctas(kern);
         t0.nblk = std::min(t0.nblk, wave);
@@ -1178,6 +1254,11 @@ struct Launcher : LaunchBase {
             tiled_iteration(*this);
             return;
         }
+        if (h->forest) {
+            if (h->f32) forest_iteration<float>(*this);
+            else forest_iteration<double>(*this);
+            return;
+        }
         if (h->f32) iteration_t<float>();
         else iteration_t<double>();
     }
@@ -1190,6 +1271,8 @@ struct Launcher : LaunchBase {
         R* Axp = vals<R>(A.xpost);
         const bool pr = predictive(h->variant);
         const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
+        const int fa = first_level(A), fb = first_level(Bp);  // the top's levels are not launched
+        auto skip = [](int l, int f) { return l < f ? -1 : l; };
         // next_strategy of both players (independent): PRED deep -> shallow,
         // then TD + average shallow -> deep, the two players sharing launches.
         if (pr) {
@@ -1216,8 +1299,8 @@ struct Launcher : LaunchBase {
         // forced leaf levels: their x / avg are the parents' (k_expand_leaf)
         const bool xa = h->leaf_x && leaf_single(A), xb = h->leaf_x && leaf_single(Bp);
         for (int k = 0; k < L; ++k)
-            level<R>(LK_TD_AVG, KK_TD_AVG, &A, xa && k == LA - 1 ? -1 : k, &Bp, xb && k == LB - 1 ? -1 : k,
-                     nullptr, nullptr, Ax, Bx, false);
+            level<R>(LK_TD_AVG, KK_TD_AVG, &A, xa && k == LA - 1 ? -1 : skip(k, fa), &Bp,
+                     xb && k == LB - 1 ? -1 : skip(k, fb), nullptr, nullptr, Ax, Bx, false);
         const bool fused = fuse_spmv();
         // OBS on a forced leaf level: its V equals u (leaf_note), so the
         // parent level reads u and the leaf launch skips writing V
@@ -1243,8 +1326,8 @@ struct Launcher : LaunchBase {
             // already regret-matched (into b, or into bcur for the predictive
             // variants), or RM on the fly (SCFR_NO_BCUR=1)
             for (int k = 0; k < LA; ++k)
-                level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : k, nullptr,
-                         -1, nullptr, nullptr, Axp, nullptr, false);
+                level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : skip(k, fa),
+                         nullptr, -1, nullptr, nullptr, Axp, nullptr, false);
             bcur_ = nullptr;
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             for (int k = 0; k < LB; ++k)
@@ -1436,6 +1519,71 @@ using namespace scfr;
 extern "C" {
 
 // Shared body of scfr_create / scfr_create_sharded (nccl_id == nullptr: one GPU).
+// The top of player k (TopInfo): the largest split ls whose levels [0, ls)
+// hold at most kTopDPs decision points and under whose sequences hang only
+// level-ls DPs.  Top-down passes (TD + average, TD into xpost) then do not
+// launch those levels: the level-ls launch recomputes each DP's parent x from
+// its ancestor chain, x = b_a·(…·(b_0·1.0)), the same products in the same
+// order, and writes the top's x (and average) once.  Bottom-up passes keep
+// launching every level (completing the top in-kernel by last arrival
+// measured slower than the launches it saved: DESIGN.md §4).
+static void prepare_top(scfr_handle* h, int k) {
+    constexpr int kTopDPs = 1 << 16;
+    const char* off = std::getenv("SCFR_NO_TOP");
+    if (off && off[0] == '1') return;
+    Player& P = h->P[k];
+    const int L = P.levels();
+    if (L < 2 || !P.h_seq_ptr || !P.h_dp_parent) return;
+    // player 1's current strategy regret-matches on the fly (SCFR_NO_BCUR=1):
+    // its chain would need the sums, so keep its top launched
+    if (k == 0 && predictive(h->variant) && h->mode == SCFR_MODE_ALT && !h->bcur_on) return;
+    const std::vector<int>& sp = *P.h_seq_ptr;
+    const std::vector<int>& par = *P.h_dp_parent;
+    // the level-ls launch must run: not a forced leaf level whose top-down
+    // launches are skipped (leaf_x)
+    const int lmax = std::min(h->leaf_x && leaf_single(h, P) ? L - 2 : L - 1, kTopMax);
+    int ls = 0;
+    for (int l = lmax; l >= 1; --l) {
+        if (P.lvl[l] > kTopDPs) continue;
+        const int Stop = sp[P.lvl[l]];
+        bool ok = true;  // DPs below level l hang under forest sequences only
+        for (int q = P.lvl[l + 1]; q < P.J && ok; ++q) ok = par[q] >= Stop;
+        if (ok) {
+            ls = l;
+            break;
+        }
+    }
+    if (ls == 0) return;
+    const int Jtop = P.lvl[ls], Stop = sp[Jtop];
+    std::vector<int> sdp(std::max(Stop, 1), -1), lvl_of(Jtop, 0);
+    for (int q = 0; q < Jtop; ++q)
+        for (int s = sp[q]; s < sp[q + 1]; ++s) sdp[s] = q;
+    for (int l = 0; l < ls; ++l)
+        for (int q = P.lvl[l]; q < P.lvl[l + 1]; ++q) lvl_of[q] = l;
+    std::vector<int> anc((size_t)std::max(Stop, 1) * ls, -1);
+    for (int s = 1; s < Stop; ++s) {
+        int chain[kTopMax + 1], n = 0;
+        for (int a = s; a != 0 && n <= kTopMax; a = par[sdp[a]]) chain[n++] = a;
+        if (n > ls) return;  // (cannot happen: one ancestor per top level)
+        for (int i = 0; i < n; ++i) {
+            const int a = chain[n - 1 - i];
+            anc[(size_t)s * ls + i] = a | (P.lvl_shape[lvl_of[sdp[a]]].un == 1 ? 1 << 30 : 0);
+        }
+    }
+    TopPlayer& tp = h->top[k];
+    TopInfo info{};
+    info.ls = ls;
+    info.Stop = Stop;
+    tp.anc.alloc(anc.size());
+    CUDA_OK(copy_async(tp.anc.p, anc.data(), anc.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    info.anc = tp.anc.p;
+    tp.info.alloc(1);
+    CUDA_OK(copy_async(tp.info.p, &info, sizeof info, cudaMemcpyHostToDevice, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));  // the host vectors die here
+    tp.ls = ls;
+    tp.on = true;
+}
+
 static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                         const scfr_csr* UT, const scfr_config* cfg, int device,
                         const char* nccl_id, int rank, int world, scfr_handle** out) {
@@ -1632,6 +1780,15 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             h->leaf_x = l1 || l2;
             if (l2) build_iter_indices(h.get(), h->U, h->P[1]);   // U's columns: player 2's sequences
             if (l1) build_iter_indices(h.get(), h->UT, h->P[0]);  // Uᵀ's columns: player 1's
+            // opt-in forest mode (forest.cu), else the top levels completed in-kernel
+            const char* fe = std::getenv("SCFR_FOREST");
+            if (fe && fe[0] == '1' && h->u_empty_skip && prepare_forest(h.get(), U, UT)) {
+                h->fdone.alloc(1);
+                h->fdone.zero(h->stream);
+            } else {
+                prepare_top(h.get(), 0);
+                prepare_top(h.get(), 1);
+            }
         }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
