@@ -444,15 +444,29 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max, e2e_max = float(t[0]), float(t[1])
 
-    # --- per-kernel roofline: CUDA events recorded inside a replay of the
-    # iteration graph (the timed configuration), on the handle's stream
-    prof = s.profile(args.profile_iters)
+    # --- per-kernel roofline, measured inside the timed configuration: a
+    # recording copy of the iteration graph (scfr_timeline: every launch's
+    # first-CTA start and last-CTA end, %globaltimer).  A launch's own
+    # duration gives its achieved GB/s; exclusive spans end_i - end_(i-1)
+    # partition the step, so the per-kind sums add up to the graph step.
     peak, peak_kind = _peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
-    dname, d = dom
-    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
-    step_bytes = sum(v["bytes"] for v in prof.values()) / args.profile_iters
-    prof_ms = sum(v["ms"] for v in prof.values()) / args.profile_iters
+    tl_n = max(3, 3 * args.profile_iters)
+    timeline = s.timeline(tl_n)
+    kinds = {}
+    for e in timeline:
+        k = kinds.setdefault(e["kind"], {"launches": 0, "excl_us": 0.0, "own_us": 0.0, "bytes": 0.0})
+        k["launches"] += 1
+        k["excl_us"] += e["excl_us"]
+        k["own_us"] += e["end_us"] - e["start_us"]
+        k["bytes"] += e["bytes"]
+    top = max(timeline, key=lambda e: e["end_us"] - e["start_us"])
+    dname = top["kind"]
+    dur_us = top["end_us"] - top["start_us"]
+    achieved = top["bytes"] / (dur_us * 1e3)
+    step_bytes = sum(e["bytes"] for e in timeline)
+    tl_us = timeline[-1]["end_us"]
+    prof = s.profile(args.profile_iters)  # eager launches with CUDA events, for comparison
+    d = {"bytes": top["bytes"], "launches": 1}
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -494,20 +508,29 @@ def run_ours(args):
                      "size_matched_copy": copy_ref,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,
-                     "step": {"algorithmic_bytes": step_bytes, "profiled_ms": prof_ms,
+                     "method": f"in-graph timeline (scfr_timeline, {tl_n} iterations): the longest launch's "
+                               "algorithmic bytes over its own first-CTA-start to last-CTA-end duration",
+                     "kernel_us": dur_us, "kernel_bytes": top["bytes"],
+                     "step": {"algorithmic_bytes": step_bytes, "timeline_us": tl_us,
                               "graph_ms_per_step": ms_max / args.steps,
-                              "achieved_gbs": step_bytes / (prof_ms / 1e3) / 1e9,
-                              "frac": step_bytes / (prof_ms / 1e3) / 1e9 / peak},
+                              "achieved_gbs": step_bytes / (tl_us * 1e3),
+                              "frac": step_bytes / (tl_us * 1e3) / peak},
                      "survey_8d": {"algorithmic_bytes_per_step": survey_bytes,
                                    "achieved_gbs": survey_gbs, "frac": survey_gbs / peak,
                                    "note": "SURVEY §8(d) fused compulsory bytes over the graph-timed step; "
                                            "the exact shortcuts (DESIGN §4) skip part of them, so this "
                                            "overstates bandwidth use: frac above uses the bytes the "
                                            "kernels load"},
-                     "kernels": {k: {"launches": v["launches"] // args.profile_iters,
-                                     "ms": v["ms"] / args.profile_iters,
-                                     "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
-                                 for k, v in prof.items()}},
+                     "kernels": {k: {"launches": v["launches"], "excl_us": v["excl_us"], "own_us": v["own_us"],
+                                     "mb": v["bytes"] / 1e6,
+                                     "gbs": v["bytes"] / (v["own_us"] * 1e3) if v["own_us"] else None}
+                                 for k, v in kinds.items()},
+                     "launches": [{"kind": e["kind"], "start_us": round(e["start_us"], 2),
+                                   "end_us": round(e["end_us"], 2), "mb": round(e["bytes"] / 1e6, 3)}
+                                  for e in timeline],
+                     "eager_events": {k: {"launches": v["launches"] // args.profile_iters,
+                                          "ms": v["ms"] / args.profile_iters}
+                                      for k, v in prof.items()}},
     }
     s.close()
     if not args.no_sweep:

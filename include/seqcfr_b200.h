@@ -258,6 +258,19 @@ typedef struct scfr_kernel_stat {
     double bytes;
 } scfr_kernel_stat;
 int scfr_profile_step(scfr_handle* h, int64_t n_iter, scfr_kernel_stat* out, int cap, int* count);
+/* In-graph timeline of the level engine: runs n_iter iterations (they count,
+ * as with scfr_step) through a copy of the iteration graph whose kernels
+ * record their first-CTA start and last-CTA end (%globaltimer).  One span per
+ * launch of the iteration, times in microseconds from the iteration's first
+ * start, averaged over the iterations; bytes = the launch's algorithmic
+ * bytes.  Exclusive span i = end_i - end_(i-1) partitions the step. */
+typedef struct scfr_kernel_span {
+    char name[16];
+    int32_t kind;
+    double bytes;
+    double start_us, end_us;
+} scfr_kernel_span;
+int scfr_timeline(scfr_handle* h, int64_t n_iter, scfr_kernel_span* out, int cap, int* count);
 /* Process-wide bytes copied host->device and device->host by this library
  * (structure uploads, state reads); used for the end-to-end accounting. */
 int scfr_transfer_bytes(int64_t* h2d, int64_t* d2h);

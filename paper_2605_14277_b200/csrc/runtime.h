@@ -218,7 +218,29 @@ struct KParams {
     const long long* tdev;
     int post, do_rm, plus;
     int* nonfinite;
+    // scfr_timeline: first-CTA start / last-CTA end (%globaltimer ns) of this
+    // launch, slots [2 * tl_idx, 2 * tl_idx + 1]; null when not recording
+    unsigned long long* tl;
+    int tl_idx;
 };
+
+// Timeline records of a launch (scfr_timeline): every CTA's thread 0 after
+// the PDL wait (start: min) and after the CTA's last thread (end: max).
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// (the start slot holds the maximum of ~t, so both slots start at zero)
+__device__ __forceinline__ void tl_start(unsigned long long* tl, int idx) {
+    if (tl && threadIdx.x == 0) atomicMax(tl + 2 * idx, ~global_ns());
+}
+__device__ __forceinline__ void tl_end(unsigned long long* tl, int idx) {
+    if (tl) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(tl + 2 * idx + 1, global_ns());
+    }
+}
 
 // Tile engine plan of one player (tiled.cu): DPs below the split level are
 // renumbered tile-major (tile, level, root-first, original order) so every
@@ -444,10 +466,13 @@ namespace scfr {
 struct LaunchBase {
     scfr_handle* h;
     int64_t count = 0;
+    unsigned long long* tl = nullptr;  // scfr_timeline buffer while capturing its graph
+    std::vector<std::pair<int, double>>* tl_kinds = nullptr;  // (kind, bytes) per launch
     std::vector<KernelRecord>* prof = nullptr;  // per-launch events when profiling
 
     template <class F>
     void launch(int kind, double bytes, F&& f) {
+        if (tl_kinds) tl_kinds->emplace_back(kind, bytes * h->B);
         if (prof) {
             KernelRecord r;
             r.kind = kind;
@@ -502,7 +527,7 @@ void tiled_iteration(LaunchBase& L);
 // Device pointer to `buf` (a [B][S] vector of `player` in the engine's
 // numbering) for `solve`, in the reference's sequence order.
 const double* orig_order(scfr_handle* h, int player, const double* buf, int solve);
-__global__ void k_tick(long long* tdev);
+__global__ void k_tick(long long* tdev, unsigned long long* tl, int tl_idx);
 
 // Forest mode (forest.cu): plan at creation, per-iteration launches.
 bool prepare_forest(scfr_handle* h, const scfr_csr* U, const scfr_csr* UT);

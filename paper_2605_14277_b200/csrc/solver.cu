@@ -206,8 +206,11 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
         const bool valid = g < G && item < t.n;
         const int j = t.lo + (valid ? item : 0);
         if constexpr (KIND == LK_TD_AVG || KIND == LK_TD) {
-            R xp;  // the top's x is recomputed from the ancestor chain
-            if (t.top && valid) xp = top_x(t.top, t.b + so, parent_of<LdL1>(t.T, j));
+            R xp = R(0);  // the top's x, recomputed from the ancestor chain by the group's first lane
+            if (t.top) {
+                if (valid && a == 0) xp = top_x(t.top, t.b + so, parent_of<LdL1>(t.T, j));
+                xp = __shfl_sync(kFullMask, xp, gb);
+            }
             td_dp_group<LdL1s>(t.T, j, valid, a, n, t.b + so, t.x + so, KIND == LK_TD_AVG ? t.avg + so : nullptr, w,
                                t.top ? &xp : nullptr);
         } else if constexpr (KIND == LK_CUR) {
@@ -228,8 +231,10 @@ __global__ void __launch_bounds__(TPB, 8) k_level_g(const __grid_constant__ Task
                                                     const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
     pdl_wait();
+    tl_start(kp.tl, kp.tl_idx);
     if ((int)blockIdx.x < t0.nblk) level_body_group<KIND, N, R>(t0, blockIdx.x, kp);
     else level_body_group<KIND, N, R>(t1, blockIdx.x - t0.nblk, kp);
+    tl_end(kp.tl, kp.tl_idx);
 }
 
 // Narrow variants (<= 2 actions in registers: the deep, bandwidth-bound
@@ -244,8 +249,10 @@ __global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : WARP ? 4 : 1)
                                                const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
     pdl_wait();
+    tl_start(kp.tl, kp.tl_idx);
     if ((int)blockIdx.x < t0.nblk) level_body<KIND, MAXA, WARP, R>(t0, blockIdx.x, kp);
     else level_body<KIND, MAXA, WARP, R>(t1, blockIdx.x - t0.nblk, kp);
+    tl_end(kp.tl, kp.tl_idx);
 }
 
 template <class R>
@@ -361,10 +368,12 @@ __global__ void k_normalize(const double* __restrict__ a, double w, double* __re
     if (i < n) out[i] = ddiv(a[i], w);
 }
 
-__global__ void k_tick(long long* tdev) {
+__global__ void k_tick(long long* tdev, unsigned long long* tl, int tl_idx) {
     pdl_launch_dependents();
     pdl_wait();
+    tl_start(tl, tl_idx);
     *tdev += 1;
+    tl_end(tl, tl_idx);
 }
 
 // float(t) ** e with the reference's semantics (pkg/solvers.py:82-94, :172):
@@ -1031,7 +1040,7 @@ struct LevelBytes {  // v: bytes per value (8 fp64, 4 in the fp32 mode)
 KParams LaunchBase::kparams(bool do_rm) const {
     return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
                    post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
-                   h->nonfinite.p};
+                   h->nonfinite.p, tl, (int)count};
 }
 
 struct Launcher : LaunchBase {
@@ -1334,7 +1343,7 @@ struct Launcher : LaunchBase {
                 level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
                          nullptr, Bx, !pr, nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0, ob && k == 0);
         }
-        launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p); });
+        launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p, tl, (int)count); });
     }
 };
 
@@ -1528,7 +1537,8 @@ extern "C" {
 // launching every level (completing the top in-kernel by last arrival
 // measured slower than the launches it saved: DESIGN.md §4).
 static void prepare_top(scfr_handle* h, int k) {
-    constexpr int kTopDPs = 1 << 16;
+    int kTopDPs = 4096;  // SCFR_TOP_DPS: the cap (A/B: Goofspiel-5 137.4 us at 505 top DPs vs 142.1 us at 24505)
+    if (const char* e = std::getenv("SCFR_TOP_DPS")) kTopDPs = std::atoi(e);
     const char* off = std::getenv("SCFR_NO_TOP");
     if (off && off[0] == '1') return;
     Player& P = h->P[k];
@@ -1900,6 +1910,66 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
             cudaEventDestroy(r.e1);
         }
         *count = KK_COUNT;
+    });
+}
+
+int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int* count) {
+    return guarded([&] {
+        if (!h || !out || !count) fail(SCFR_EINVAL, "bad arguments");
+        if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
+        if (is_persistent(h->engine) || h->forest)
+            fail(SCFR_EINVAL, "the timeline covers the level engine's launches");
+        set_device(h);
+        add_weights(h, n);
+        preset_constant_rows(h);
+        // capture a recording copy of the iteration graph
+        std::vector<std::pair<int, double>> kinds;
+        DevBuf<unsigned long long> buf;
+        {
+            AllocStream alloc_on(h->stream);
+            buf.alloc(2 * 4096);
+        }
+        Launcher L(h);
+        L.tl = buf.p;
+        L.tl_kinds = &kinds;
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        L.iteration();
+        CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
+        CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        const int m = (int)kinds.size();
+        if (m > 4096 || m > cap) {
+            cudaGraphExecDestroy(exec);
+            fail(SCFR_EINVAL, "%d launches per iteration exceed the output capacity", m);
+        }
+        std::vector<unsigned long long> host(2 * m);
+        std::vector<double> st(m, 0.0), en(m, 0.0);
+        for (int64_t i = 0; i < n; ++i) {
+            CUDA_OK(cudaMemsetAsync(buf.p, 0, 2 * m * sizeof(unsigned long long), h->stream));
+            CUDA_OK(cudaGraphLaunch(exec, h->stream));
+            CUDA_OK(cudaMemcpyAsync(host.data(), buf.p, 2 * m * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, h->stream));
+            CUDA_OK(cudaStreamSynchronize(h->stream));
+            const unsigned long long t0 = ~host[0];
+            for (int k = 0; k < m; ++k) {
+                st[k] += (double)(long long)(~host[2 * k] - t0) / 1e3;
+                en[k] += (double)(long long)(host[2 * k + 1] - t0) / 1e3;
+            }
+        }
+        cudaGraphExecDestroy(exec);
+        h->timed = false;
+        h->t += n;
+        h->launches += n * m;
+        for (int k = 0; k < m; ++k) {
+            std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[kinds[k].first]);
+            out[k].kind = kinds[k].first;
+            out[k].bytes = kinds[k].second;
+            out[k].start_us = st[k] / (double)n;
+            out[k].end_us = en[k] / (double)n;
+        }
+        *count = m;
     });
 }
 

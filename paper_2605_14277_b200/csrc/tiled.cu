@@ -936,7 +936,7 @@ void tiled_iteration(LaunchBase& L) {
              pr ? h->tp[0].bytes_cur : h->tp[0].bytes_td);
         pass(L, kobs, true, TK_OBS, !pr, o2, nullptr, maxa, ob2);
     }
-    L.launch(KK_TICK, 0.0, [&] { L.run1(k_tick, dim3(1), h->tdev.p); });
+    L.launch(KK_TICK, 0.0, [&] { L.run1(k_tick, dim3(1), h->tdev.p, L.tl, (int)L.count); });
 }
 
 __global__ void k_scatter_seq(int S, const int* __restrict__ sperm, const double* __restrict__ src,

@@ -71,6 +71,11 @@ class KernelStat(C.Structure):
                 ("bytes", C.c_double)]
 
 
+class KernelSpan(C.Structure):
+    _fields_ = [("name", C.c_char * 16), ("kind", C.c_int32), ("bytes", C.c_double),
+                ("start_us", C.c_double), ("end_us", C.c_double)]
+
+
 class Config(C.Structure):
     _fields_ = [("variant", C.c_int32), ("mode", C.c_int32), ("alpha", C.c_double),
                 ("beta", C.c_double), ("gamma", C.c_double), ("batch", C.c_int32),
@@ -115,6 +120,10 @@ _SIGS = {
     "scfr_last_step_ms": ([C.c_void_p, f64p], C.c_int),
     "scfr_profile_step": ([C.c_void_p, C.c_int64, C.POINTER(KernelStat), C.c_int,
                            C.POINTER(C.c_int)], C.c_int),
+    "scfr_timeline": ([C.c_void_p, C.c_int64, C.POINTER(KernelSpan), C.c_int, C.POINTER(C.c_int)],
+                      C.c_int),
+    "scfr_trace_start": ([C.c_int], C.c_int),
+    "scfr_trace_read": ([i64p, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "scfr_transfer_bytes": ([i64p, i64p], C.c_int),
     "scfr_destroy": ([C.c_void_p], C.c_int),
 }

@@ -214,6 +214,22 @@ class Solver:
                                          "bytes": float(stats[k].bytes)}
                 for k in range(cnt.value) if stats[k].launches}
 
+    def timeline(self, n: int = 3) -> list[dict]:
+        """Run n real iterations through a recording copy of the iteration
+        graph; one entry per launch: kind, algorithmic bytes, mean start / end
+        (us from the iteration's first start, %globaltimer) and the exclusive
+        span end_i - end_(i-1), which partitions the in-graph step."""
+        spans = (N.KernelSpan * 4096)()
+        cnt = C.c_int()
+        N.check(N.lib().scfr_timeline(self._h, int(n), spans, 4096, C.byref(cnt)))
+        out, prev = [], 0.0
+        for k in range(cnt.value):
+            sp = spans[k]
+            out.append({"kind": sp.name.decode(), "bytes": float(sp.bytes), "start_us": float(sp.start_us),
+                        "end_us": float(sp.end_us), "excl_us": float(sp.end_us) - prev})
+            prev = float(sp.end_us)
+        return out
+
     # -- reads -----------------------------------------------------------------
     def _nseq(self, player: int) -> int:
         if player not in (1, 2):

@@ -1,0 +1,21 @@
+"""In-graph per-launch timeline of one Goofspiel-5 PCFR+ alt iteration
+(scfr_timeline): python scripts/micro/timeline.py [goof5] [n]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, flat_goofspiel  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "goof5"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+s = Solver(GameBundle(flat_goofspiel(int(name[-1]))), SolverConfig("pcfr+"), engine="levels")
+s.step(5)
+s.synchronize()
+tl = s.timeline(n)
+s.step(20)
+s.synchronize()
+print(f"graph step {s.last_step_ms() / 20 * 1e3:.1f} us; timeline end {tl[-1]['end_us']:.1f} us; launches {len(tl)}")
+for k, e in enumerate(tl):
+    gbs = e["bytes"] / (e["excl_us"] * 1e3) if e["excl_us"] > 0 else 0
+    print(f"{k:3d} {e['kind']:>8} start {e['start_us']:7.1f} end {e['end_us']:7.1f} excl {e['excl_us']:6.1f} us "
+          f"{e['bytes'] / 1e6:7.2f} MB {gbs:7.1f} GB/s")
