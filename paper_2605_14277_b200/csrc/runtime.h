@@ -413,6 +413,7 @@ struct scfr_handle {
     int64_t warp_nj = 4096;  // size limit of the fat / small warp rules (SCFR_WARP_NJ)
     bool bcur_on = false;  // predictive alt: OBS P1 writes RM(r) to P[0].bcur, CUR is a plain TD (SCFR_NO_BCUR=1: off)
     bool group = true;
+    bool pair = false;  // bottom-up group launches also compute the parent level (opt-in SCFR_PAIR=1)
     int64_t group_nj = 4096;  // group mode only above this many DPs per level (SCFR_GROUP_NJ)  // big affine 2..16-action levels run G = 32/n DPs per warp (SCFR_NO_GROUP=1: off)
     bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)
     bool leaf_skip = true;  // PRED skips a forced deepest level (kernels.cuh leaf_note; SCFR_NO_LEAF_SKIP)

@@ -74,6 +74,14 @@ struct TaskT {
     // parents' x come from their ancestor chains, and the launch also writes
     // the top's x (and average).
     const TopInfo* top;
+    // Parent pair (bottom-up group launches, Launcher::pair_ok): the launch
+    // also computes the parent level.  A warp takes pblk parent DPs, runs
+    // their pblk*pch children (this level, contiguous) in group rounds, then
+    // the parents from the children's V.
+    int pair, plo, pn, pblk, pch;
+    DevTree PT;       // the parent level's shape
+    FuseUT<R> pfu;    // the parent level's fused payoff rows (fu.ip unset: none)
+    const R* pu;      // the parent level's utility / prediction (null: empty rows)
 };
 using Task = TaskT<double>;
 
@@ -201,6 +209,40 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
     if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
     const R* Vc = t.Vc ? t.Vc + so : nullptr;
     if ((KIND == LK_TD_AVG || KIND == LK_TD) && t.top) top_prologue<KIND, R>(t, blk, w);
+    if constexpr (KIND == LK_OBS || KIND == LK_PRED) {
+        if (t.pair) {  // blocks of pblk parents: their children, then the parents
+            FuseUT<R> pfu = t.pfu;
+            if (KIND == LK_OBS && pfu.ip) pfu.x += (size_t)blockIdx.y * t.fu_sx;
+            const int pn2 = t.PT.un, pG = 32 / pn2, pg = lane / pn2, pa = lane - pg * pn2, pgb = pg * pn2;
+            for (int bi = blk * W + (int)(threadIdx.x >> 5); bi * t.pblk < t.pn; bi += t.nblk * W) {
+                const int p0 = bi * t.pblk, np = min(t.pblk, t.pn - p0);
+                const int c0 = p0 * t.pch, c1 = c0 + np * t.pch;
+                for (int base = c0; base < c1; base += G) {
+                    const int item = base + g;
+                    const bool valid = g < G && item < c1;
+                    const int j = t.lo + (valid ? item : c0);
+                    if constexpr (KIND == LK_OBS)
+                        obs_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so,
+                                               V, kp.post, pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc,
+                                               t.bw ? t.bw + so : nullptr);
+                    else
+                        pred_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so,
+                                                t.b + so, V, kp.plus != 0, Vc);
+                }
+                __syncwarp();  // the children's V (this warp's) before the parents read them
+                const bool pv = pg < pG && pg < np;
+                const int pj = t.plo + p0 + (pv ? pg : 0);
+                if constexpr (KIND == LK_OBS)
+                    obs_dp_group<LdL1s>(t.PT, pj, pv, pa, pgb, pn2, t.pu ? t.pu + so : nullptr, t.r + so, t.b + so, V,
+                                        kp.post, pf, nf, kp.do_rm != 0, kp.nonfinite, pfu,
+                                        static_cast<const R*>(nullptr), t.bw ? t.bw + so : nullptr);
+                else
+                    pred_dp_group<LdL1s>(t.PT, pj, pv, pa, pgb, pn2, t.pu ? t.pu + so : nullptr, t.r + so, t.b + so,
+                                         V, kp.plus != 0, static_cast<const R*>(nullptr));
+            }
+            return;
+        }
+    }
     for (int wi = blk * W + (int)(threadIdx.x >> 5); wi * G < t.n; wi += t.nblk * W) {
         const int item = wi * G + g;
         const bool valid = g < G && item < t.n;
@@ -1048,6 +1090,21 @@ struct Launcher : LaunchBase {
     // predictive alt mode: player 1's OBS regret-matches into bcur (instead
     // of b, which PRED still needs) and CUR reads it as a plain TD
     void* bcur_ = nullptr;
+    // parent pairs: the level (and pass kind) each player's last pair launch
+    // already computed
+    int paired_[2] = {-1, -1}, paired_kind_[2] = {-1, -1};
+    // Level l can carry its parent level l-1 in one group launch: both
+    // uniform group-width levels, and the parents' children are exactly level
+    // l, contiguous, the same number per parent (opt-in SCFR_PAIR=1: a warp's
+    // block is one serial chain of rounds, 164 vs 145 us on Goofspiel-5).
+    bool pair_ok(const Player& P, int l) const {
+        if (!h->pair || l < 1 || l >= P.levels()) return false;
+        const DevTree& c = P.lvl_shape[l];
+        const DevTree& p = P.lvl_shape[l - 1];
+        if (c.un < 2 || c.un > 16 || p.un < 2 || p.un > 16 || p.cn < 1) return false;
+        if (p.c_lo != P.lvl[l] || (double)p.un * p.cn * P.lvl_nj[l - 1] != P.lvl_nj[l]) return false;
+        return true;
+    }
     // first level of player P that top-down passes launch (the top's are not)
     int first_level(const Player& P) const {
         const int k = &P == &h->P[0] ? 0 : 1;
@@ -1132,6 +1189,9 @@ struct Launcher : LaunchBase {
     void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
                R* xa, R* xb, bool do_rm, const R* vca = nullptr, const R* vcb = nullptr, int skipa = 0,
                int skipb = 0) {
+        // a level already computed by its child level's pair launch
+        if (A && la >= 0 && la == paired_[0] && lk == paired_kind_[0]) la = -1;
+        if (Bp && lb >= 0 && lb == paired_[1] && lk == paired_kind_[1]) lb = -1;
         TaskT<R> t0 = A ? task<R>(*A, la, ua, xa) : TaskT<R>{};
         TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
         t0.Vc = vca;
@@ -1235,6 +1295,49 @@ struct Launcher : LaunchBase {
             gun = ua < 0 ? ub : ub < 0 ? ua : ua == ub ? ua : 0;
         }
         const LevelKernelT<R> kern = group ? pick_group_kernel<R>(lk, gun) : pick_level_kernel<R>(lk, maxa, warp);
+        // parent pairs: a bottom-up group launch also computes the parent level
+        if (group && (lk == LK_OBS || lk == LK_PRED)) {
+            auto pair = [&](TaskT<R>& t, Player* P, int l, int skip_v, const R* u) {
+                if (!P || !pair_ok(*P, l) || skip_v) return;
+                const DevTree& ps = P->lvl_shape[l - 1];
+                const int G = 32 / P->lvl_shape[l].un, pG = 32 / ps.un, C = ps.un * ps.cn;
+                int pb = pG;
+                for (int q = pG; q >= 1; --q)
+                    if ((q * C) % G == 0) {
+                        pb = q;
+                        break;
+                    }
+                t.pair = 1;
+                t.plo = P->lvl[l - 1];
+                t.pn = P->lvl[l] - P->lvl[l - 1];
+                t.pblk = pb;
+                t.pch = C;
+                t.PT = shaped_tree(*P, l - 1);
+                t.pu = u;
+                t.pfu = FuseUT<R>{};
+                const DevCsr& M = P == &h->P[0] ? h->U : h->UT;  // the player's payoff rows
+                const bool empty = h->u_empty_skip && rows_empty(*P, l - 1, M);
+                if (empty) t.pu = nullptr;
+                if (lk == LK_OBS && fused && !empty) {
+                    t.pfu = t.fu.ip ? t.fu : FuseUT<R>{M.indptr.p, M.iter_indices(), payoff_data<R>(M),
+                                                        P == &h->P[0] ? vals<R>(h->P[1].x)
+                                                                      : (h->mode == SCFR_MODE_ALT ? vals<R>(h->P[0].xpost)
+                                                                                                  : vals<R>(h->P[0].x)),
+                                                        P == &h->P[0] ? 0 : 1};
+                    t.pfu.rc = 0;
+                    if (h->affine_rows) set_row_shape(t.pfu, M, P, l - 1);
+                    if (!t.fu.ip) t.fu_sx = P == &h->P[0] ? h->P[1].S : h->P[0].S;
+                }
+                const int k = P == &h->P[0] ? 0 : 1;
+                paired_[k] = l - 1;
+                paired_kind_[k] = lk;
+                bytes += lk == LK_OBS ? LevelBytes::obs(*P, l - 1, do_rm, sizeof(R)) : LevelBytes::pred(*P, l - 1, sizeof(R));
+                // the parents of a block are processed by the warp of their children
+                t.nblk = std::min(t.nblk, std::max(1, (t.pn + t.pblk * (TPB / 32) - 1) / (t.pblk * (TPB / 32))));
+            };
+            pair(t0, A, la, skipa, ua);
+            pair(t1, Bp, lb, skipb, ub);
+        }
         // grid-stride tasks: cap each at one resident wave of this kernel
         const int wave = resident_ctas(kern);
         t0.nblk = std::min(t0.nblk, wave);
@@ -1741,6 +1844,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->leaf_skip = !(nls && nls[0] == '1');
         const char* ngr = std::getenv("SCFR_NO_GROUP");
         h->group = !(ngr && ngr[0] == '1');
+        const char* npr = std::getenv("SCFR_PAIR");  // opt-in: measured slower
+        h->pair = npr && npr[0] == '1';
         if (const char* gnj = std::getenv("SCFR_GROUP_NJ")) h->group_nj = std::atoll(gnj);
         const char* nsw = std::getenv("SCFR_NO_SMALL_WARP");
         h->small_warp = !(nsw && nsw[0] == '1');
