@@ -528,6 +528,14 @@ template <class Ld, class R>
 __device__ __forceinline__ R lane_child_value(int2 c, const R* __restrict__ V) {
     if (c.y == 0) return R(0);
     if (c.y == 1) return Ld::ld(V + c.x);
+    if (c.y <= 4) {  // the common small observation points, unpredicated (same order)
+        const R v0 = Ld::ld(V + c.x), v1 = Ld::ld(V + c.x + 1);
+        if (c.y == 2) return dadd(dadd(R(0), v0), v1);
+        const R v2 = Ld::ld(V + c.x + 2);
+        if (c.y == 3) return dadd(dadd(dadd(R(0), v0), v1), v2);
+        const R v3 = Ld::ld(V + c.x + 3);
+        return dadd(dadd(dadd(dadd(R(0), v0), v1), v2), v3);
+    }
     constexpr int CH = Ld::kChunk;
     R acc = R(0);
     for (int base = 0; base < c.y; base += CH) {
@@ -567,7 +575,20 @@ __device__ __forceinline__ R lane_seq_sum(R v, int n) {
 template <int N = 0, class R>
 __device__ __forceinline__ R group_seq_sum(R v, int gb, int n) {
     R acc = R(0);
-    if constexpr (N > 0) {
+    if constexpr (N == 2) {  // one shuffle: the partner's value (groups are aligned pairs)
+        const R o = __shfl_xor_sync(kFullMask, v, 1);
+        const bool first = ((threadIdx.x & 31) - gb) == 0;
+        return dadd(dadd(R(0), first ? v : o), first ? o : v);
+    } else if constexpr (N == 3) {  // two shuffles: the other two members, by rotation
+        const int a = (int)(threadIdx.x & 31) - gb;
+        const R n1 = __shfl_sync(kFullMask, v, gb + (a == 2 ? 0 : a + 1));
+        const R n2 = __shfl_sync(kFullMask, v, gb + (a == 0 ? 2 : a - 1));
+        // member values in group order: a = 0 -> (v, n1, n2), 1 -> (n2, v, n1), 2 -> (n1, n2, v)
+        const R v0 = a == 0 ? v : a == 1 ? n2 : n1;
+        const R v1 = a == 0 ? n1 : a == 1 ? v : n2;
+        const R v2 = a == 0 ? n2 : a == 1 ? n1 : v;
+        return dadd(dadd(dadd(R(0), v0), v1), v2);
+    } else if constexpr (N > 0) {
 #pragma unroll
         for (int a = 0; a < N; ++a) acc = dadd(acc, __shfl_sync(kFullMask, v, gb + a));
     } else {
@@ -581,7 +602,11 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
                                              const R* __restrict__ u, R* __restrict__ r, R* __restrict__ b,
                                              R* __restrict__ V, int post, typename nd<R>::type pf,
                                              typename nd<R>::type nf, bool do_rm, int* nonfinite,
-                                             FuseUT<R> fuse, const R* Vc, R* bw = nullptr) {
+                                             FuseUT<R> fuse, const R* Vc, R* bw = nullptr, R* r_out = nullptr,
+                                             const FuseUT<R>* cfu = nullptr, R* cu = nullptr, int cshift = 0) {
+    // cfu: the child level is a forced leaf level whose utilities are
+    // computed here (its fused payoff rows, written to cu) and used as the
+    // child values directly (leaf_note); child DP c is sequence c + cshift
     if constexpr (N > 0) n = N;
     const R* Vr = Vc ? Vc : V;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
@@ -592,7 +617,41 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
         const R uu = fuse.ip ? fused_u<Ld>(fuse, const_cast<R*>(u), s, bad) : ld_u<Ld>(u, s);
         bb = Ld::ld(b + s);
         rr = Ld::ld(r + s);
-        q = dadd(dadd(R(0), uu), lane_child_value<Ld>(c, Vr));
+        R cv;
+        if (cfu) {  // in-order child sum, as lane_child_value
+            auto row = [&](int sc) {  // (±) payoff row sc, as fused_u without the store
+                R v;
+                if (cfu->rc > 0) {
+                    const int k0 = cfu->rk0 + (sc - cfu->rs0) * cfu->rc;
+                    v = spmv_range<Ld>(cfu->ix, cfu->d, cfu->x, k0, k0 + cfu->rc);
+                } else {
+                    v = spmv_row<Ld>(cfu->ip, cfu->ix, cfu->d, cfu->x, sc);
+                }
+                if (cfu->neg) v = dmul(R(-1), v);
+                bad |= !isfinite(v);
+                return v;
+            };
+            const int c0 = c.x + cshift;
+            if (c.y == 1) {
+                cv = row(c0);
+                cu[c0] = cv;
+            } else if (c.y == 2) {  // both rows' loads in flight before the stores
+                const R v0 = row(c0), v1 = row(c0 + 1);
+                cu[c0] = v0;
+                cu[c0 + 1] = v1;
+                cv = dadd(dadd(R(0), v0), v1);
+            } else {
+                cv = R(0);
+                for (int k = 0; k < c.y; ++k) {
+                    const R v = row(c0 + k);
+                    cu[c0 + k] = v;
+                    cv = dadd(cv, v);
+                }
+            }
+        } else {
+            cv = lane_child_value<Ld>(c, Vr);
+        }
+        q = dadd(dadd(R(0), uu), cv);
     }
     const R E = group_seq_sum<N>(dmul(bb, q), gb, n);
     if (valid && a == 0) V[j] = E;
@@ -602,7 +661,7 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
         bad |= !isfinite(q);
         rv = post_op(dadd(rr, dadd(negE, q)), post, pf, nf);
         bad |= !isfinite(rv);
-        r[s] = rv;
+        (r_out ? r_out : r)[s] = rv;
     }
     const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
     if (do_rm && valid) (bw ? bw : b)[s] = rm_prob(rv, S, n);
@@ -612,7 +671,8 @@ __device__ __forceinline__ void obs_dp_group(const DevTree& T, int j, bool valid
 template <class Ld, int N = 0, class R>
 __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool valid, int a, int gb, int n,
                                               const R* __restrict__ m, const R* __restrict__ r,
-                                              R* __restrict__ b, R* __restrict__ V, bool plus, const R* Vc) {
+                                              R* __restrict__ b, R* __restrict__ V, bool plus, const R* Vc,
+                                              R* b_out = nullptr) {
     if constexpr (N > 0) n = N;
     const R* Vr = Vc ? Vc : V;
     const int s = T.s_lo + (j - T.j_lo) * n + a;
@@ -633,7 +693,7 @@ __device__ __forceinline__ void pred_dp_group(const DevTree& T, int j, bool vali
         if (plus) rv = rv > R(0) ? rv : R(0);
     }
     const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
-    if (valid) b[s] = rm_prob(rv, S, n);
+    if (valid) (b_out ? b_out : b)[s] = rm_prob(rv, S, n);
 }
 
 // TD (+ average): x[s] = b[s] * x[parent(j)], avg[s] = w*x[s] + avg[s].

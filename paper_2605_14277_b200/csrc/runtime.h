@@ -413,6 +413,11 @@ struct scfr_handle {
     int64_t warp_nj = 4096;  // size limit of the fat / small warp rules (SCFR_WARP_NJ)
     bool bcur_on = false;  // predictive alt: OBS P1 writes RM(r) to P[0].bcur, CUR is a plain TD (SCFR_NO_BCUR=1: off)
     bool group = true;
+    bool leaf_fuse = true;  // OBS: the forced leaf level computed in the group launch above it (SCFR_NO_LEAF_FUSE=1)
+    bool pipe = true;            // big affine group levels: the cp.async-pipelined kernel (SCFR_NO_PIPE=1: off)
+    int64_t pipe_nj = 65536;     // ... on levels of at least this many DPs (SCFR_PIPE_NJ)
+    int pipe_kinds = 1 << 0;     // ... for these LK_* kinds (SCFR_PIPE_KINDS bit mask; TD + average only:
+                                 //     OBS / PRED / CUR measured slower pipelined)
     bool pair = false;  // bottom-up group launches also compute the parent level (opt-in SCFR_PAIR=1)
     int64_t group_nj = 4096;  // group mode only above this many DPs per level (SCFR_GROUP_NJ)  // big affine 2..16-action levels run G = 32/n DPs per warp (SCFR_NO_GROUP=1: off)
     bool td_warp = true;    // top-down passes warp-per-DP on wide levels (SCFR_NO_TD_WARP=1: thread per DP)

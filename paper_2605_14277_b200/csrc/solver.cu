@@ -74,6 +74,13 @@ struct TaskT {
     // parents' x come from their ancestor chains, and the launch also writes
     // the top's x (and average).
     const TopInfo* top;
+    // OBS group launch over the level above a forced leaf level: the leaf's
+    // fused payoff rows are computed here (lfu.ip set), u written, used as
+    // the child values; the leaf launch is skipped.  Child DP c is sequence
+    // c + lshift.
+    FuseUT<R> lfu;
+    int lshift;
+    R* tu_leaf;  // the utility array the leaf rows are written to
     // Parent pair (bottom-up group launches, Launcher::pair_ok): the launch
     // also computes the parent level.  A warp takes pblk parent DPs, runs
     // their pblk*pch children (this level, contiguous) in group rounds, then
@@ -258,8 +265,18 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
         } else if constexpr (KIND == LK_CUR) {
             cur_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.r + so, t.x + so);
         } else if constexpr (KIND == LK_OBS) {
-            obs_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V, kp.post,
-                               pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc, t.bw ? t.bw + so : nullptr);
+            if (t.lfu.ip) {
+                FuseUT<R> lfu = t.lfu;
+                lfu.x += (size_t)blockIdx.y * t.fu_sx;
+                obs_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
+                                       kp.post, pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc,
+                                       t.bw ? t.bw + so : nullptr, static_cast<R*>(nullptr), &lfu, t.tu_leaf + so,
+                                       t.lshift);
+            } else {
+                obs_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
+                                       kp.post, pf, nf, kp.do_rm != 0, kp.nonfinite, fu, Vc,
+                                       t.bw ? t.bw + so : nullptr);
+            }
         } else {
             pred_dp_group<LdL1s, N>(t.T, j, valid, a, gb, n, t.u ? t.u + so : nullptr, t.r + so, t.b + so, V,
                                 kp.plus != 0, Vc);
@@ -267,8 +284,11 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
     }
 }
 
+#ifndef SCFR_GROUP_MINB
+#define SCFR_GROUP_MINB 8
+#endif
 template <int KIND, int N, class R>
-__global__ void __launch_bounds__(TPB, 8) k_level_g(const __grid_constant__ TaskT<R> t0,
+__global__ void __launch_bounds__(TPB, SCFR_GROUP_MINB) k_level_g(const __grid_constant__ TaskT<R> t0,
                                                     const __grid_constant__ TaskT<R> t1,
                                                     const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
@@ -276,6 +296,140 @@ __global__ void __launch_bounds__(TPB, 8) k_level_g(const __grid_constant__ Task
     tl_start(kp.tl, kp.tl_idx);
     if ((int)blockIdx.x < t0.nblk) level_body_group<KIND, N, R>(t0, blockIdx.x, kp);
     else level_body_group<KIND, N, R>(t1, blockIdx.x - t0.nblk, kp);
+    tl_end(kp.tl, kp.tl_idx);
+}
+
+// --- pipelined group mode --------------------------------------------------
+// The big affine levels are bound by the loads each warp keeps in flight: a
+// group round issues ~4 per lane and waits a full HBM round trip for them
+// (Little's law: ~5 MB in flight across the GPU, ~3 TB/s).  Here every warp
+// stages the inputs of its next kPipe - 1 rounds into shared memory with
+// cp.async (LDGSTS: per-lane addresses, no registers held) while it computes
+// the current round from the staged copy.  Slot layout (R values): up passes
+// [u | b | r | child values, cn per sequence], top-down [b or r | avg |
+// parent x], 32 lanes each.  The per-round arithmetic is the group code.
+constexpr int kPipe = 4;
+
+template <class R>
+__device__ __forceinline__ void cp_async_val(R* dst, const R* src) {
+    if constexpr (sizeof(R) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(src)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(src)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory");
+}
+
+template <int KIND, int N, class R>
+__device__ __forceinline__ void level_body_gp(const TaskT<R>& t, int blk, const KParams& kp, R* smem) {
+    constexpr int W = TPB / 32;
+    constexpr bool UP = KIND == LK_OBS || KIND == LK_PRED;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t so = (size_t)blockIdx.y * t.S;
+    R* V = t.V + (size_t)blockIdx.y * (t.J > 0 ? t.J : 1);
+    constexpr int n = N, G = 32 / N;
+    const int g = lane / n, a = lane - g * n, gb = g * n;
+    R w = R(0), pf = R(1), nf = R(1);
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_OBS && kp.post == POST_DCFR) {
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        pf = (R)kp.pfsched[k];
+        nf = (R)kp.nfsched[k];
+    }
+    FuseUT<R> fu = t.fu;
+    if (KIND == LK_OBS && fu.ip) fu.x += (size_t)blockIdx.y * t.fu_sx;
+    const DevTree& T = t.T;
+    const int cn = UP ? T.cn : 0;
+    const int sv = 32 * (3 + cn);  // R values per slot
+    R* wsm = smem + (size_t)warp * kPipe * sv;
+    const R* Vr = t.Vc ? t.Vc + so : V;
+    const R* ug = t.u ? t.u + so : nullptr;
+    const bool stage_u = UP && ug && !fu.ip;
+    const int ngroups = (t.n + G - 1) / G;
+    const int first = blk * W + warp, stride = t.nblk * W;
+    auto stage = [&](int wi, int q) {
+        if (wi >= ngroups) return;
+        const int j0 = t.lo + wi * G;
+        const int ns = min(G, t.n - wi * G) * n;
+        const int s0 = T.s_lo + (j0 - T.j_lo) * n;
+        R* sl = wsm + q * sv;
+        if (lane < ns) {
+            const int s = s0 + lane;
+            if constexpr (UP) {
+                if (stage_u) cp_async_val(sl + lane, ug + s);
+                cp_async_val(sl + 32 + lane, t.b + so + s);
+                cp_async_val(sl + 64 + lane, t.r + so + s);
+                const int c0 = T.c_lo + (s - T.s_lo) * cn;
+                for (int c = 0; c < cn; ++c) cp_async_val(sl + 96 + lane * cn + c, Vr + c0 + c);
+            } else {
+                cp_async_val(sl + lane, (KIND == LK_CUR ? t.r : t.b) + so + s);
+                if (KIND == LK_TD_AVG) cp_async_val(sl + 32 + lane, t.avg + so + s);
+                cp_async_val(sl + 64 + lane, t.x + so + parent_of<LdL1>(T, j0 + lane / n));
+            }
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < kPipe - 1; ++i) {
+        stage(first + i * stride, i);
+        cp_async_commit();
+    }
+    for (int i = 0; first + i * stride < ngroups; ++i) {
+        const int wi = first + i * stride;
+        stage(first + (i + kPipe - 1) * stride, (i + kPipe - 1) % kPipe);
+        cp_async_commit();
+        cp_async_wait<kPipe - 1>();  // this lane's copies of round i
+        __syncwarp();                // ... and every lane's
+        R* sl = wsm + (i % kPipe) * sv;
+        const int j0 = t.lo + wi * G;
+        const int s0 = T.s_lo + (j0 - T.j_lo) * n;
+        const int item = wi * G + g;
+        const bool valid = g < G && item < t.n;
+        const int j = t.lo + (valid ? item : wi * G);
+        if constexpr (UP) {
+            const R* u_arg = fu.ip ? ug : stage_u ? sl - s0 : nullptr;
+            const R* vc = sl + 96 - (T.c_lo + (s0 - T.s_lo) * cn);
+            if constexpr (KIND == LK_OBS)
+                obs_dp_group<LdS, N>(T, j, valid, a, gb, n, u_arg, sl + 64 - s0, sl + 32 - s0, V, kp.post, pf, nf,
+                                     kp.do_rm != 0, kp.nonfinite, fu, vc, t.bw ? t.bw + so : t.b + so, t.r + so);
+            else
+                pred_dp_group<LdS, N>(T, j, valid, a, gb, n, u_arg, sl + 64 - s0, sl + 32 - s0, V, kp.plus != 0, vc,
+                                      t.b + so);
+        } else {
+            // td_dp_group / cur_dp_group on the staged copies
+            const R xp = sl[64 + lane];
+            const int s = s0 + lane;
+            if constexpr (KIND == LK_CUR) {
+                const R rv = valid ? sl[lane] : R(0);
+                const R S = group_seq_sum<N>(rv > R(0) ? rv : R(0), gb, n);
+                if (valid) t.x[so + s] = dmul(rm_prob(rv, S, n), xp);
+            } else if (valid) {
+                const R xa = dmul(sl[lane], xp);
+                t.x[so + s] = xa;
+                if (KIND == LK_TD_AVG) t.avg[so + s] = dadd(dmul(w, xa), sl[32 + lane]);
+            }
+        }
+        __syncwarp();  // round i's slot is restaged at i + 1
+    }
+    cp_async_wait<0>();
+}
+
+template <int KIND, int N, class R>
+__global__ void __launch_bounds__(TPB, 8) k_level_gp(const __grid_constant__ TaskT<R> t0,
+                                                     const __grid_constant__ TaskT<R> t1,
+                                                     const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) unsigned char gsm[];
+    pdl_launch_dependents();
+    pdl_wait();
+    tl_start(kp.tl, kp.tl_idx);
+    if ((int)blockIdx.x < t0.nblk) level_body_gp<KIND, N, R>(t0, blockIdx.x, kp, reinterpret_cast<R*>(gsm));
+    else level_body_gp<KIND, N, R>(t1, blockIdx.x - t0.nblk, kp, reinterpret_cast<R*>(gsm));
     tl_end(kp.tl, kp.tl_idx);
 }
 
@@ -300,6 +454,18 @@ __global__ void __launch_bounds__(TPB, (MAXA <= 2 && !WARP) ? 12 : WARP ? 4 : 1)
 template <class R>
 using LevelKernelT = void (*)(TaskT<R>, TaskT<R>, KParams);
 using LevelKernel = LevelKernelT<double>;
+
+template <int N, class R>
+static LevelKernelT<R> pick_pipe_kernel_n(int kind) {
+    switch (kind) {
+        case LK_TD_AVG: return k_level_gp<LK_TD_AVG, N, R>;
+        case LK_TD: return k_level_gp<LK_TD, N, R>;
+        case LK_CUR: return k_level_gp<LK_CUR, N, R>;
+        case LK_OBS: return k_level_gp<LK_OBS, N, R>;
+        default: return k_level_gp<LK_PRED, N, R>;
+    }
+}
+
 
 // Warp-per-DP only pays on small, fat levels: few DPs (parallelism is
 // scarce, so per-DP latency is the critical path) with >= 8 child-DP
@@ -1090,6 +1256,17 @@ struct Launcher : LaunchBase {
     // predictive alt mode: player 1's OBS regret-matches into bcur (instead
     // of b, which PRED still needs) and CUR reads it as a plain TD
     void* bcur_ = nullptr;
+    // OBS: the forced leaf level of player k is computed inside the group
+    // launch of the level above (TaskT::lfu), set per pass by iteration_t
+    bool lf_[2] = {false, false};
+    bool leaf_fusable(const Player& P) const {
+        if (!h->leaf_fuse || !fuse_spmv() || !leaf_single(P) || !h->group) return false;
+        const int l = P.levels() - 2;
+        if (l < 1) return false;  // (level 0 never runs in group mode)
+        const DevTree& sh = P.lvl_shape[l];
+        return sh.un >= 2 && sh.un <= 16 && P.lvl_nj[l] > h->group_nj && !warp_level(h, P, l) &&
+               !(h->pipe && ((h->pipe_kinds >> LK_OBS) & 1));
+    }
     // parent pairs: the level (and pass kind) each player's last pair launch
     // already computed
     int paired_[2] = {-1, -1}, paired_kind_[2] = {-1, -1};
@@ -1226,6 +1403,33 @@ struct Launcher : LaunchBase {
                 set_row_shape(t1.fu, h->UT, Bp, lb);
             }
         }
+        // a forced leaf level computed inside this launch (leaf_fusable)
+        double leaf_bytes = 0.0;
+        if (lk == LK_OBS && fused) {
+            auto attach_leaf = [&](TaskT<R>& t, Player* P, int l) {
+                const int k = P == &h->P[0] ? 0 : 1;
+                if (!P || !lf_[k] || l != P->levels() - 2) return;
+                const DevCsr& M = k == 0 ? h->U : h->UT;
+                const int ll = P->levels() - 1;
+                t.lfu = FuseUT<R>{M.indptr.p, M.iter_indices(), payoff_data<R>(M),
+                                  k == 0 ? vals<R>(h->P[1].x)
+                                         : (h->mode == SCFR_MODE_ALT ? vals<R>(h->P[0].xpost) : vals<R>(h->P[0].x)),
+                                  k};
+                if (h->affine_rows) set_row_shape(t.lfu, M, P, ll);
+                t.lshift = P->lvl_shape[ll].s_lo - P->lvl_shape[ll].j_lo;
+                t.tu_leaf = vals<R>(P->u);
+                t.fu_sx = h->P[1 - k].S;
+                t.Vc = nullptr;
+                const double ns = P->lvl_ns[ll];
+                const double nnz = (double)(M.ptr_at(P->lvl_s0[ll] + (int)ns) - M.ptr_at(P->lvl_s0[ll]));
+                const bool shaped = h->affine_rows && ll < (int)M.lvl_rowc.size() && M.lvl_rowc[ll] >= 1;
+                // the leaf's rows (indptr, indices + data, x gathers) and its u writes
+                // replace the launch's reads of the leaf utilities
+                leaf_bytes += (shaped ? 0.0 : 4.0 * (ns + 1)) + (4.0 + sizeof(R)) * nnz + sizeof(R) * nnz;
+            };
+            attach_leaf(t0, A, la);
+            attach_leaf(t1, Bp, lb);
+        }
         // levels whose payoff rows are all empty: u is a constant ±0.0
         // (kernels.cuh ld_u), neither computed nor read
         bool empty[2] = {false, false};
@@ -1294,6 +1498,7 @@ struct Launcher : LaunchBase {
             const int ub = Bp && lb >= 0 && lb < Bp->levels() ? Bp->lvl_shape[lb].un : -1;
             gun = ua < 0 ? ub : ub < 0 ? ua : ua == ub ? ua : 0;
         }
+        bytes += leaf_bytes;
         const LevelKernelT<R> kern = group ? pick_group_kernel<R>(lk, gun) : pick_level_kernel<R>(lk, maxa, warp);
         // parent pairs: a bottom-up group launch also computes the parent level
         if (group && (lk == LK_OBS || lk == LK_PRED)) {
@@ -1337,6 +1542,52 @@ struct Launcher : LaunchBase {
             };
             pair(t0, A, la, skipa, ua);
             pair(t1, Bp, lb, skipb, ub);
+        }
+        // big affine group levels: the cp.async-pipelined variant (one width,
+        // affine children / parents, no top, no pair)
+        size_t psmem = 0;
+        LevelKernelT<R> pkern = nullptr;
+        if (group && h->pipe && gun >= 2 && gun <= 4 && ((h->pipe_kinds >> lk) & 1)) {
+            auto pipeable = [&](const TaskT<R>& t, Player* P, int l) {
+                if (!P || l < 0 || l >= P->levels()) return true;  // absent task
+                const DevTree& sh = P->lvl_shape[l];
+                if (P->lvl_nj[l] < h->pipe_nj || t.top || t.pair || t.skip_v) return false;
+                if (lk == LK_OBS || lk == LK_PRED) return sh.cn >= 0 && sh.cn <= 8;
+                return sh.pc > 0;
+            };
+            if (pipeable(t0, A, la) && pipeable(t1, Bp, lb) && (t0.n > 0 || t1.n > 0)) {
+                int cn = 0;
+                if (lk == LK_OBS || lk == LK_PRED)
+                    for (int k = 0; k < 2; ++k) {
+                        Player* P = k == 0 ? A : Bp;
+                        const int l = k == 0 ? la : lb;
+                        if (P && l >= 0 && l < P->levels()) cn = std::max(cn, P->lvl_shape[l].cn);
+                    }
+                // both tasks index their slots with the widest child count
+                if (lk == LK_OBS || lk == LK_PRED) {
+                    const int ca = A && la >= 0 && la < A->levels() ? A->lvl_shape[la].cn : cn;
+                    const int cb = Bp && lb >= 0 && lb < Bp->levels() ? Bp->lvl_shape[lb].cn : cn;
+                    if (ca != cb) cn = -1;
+                }
+                if (cn >= 0) {
+                    psmem = (size_t)(TPB / 32) * kPipe * 32 * (3 + cn) * sizeof(R);
+                    switch (gun) {
+                        case 2: pkern = pick_pipe_kernel_n<2, R>(lk); break;
+                        case 3: pkern = pick_pipe_kernel_n<3, R>(lk); break;
+                        default: pkern = pick_pipe_kernel_n<4, R>(lk); break;
+                    }
+                }
+            }
+        }
+        if (pkern) {
+            int occ = 0;
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pkern, TPB, psmem));
+            const int wave = std::max(1, occ) * h->num_sms;
+            t0.nblk = std::min(t0.nblk, wave);
+            t1.nblk = std::min(t1.nblk, wave);
+            const KParams kp = kparams(do_rm);
+            launch(kk, bytes, [&] { run_ex(pkern, dim3(t0.nblk + t1.nblk, h->B), TPB, psmem, t0, t1, kp); });
+            return;
         }
         // grid-stride tasks: cap each at one resident wave of this kernel
         const int wave = resident_ctas(kern);
@@ -1424,16 +1675,22 @@ struct Launcher : LaunchBase {
         if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
             if (!fused) spmv<R>(h->UT, Ax, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1
+            lf_[0] = lf_[1] = leaf_fusable(A) && leaf_fusable(Bp) && LA == LB;  // (one launch: both or none)
             for (int k = 0; k < L; ++k)
-                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, &Bp, LB - 1 - k, Au, Bu, Ax, Bx,
-                         !pr, oa && k == 1 ? leaf_u(A, Au) : nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr,
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, lf_[0] && k == 0 ? -1 : LA - 1 - k, &Bp,
+                         lf_[1] && k == 0 ? -1 : LB - 1 - k, Au, Bu, Ax, Bx, !pr,
+                         oa && k == 1 ? leaf_u(A, Au) : nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr,
                          oa && k == 0, ob && k == 0);
+            lf_[0] = lf_[1] = false;
         } else {
             const bool bc = pr && h->bcur_on;
             if (bc) bcur_ = vals<R>(A.bcur);
+            lf_[0] = leaf_fusable(A);
             for (int k = 0; k < LA; ++k)
-                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, LA - 1 - k, nullptr, -1, Au, nullptr, Ax,
-                         nullptr, !pr || bc, oa && k == 1 ? leaf_u(A, Au) : nullptr, nullptr, oa && k == 0, 0);
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, &A, lf_[0] && k == 0 ? -1 : LA - 1 - k, nullptr, -1, Au,
+                         nullptr, Ax, nullptr, !pr || bc, oa && k == 1 ? leaf_u(A, Au) : nullptr, nullptr,
+                         oa && k == 0, 0);
+            lf_[0] = false;
             // current_strategy of player 1 into xpost: TD of the b that OBS
             // already regret-matched (into b, or into bcur for the predictive
             // variants), or RM on the fly (SCFR_NO_BCUR=1)
@@ -1442,9 +1699,12 @@ struct Launcher : LaunchBase {
                          nullptr, -1, nullptr, nullptr, Axp, nullptr, false);
             bcur_ = nullptr;
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
+            lf_[1] = leaf_fusable(Bp);
             for (int k = 0; k < LB; ++k)
-                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, LB - 1 - k, nullptr, Bu,
-                         nullptr, Bx, !pr, nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0, ob && k == 0);
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, lf_[1] && k == 0 ? -1 : LB - 1 - k,
+                         nullptr, Bu, nullptr, Bx, !pr, nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0,
+                         ob && k == 0);
+            lf_[1] = false;
         }
         launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p, tl, (int)count); });
     }
@@ -1844,6 +2104,12 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         h->leaf_skip = !(nls && nls[0] == '1');
         const char* ngr = std::getenv("SCFR_NO_GROUP");
         h->group = !(ngr && ngr[0] == '1');
+        const char* nlf = std::getenv("SCFR_NO_LEAF_FUSE");
+        h->leaf_fuse = !(nlf && nlf[0] == '1');
+        const char* npp = std::getenv("SCFR_NO_PIPE");
+        h->pipe = !(npp && npp[0] == '1');
+        if (const char* pnj = std::getenv("SCFR_PIPE_NJ")) h->pipe_nj = std::atoll(pnj);
+        if (const char* pk = std::getenv("SCFR_PIPE_KINDS")) h->pipe_kinds = std::atoi(pk);
         const char* npr = std::getenv("SCFR_PAIR");  // opt-in: measured slower
         h->pair = npr && npr[0] == '1';
         if (const char* gnj = std::getenv("SCFR_GROUP_NJ")) h->group_nj = std::atoll(gnj);
