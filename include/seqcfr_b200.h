@@ -243,10 +243,7 @@ int scfr_launch_count(const scfr_handle* h, int64_t* out);
 /* Kernel-only device time of the last scfr_step in ms (CUDA events on the
  * handle's stream), and the summed duration of the payoff-SpMV kernels. */
 int scfr_last_step_ms(scfr_handle* h, double* total_ms);
-/* Tuning aid: CTA 0 of every forest / top kernel appends (clock64 << 8 | tag)
-   values to an armed device buffer of `cap` entries (0 disarms). */
-int scfr_trace_start(int cap);
-int scfr_trace_read(int64_t* out, int cap, int* n);
+
 /* Runs n iterations (real ones: state advances) without the graph, timing
  * every kernel launch with CUDA events on the handle's stream; aggregates
  * per kernel kind (td_avg, td, cur, obs_rm, obs, pred, spmv, tick): launch

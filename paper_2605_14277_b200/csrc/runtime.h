@@ -69,8 +69,8 @@ struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     bool pooled = false;
-    // kPad bytes past the end: the forest engine's bulk copies round ranges
-    // out to 16-byte granules, so the last granule may extend past n.
+    // kPad bytes past the end: bulk copies may round ranges out to 16-byte
+    // granules, so the last granule may extend past n.
     static constexpr size_t kPad = 16;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;  // owns device memory: never copied
@@ -272,72 +272,8 @@ struct TilePlayer {
 // Pass kinds of the level kernels.
 enum : int { LK_TD_AVG = 0, LK_TD, LK_CUR, LK_OBS, LK_PRED };
 
-// Forest mode of the level engine (forest.cu).
-constexpr int kFMax = 8;             // forest levels
-constexpr int kTopMax = 8;           // top levels
-constexpr int kTopMaxDPs = 1 << 16;  // top DPs (one cluster per player)
-enum : int { FP_OBS = 0, FP_PRED, FP_TDAVG, FP_TD, FP_CUR, FP_COUNT };
-// Stage arrays of one forest level: staged (bulk-copied) R, B, M (prediction),
-// IX / D / IP (payoff rows), SP / CH / PAR (structure), AVG; computed P
-// (payoff products), U (utility), V, X.
-enum : int { FA_R = 0, FA_B, FA_M, FA_IX, FA_D, FA_IP, FA_SP, FA_CH, FA_PAR, FA_AVG, FA_P, FA_U, FA_V, FA_X,
-             FA_N };
-__host__ __device__ inline int fa_size(int a, int v) {
-    return a == FA_IX || a == FA_IP || a == FA_SP || a == FA_PAR ? 4 : a == FA_CH ? 8 : v;
-}
-struct FLev {  // one level: exact affine shape (DevTree fields), payoff rows
-    int j_lo, s_lo, un, cn, c_lo, pc, p_lo;
-    int rows;      // the level's payoff rows hold non-zeros
-    int rc;        // > 0: every row holds rc non-zeros (no indptr staged)
-    int rs0, rk0;  // first row of the level and its first non-zero (row shape base)
-    // affine forest: the level's first DP / sequence / payoff nnz of root r
-    // are (aj0, as0, ak0) + r * (dj, ds, dk)
-    int aj0, as0, ak0, dj, ds, dk;
-};
-struct FHdr {  // one forest level of one stage: the item's bounds and the stage layout
-    int j0, j1, s0, s1, k0, k1;
-    int off[FA_N], alo[FA_N], cnt[FA_N];
-};
-template <class R>
-struct ForestTaskT {
-    int nl, nla;          // levels run by this pass / levels per table row
-    int leaf;             // the deepest level is forced moves into end nodes (kernels.cuh leaf_note)
-    int nitems, nblk;     // items (root ranges) and CTAs of this task
-    int nroots, aff, aR;  // aff: items of aR roots with affine positions (no table reads)
-    int stage_bytes, do_rm;
-    const int* items;     // [nitems + 1] root boundaries (root index)
-    const int* tab;       // [(nroots + 1)][nla][3]: first DP, sequence, payoff nnz per level
-    FLev lv[kFMax];
-    // the top (levels [0, ls)): last-arrival bottom-up, chain recompute top-down
-    int ls, Jtop, Stop, row0;
-    int tlo[kTopMax + 1];
-    FLev tlv[kTopMax];
-    const int* top_sdp;   // [Stop] top sequence -> its DP
-    const int* top_anc;   // [Stop][ls] ancestor sequences top-down (-1 pad; bit 30: single-action level)
-    const int* nch;       // [Jtop + 1] child DPs of each top DP; [Jtop]: DPs under the empty sequence
-    unsigned* cnt;        // [B][Jtop + 1] arrival counters (zero between launches)
-    unsigned* done;       // completion counter of the launch (tick)
-    long long* tick;      // advance when all `ntick` roots (tasks x solves) completed
-    int ntick;
-    int S, J;             // per-solve strides
-    const int* seq_ptr;
-    const int* dp_parent;
-    const int2* child;
-    const int* ip;        // OBS: the player's payoff rows and the opponent's strategy
-    const int* ix;
-    const R* d;
-    const R* xo;
-    int neg, xo_sx;
-    const R* u;           // PRED: prediction
-    R* uo;                // OBS: utility written
-    R* r;
-    R* b;
-    R* bo;                // OBS / PRED: behaviour written here (b, or bcur)
-    R* V;
-    R* x;                 // top-down output (x or xpost)
-    R* avg;
-    const R* src;         // top-down source: b, or bcur
-};
+constexpr int kTopMax = 8;  // top levels
+
 // The level engine's top (solver.cu prepare_top): top-down passes do not
 // launch levels [0, ls) of a player; its level-ls launch recomputes each
 // parent's x from the ancestor chain.  Lives in device memory.
@@ -350,23 +286,6 @@ struct TopPlayer {
     int ls = 0;
     DevBuf<int> anc;
     DevBuf<TopInfo> info;
-};
-
-struct ForestPlayer {
-    int ls = 0, nl = 0, nl_down = 0;
-    bool leaf = false;
-    int nroots = 0, nitems = 0, stage = 0, maxa = 1;
-    bool aff = false;
-    int aR = 0;
-    int Jtop = 0, Stop = 0;
-    FLev lv[kFMax];
-    FLev tlv[kTopMax];
-    FHdr all[kFMax];  // bounds of the whole forest (byte accounting)
-    std::vector<int> h_tab, h_items, h_sdp, h_anc, h_nch;
-    DevBuf<int> tab, items, top_sdp, top_anc, nch;
-    DevBuf<unsigned> cnt;
-    double bytes[FP_COUNT] = {0, 0, 0, 0, 0};  // algorithmic bytes per pass (OBS with RM)
-    double bytes_obs_norm = 0;                  // OBS without the RM write
 };
 
 }  // namespace scfr
@@ -446,10 +365,6 @@ struct scfr_handle {
     std::vector<std::pair<const void*, int>> tile_occ;  // resident CTAs per SM, per tile kernel
     // The level engine's top (prepare_top; SCFR_NO_TOP=1: off)
     scfr::TopPlayer top[2];
-    // Forest mode of the level engine (forest.cu; opt-in SCFR_FOREST=1)
-    bool forest = false;
-    scfr::ForestPlayer fp[2];
-    scfr::DevBuf<unsigned> fdone;  // forest: launch completion counter (in-kernel tick)
     void (*comm_destroy)(void*) = nullptr;  // set with comm (NCCL is dlopen'ed)
     ~scfr_handle() {
         // in-flight async copies / kernels may still use buffers that the
@@ -535,11 +450,7 @@ void tiled_iteration(LaunchBase& L);
 const double* orig_order(scfr_handle* h, int player, const double* buf, int solve);
 __global__ void k_tick(long long* tdev, unsigned long long* tl, int tl_idx);
 
-// Forest mode (forest.cu): plan at creation, per-iteration launches.
-bool prepare_forest(scfr_handle* h, const scfr_csr* U, const scfr_csr* UT);
-template <class R>
-void forest_iteration(LaunchBase& L);
-// solver.cu helpers shared with forest.cu
+// solver.cu helpers
 bool leaf_single(const scfr_handle* h, const Player& P);
 bool warp_level(const scfr_handle* h, const Player& P, int l);
 

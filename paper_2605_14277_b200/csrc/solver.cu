@@ -1617,11 +1617,6 @@ struct Launcher : LaunchBase {
             tiled_iteration(*this);
             return;
         }
-        if (h->forest) {
-            if (h->f32) forest_iteration<float>(*this);
-            else forest_iteration<double>(*this);
-            return;
-        }
         if (h->f32) iteration_t<float>();
         else iteration_t<double>();
     }
@@ -2161,15 +2156,9 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             h->leaf_x = l1 || l2;
             if (l2) build_iter_indices(h.get(), h->U, h->P[1]);   // U's columns: player 2's sequences
             if (l1) build_iter_indices(h.get(), h->UT, h->P[0]);  // Uᵀ's columns: player 1's
-            // opt-in forest mode (forest.cu), else the top levels completed in-kernel
-            const char* fe = std::getenv("SCFR_FOREST");
-            if (fe && fe[0] == '1' && h->u_empty_skip && prepare_forest(h.get(), U, UT)) {
-                h->fdone.alloc(1);
-                h->fdone.zero(h->stream);
-            } else {
-                prepare_top(h.get(), 0);
-                prepare_top(h.get(), 1);
-            }
+            // top-down passes recompute the top's x from ancestor chains
+            prepare_top(h.get(), 0);
+            prepare_top(h.get(), 1);
         }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
@@ -2288,8 +2277,7 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
     return guarded([&] {
         if (!h || !out || !count) fail(SCFR_EINVAL, "bad arguments");
         if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
-        if (is_persistent(h->engine) || h->forest)
-            fail(SCFR_EINVAL, "the timeline covers the level engine's launches");
+        if (is_persistent(h->engine)) fail(SCFR_EINVAL, "the timeline covers the level engine's launches");
         set_device(h);
         add_weights(h, n);
         preset_constant_rows(h);

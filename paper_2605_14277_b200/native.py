@@ -122,8 +122,6 @@ _SIGS = {
                            C.POINTER(C.c_int)], C.c_int),
     "scfr_timeline": ([C.c_void_p, C.c_int64, C.POINTER(KernelSpan), C.c_int, C.POINTER(C.c_int)],
                       C.c_int),
-    "scfr_trace_start": ([C.c_int], C.c_int),
-    "scfr_trace_read": ([i64p, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "scfr_transfer_bytes": ([i64p, i64p], C.c_int),
     "scfr_destroy": ([C.c_void_p], C.c_int),
 }

@@ -2,10 +2,10 @@
 (regrets, behaviour, accumulators, utilities, average and current strategies)
 across games, variants, modes, batches and dtypes; prints launches per
 iteration.  The switch is an environment variable read at creation:
-SCFR_NO_TOP (default: the in-kernel top vs launched top levels) or
-SCFR_FOREST (the opt-in forest mode).
+SCFR_NO_TOP (default), SCFR_NO_LEAF_FUSE, SCFR_NO_PIPE, SCFR_NO_GROUP,
+SCFR_PAIR, ... (SCFR_NO_* switches off the optimisation, other names on).
 
-    python scripts/forest_check.py [--quick] [--env SCFR_NO_TOP|SCFR_FOREST]
+    python scripts/mode_check.py [--quick] [--env SCFR_NO_TOP|SCFR_NO_LEAF_FUSE|...]
 """
 
 from __future__ import annotations
@@ -28,7 +28,7 @@ ENV = "SCFR_NO_TOP"
 
 
 def run(b, cfg, n, on, batch=None, dtype="f64"):
-    # on: the optimised path (SCFR_NO_TOP=0 / SCFR_FOREST=1)
+    # on: the optimised path (SCFR_NO_X=0 / SCFR_X=1)
     os.environ[ENV] = ("0" if on else "1") if ENV.startswith("SCFR_NO") else ("1" if on else "0")
     s = Solver(b, cfg, engine="levels", batch_params=batch, dtype=dtype)
     s.step(n)

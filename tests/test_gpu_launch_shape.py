@@ -21,6 +21,10 @@ def _launches(b, cfg):
 
 
 def test_liars_dice_merged_levels(gpu, monkeypatch):
+    # the level engine's launched levels (the top recompute and the fused
+    # leaf rows change the count; test_top_and_leaf_fusion covers those)
+    monkeypatch.setenv("SCFR_NO_TOP", "1")
+    monkeypatch.setenv("SCFR_NO_LEAF_FUSE", "1")
     b = GameBundle(flat_liars_dice(6))
     cfg = SolverConfig("dcfr", gamma=2.0)
     merged, r_merged = _launches(b, cfg)
@@ -41,6 +45,7 @@ def test_group_mode_same_launches_same_bits(gpu, monkeypatch):
     cfg = SolverConfig("pcfr+")
     monkeypatch.setenv("SCFR_GROUP_NJ", "0")
     monkeypatch.setenv("SCFR_NO_SMALL_WARP", "1")  # Goofspiel-4's levels are small
+    monkeypatch.setenv("SCFR_NO_LEAF_FUSE", "1")  # (needs group mode: would change the count)
     grouped, r_g = _launches(b, cfg)
     monkeypatch.setenv("SCFR_NO_GROUP", "1")
     plain, r_p = _launches(b, cfg)
@@ -67,3 +72,22 @@ def test_batched_level_engine_group_and_bcur(gpu, monkeypatch):
             np.testing.assert_array_equal(s.average(pl, k), one.average(pl))
         one.close()
     s.close()
+
+
+def test_top_and_leaf_fusion(gpu, monkeypatch):
+    """Top-down passes skip the top's launches (ancestor-chain x) and OBS
+    computes the forced leaf level inside the level above: fewer launches,
+    the same iterates bit for bit."""
+    from conftest import bundle
+    b = bundle("goof4")
+    cfg = SolverConfig("pcfr+")
+    monkeypatch.setenv("SCFR_GROUP_NJ", "0")
+    monkeypatch.setenv("SCFR_NO_SMALL_WARP", "1")
+    fused, r_f = _launches(b, cfg)
+    monkeypatch.setenv("SCFR_NO_TOP", "1")
+    monkeypatch.setenv("SCFR_NO_LEAF_FUSE", "1")
+    plain, r_p = _launches(b, cfg)
+    assert fused["td_avg"] < plain["td_avg"] and fused["cur"] < plain["cur"], (fused, plain)
+    assert fused["obs"] == plain["obs"] - 2, (fused, plain)  # one leaf launch per observe pass
+    assert fused["pred"] == plain["pred"]
+    np.testing.assert_array_equal(r_f, r_p)

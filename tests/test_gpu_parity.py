@@ -106,6 +106,31 @@ def test_group_mode_bit_exact(gpu, key, monkeypatch):
     assert e == rec["expl"] and list(br) == rec["br_avg"]
 
 
+# Level-engine modes forced onto every eligible level, each checked against
+# the reference digests: the cp.async-pipelined group kernels (all pass
+# kinds), parent pairs, and the plain launches without the top recompute /
+# fused leaf rows.
+MODES = {
+    "pipelined": {"SCFR_GROUP_NJ": "0", "SCFR_PIPE_NJ": "0", "SCFR_PIPE_KINDS": "31"},
+    "pairs": {"SCFR_GROUP_NJ": "0", "SCFR_PAIR": "1"},
+    "unfused": {"SCFR_NO_TOP": "1", "SCFR_NO_LEAF_FUSE": "1"},
+}
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
+@pytest.mark.parametrize("key", [k for k in CASES if k.split(".")[0] in ("goof4", "liars6", "random7", "leduc")])
+def test_level_engine_modes_bit_exact(gpu, key, mode, monkeypatch):
+    for name, value in MODES[mode].items():
+        monkeypatch.setenv(name, value)
+    rec = golden_meta()["lockstep"][key]
+    s = Solver(bundle(rec["game"]), _cfg(rec), device=gpu, engine="levels")
+    s.step(rec["iters"])
+    for k, v in _state(s).items():
+        assert digest(v) == rec["digests"][k], (key, mode, k)
+    e, br = s.exploitability("average")
+    assert e == rec["expl"] and list(br) == rec["br_avg"]
+
+
 def test_deterministic_and_graph_free_path_agree(gpu, monkeypatch):
     """The level engine with and without CUDA-graph replay."""
     rec = golden_meta()["lockstep"]["liars3.pcfr+.alt.60"]
