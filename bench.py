@@ -447,24 +447,26 @@ def run_ours(args):
     # --- per-kernel roofline, measured inside the timed configuration: a
     # recording copy of the iteration graph (scfr_timeline: every launch's
     # first-CTA start and last-CTA end, %globaltimer).  A launch's own
-    # duration gives its achieved GB/s; exclusive spans end_i - end_(i-1)
-    # partition the step, so the per-kind sums add up to the graph step.
+    # duration gives its achieved GB/s; exclusive spans (launches ordered by
+    # end time, each instant belonging to the launch that finishes next)
+    # partition the step, so the per-kind sums add up to the graph step.  With
+    # overlapped alt iterations the recorded graph is the two-stream body.
     peak, peak_kind = _peaks()
     tl_n = max(3, 3 * args.profile_iters)
-    timeline = s.timeline(tl_n)
+    timeline = s.timeline(tl_n)  # (overlapped body when the handle overlaps alt iterations)
     kinds = {}
     for e in timeline:
         k = kinds.setdefault(e["kind"], {"launches": 0, "excl_us": 0.0, "own_us": 0.0, "bytes": 0.0})
         k["launches"] += 1
         k["excl_us"] += e["excl_us"]
-        k["own_us"] += e["end_us"] - e["start_us"]
+        k["own_us"] += e["own_us"]
         k["bytes"] += e["bytes"]
     top = max(timeline, key=lambda e: e["end_us"] - e["start_us"])
     dname = top["kind"]
     dur_us = top["end_us"] - top["start_us"]
     achieved = top["bytes"] / (dur_us * 1e3)
     step_bytes = sum(e["bytes"] for e in timeline)
-    tl_us = timeline[-1]["end_us"]
+    tl_us = max(e["end_us"] for e in timeline)
     prof = s.profile(args.profile_iters)  # eager launches with CUDA events, for comparison
     d = {"bytes": top["bytes"], "launches": 1}
     traffic = None
@@ -525,7 +527,7 @@ def run_ours(args):
                                      "mb": v["bytes"] / 1e6,
                                      "gbs": v["bytes"] / (v["own_us"] * 1e3) if v["own_us"] else None}
                                  for k, v in kinds.items()},
-                     "launches": [{"kind": e["kind"], "start_us": round(e["start_us"], 2),
+                     "launches": [{"kind": e["kind"], "stream": e["stream"], "start_us": round(e["start_us"], 2),
                                    "end_us": round(e["end_us"], 2), "mb": round(e["bytes"] / 1e6, 3)}
                                   for e in timeline],
                      "eager_events": {k: {"launches": v["launches"] // args.profile_iters,

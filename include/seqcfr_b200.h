@@ -257,13 +257,17 @@ typedef struct scfr_kernel_stat {
 int scfr_profile_step(scfr_handle* h, int64_t n_iter, scfr_kernel_stat* out, int cap, int* count);
 /* In-graph timeline of the level engine: runs n_iter iterations (they count,
  * as with scfr_step) through a copy of the iteration graph whose kernels
- * record their first-CTA start and last-CTA end (%globaltimer).  One span per
- * launch of the iteration, times in microseconds from the iteration's first
- * start, averaged over the iterations; bytes = the launch's algorithmic
- * bytes.  Exclusive span i = end_i - end_(i-1) partitions the step. */
+ * record their first-CTA start and last-CTA end (%globaltimer).  With
+ * overlapped alt iterations the recorded graph is the two-stream body
+ * (n_iter >= 2: prologue, n_iter - 1 recorded bodies, epilogue).  One span
+ * per launch, times in microseconds from the iteration's first start,
+ * averaged; stream 0 / 1; bytes = the launch's algorithmic bytes.  Spans
+ * ordered by end time partition the step: each instant belongs to the
+ * launch that finishes next. */
 typedef struct scfr_kernel_span {
     char name[16];
     int32_t kind;
+    int32_t stream;
     double bytes;
     double start_us, end_us;
 } scfr_kernel_span;

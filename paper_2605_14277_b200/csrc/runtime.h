@@ -222,6 +222,9 @@ struct KParams {
     // launch, slots [2 * tl_idx, 2 * tl_idx + 1]; null when not recording
     unsigned long long* tl;
     int tl_idx;
+    // schedule index = *tdev + tofs: the overlapped alt iteration runs the
+    // next iteration's PRED / TD + average before the tick (tofs = 1)
+    int tofs;
 };
 
 // Timeline records of a launch (scfr_timeline): every CTA's thread 0 after
@@ -323,6 +326,15 @@ struct scfr_handle {
     std::vector<double> avg_weight;  // [B]
     cudaGraphExec_t exec = nullptr;
     int64_t nodes_per_iter = 0;
+    // Overlapped alt iterations (solver.cu Launcher::body_t; SCFR_NO_OVERLAP=1:
+    // off): prologue (next of both players), body (observe of iteration t with
+    // player 1's next of t+1 on a second stream beside player 2's observe and
+    // next), epilogue (observe of the last iteration)
+    bool overlap = false;
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr;
+    cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
+    int64_t nodes_pro = 0, nodes_body = 0, nodes_epi = 0;
     int64_t launches = 0;
     bool use_graph = true;
     bool pdl = true;   // programmatic dependent launch between level kernels
@@ -374,6 +386,12 @@ struct scfr_handle {
         if (comm && comm_destroy) comm_destroy(comm);
         comm = nullptr;
         if (exec) cudaGraphExecDestroy(exec);
+        for (cudaGraphExec_t e : {exec_pro, exec_body, exec_epi})
+            if (e) cudaGraphExecDestroy(e);
+        if (stream2) cudaStreamSynchronize(stream2);
+        for (cudaEvent_t e : {ev_fork, ev_a, ev_b})
+            if (e) cudaEventDestroy(e);
+        if (stream2) cudaStreamDestroy(stream2);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -387,13 +405,20 @@ namespace scfr {
 struct LaunchBase {
     scfr_handle* h;
     int64_t count = 0;
+    cudaStream_t st = nullptr;  // launch stream (null: the handle's)
+    int tofs = 0;               // KParams::tofs of the launches
     unsigned long long* tl = nullptr;  // scfr_timeline buffer while capturing its graph
-    std::vector<std::pair<int, double>>* tl_kinds = nullptr;  // (kind, bytes) per launch
+    struct TlRec {
+        int kind;
+        double bytes;
+        int stream;  // 0: the handle's stream, 1: stream2 (overlapped body)
+    };
+    std::vector<TlRec>* tl_kinds = nullptr;  // per launch
     std::vector<KernelRecord>* prof = nullptr;  // per-launch events when profiling
 
     template <class F>
     void launch(int kind, double bytes, F&& f) {
-        if (tl_kinds) tl_kinds->emplace_back(kind, bytes * h->B);
+        if (tl_kinds) tl_kinds->push_back(TlRec{kind, bytes * h->B, st && st != h->stream ? 1 : 0});
         if (prof) {
             KernelRecord r;
             r.kind = kind;
@@ -419,7 +444,7 @@ struct LaunchBase {
         cfg.gridDim = grid;
         cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = smem;
-        cfg.stream = h->stream;
+        cfg.stream = st ? st : h->stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;

@@ -143,9 +143,9 @@ __device__ __forceinline__ void level_body(const TaskT<R>& t, int blk, const KPa
     const int lane = threadIdx.x & 31;
     // schedules are fp64 (host libm pow); the fp32 mode rounds them once
     R w = R(0), pf = R(1), nf = R(1);
-    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs];
     if (KIND == LK_OBS && kp.post == POST_DCFR) {
-        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs;
         pf = (R)kp.pfsched[k];
         nf = (R)kp.nfsched[k];
     }
@@ -206,9 +206,9 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
     const int n = N > 0 ? N : t.T.un, G = 32 / n;
     const int lane = threadIdx.x & 31, g = lane / n, a = lane - g * n, gb = g * n;
     R w = R(0), pf = R(1), nf = R(1);
-    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs];
     if (KIND == LK_OBS && kp.post == POST_DCFR) {
-        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs;
         pf = (R)kp.pfsched[k];
         nf = (R)kp.nfsched[k];
     }
@@ -337,9 +337,9 @@ __device__ __forceinline__ void level_body_gp(const TaskT<R>& t, int blk, const 
     constexpr int n = N, G = 32 / N;
     const int g = lane / n, a = lane - g * n, gb = g * n;
     R w = R(0), pf = R(1), nf = R(1);
-    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev];
+    if (KIND == LK_TD_AVG) w = (R)kp.wsched[(size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs];
     if (KIND == LK_OBS && kp.post == POST_DCFR) {
-        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev;
+        const size_t k = (size_t)blockIdx.y * kp.cap + *kp.tdev + kp.tofs;
         pf = (R)kp.pfsched[k];
         nf = (R)kp.nfsched[k];
     }
@@ -1248,7 +1248,7 @@ struct LevelBytes {  // v: bytes per value (8 fp64, 4 in the fp32 mode)
 KParams LaunchBase::kparams(bool do_rm) const {
     return KParams{h->wsched.p, h->pfsched.p, h->nfsched.p, h->cap, h->tdev.p,
                    post_of(h->variant), do_rm ? 1 : 0, h->variant == SCFR_PCFR_PLUS ? 1 : 0,
-                   h->nonfinite.p, tl, (int)count};
+                   h->nonfinite.p, tl, (int)count, tofs};
 }
 
 struct Launcher : LaunchBase {
@@ -1623,16 +1623,26 @@ struct Launcher : LaunchBase {
 
     template <class R>
     void iteration_t() {
+        next_part<R>(true, true);
+        observe_part<R>(true, true);
+        tick();
+    }
+
+    void tick() { launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p, tl, (int)count); }); }
+
+    // next_strategy of the chosen players (independent): PRED deep -> shallow,
+    // then TD + average shallow -> deep, two players sharing launches.
+    template <class R>
+    void next_part(bool p1, bool p2) {
         Player& A = h->P[0];
         Player& Bp = h->P[1];
+        Player* pa = p1 ? &A : nullptr;
+        Player* pb = p2 ? &Bp : nullptr;
         R *Au = vals<R>(A.u), *Bu = vals<R>(Bp.u), *Ax = vals<R>(A.x), *Bx = vals<R>(Bp.x);
-        R* Axp = vals<R>(A.xpost);
         const bool pr = predictive(h->variant);
         const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
         const int fa = first_level(A), fb = first_level(Bp);  // the top's levels are not launched
         auto skip = [](int l, int f) { return l < f ? -1 : l; };
-        // next_strategy of both players (independent): PRED deep -> shallow,
-        // then TD + average shallow -> deep, the two players sharing launches.
         if (pr) {
             // a deepest level of forced moves into end nodes needs no PRED
             // launch: its parent level reads the prediction itself (leaf_note)
@@ -1643,13 +1653,13 @@ struct Launcher : LaunchBase {
             };
             for (int k = 0; k < L; ++k) {
                 const int la = LA - 1 - k, lb = LB - 1 - k;
-                level<R>(LK_PRED, KK_PRED, &A, sa && la == LA - 1 ? -1 : la, &Bp, sb && lb == LB - 1 ? -1 : lb,
+                level<R>(LK_PRED, KK_PRED, pa, sa && la == LA - 1 ? -1 : la, pb, sb && lb == LB - 1 ? -1 : lb,
                          Au, Bu, Ax, Bx, false, sa && la == LA - 2 ? vc(A, Au) : nullptr,
                          sb && lb == LB - 2 ? vc(Bp, Bu) : nullptr);
             }
         }
-        for (Player* P : {&A, &Bp})
-            if (P->J == 0)
+        for (Player* P : {pa, pb})
+            if (P && P->J == 0)
                 launch(KK_TD_AVG, 2.0 * sizeof(R), [&] {
                     run1(k_avg0<R>, dim3(h->B), P->S, (const R*)vals<R>(P->x), vals<R>(P->avg),
                          (const double*)h->wsched.p, h->cap, (const long long*)h->tdev.p);
@@ -1657,8 +1667,23 @@ struct Launcher : LaunchBase {
         // forced leaf levels: their x / avg are the parents' (k_expand_leaf)
         const bool xa = h->leaf_x && leaf_single(A), xb = h->leaf_x && leaf_single(Bp);
         for (int k = 0; k < L; ++k)
-            level<R>(LK_TD_AVG, KK_TD_AVG, &A, xa && k == LA - 1 ? -1 : skip(k, fa), &Bp,
+            level<R>(LK_TD_AVG, KK_TD_AVG, pa, xa && k == LA - 1 ? -1 : skip(k, fa), pb,
                      xb && k == LB - 1 ? -1 : skip(k, fb), nullptr, nullptr, Ax, Bx, false);
+    }
+
+    // observe (and, alt mode, player 1's current strategy): part1 = OBS of
+    // player 1 + CUR (alt) or OBS of both (sim); part2 = OBS of player 2 (alt)
+    template <class R>
+    void observe_part(bool part1, bool part2) {
+        Player& A = h->P[0];
+        Player& Bp = h->P[1];
+        R *Au = vals<R>(A.u), *Bu = vals<R>(Bp.u), *Ax = vals<R>(A.x), *Bx = vals<R>(Bp.x);
+        R* Axp = vals<R>(A.xpost);
+        const bool pr = predictive(h->variant);
+        const int LA = A.levels(), LB = Bp.levels(), L = std::max(LA, LB);
+        const int fa = first_level(A);
+        auto skip = [](int l, int f) { return l < f ? -1 : l; };
+        const bool xa = h->leaf_x && leaf_single(A);
         const bool fused = fuse_spmv();
         // OBS on a forced leaf level: its V equals u (leaf_note), so the
         // parent level reads u and the leaf launch skips writing V
@@ -1667,8 +1692,9 @@ struct Launcher : LaunchBase {
             const DevTree& sh = P.lvl_shape[P.levels() - 1];
             return u + (sh.s_lo - sh.j_lo);
         };
-        if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);  // u1 = U x2
         if (h->mode == SCFR_MODE_SIM) {
+            if (!part1) return;
+            if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);   // u1 = U x2
             if (!fused) spmv<R>(h->UT, Ax, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1
             lf_[0] = lf_[1] = leaf_fusable(A) && leaf_fusable(Bp) && LA == LB;  // (one launch: both or none)
             for (int k = 0; k < L; ++k)
@@ -1677,7 +1703,10 @@ struct Launcher : LaunchBase {
                          oa && k == 1 ? leaf_u(A, Au) : nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr,
                          oa && k == 0, ob && k == 0);
             lf_[0] = lf_[1] = false;
-        } else {
+            return;
+        }
+        if (part1) {
+            if (!fused) spmv<R>(h->U, Bx, Bp.S, Au, A.S, false);  // u1 = U x2
             const bool bc = pr && h->bcur_on;
             if (bc) bcur_ = vals<R>(A.bcur);
             lf_[0] = leaf_fusable(A);
@@ -1693,6 +1722,8 @@ struct Launcher : LaunchBase {
                 level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : skip(k, fa),
                          nullptr, -1, nullptr, nullptr, Axp, nullptr, false);
             bcur_ = nullptr;
+        }
+        if (part2) {
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             lf_[1] = leaf_fusable(Bp);
             for (int k = 0; k < LB; ++k)
@@ -1701,7 +1732,48 @@ struct Launcher : LaunchBase {
                          ob && k == 0);
             lf_[1] = false;
         }
-        launch(KK_TICK, 0.0, [&] { run1(k_tick, dim3(1), h->tdev.p, tl, (int)count); });
+    }
+
+    // Overlapped alt iteration body: iteration t's observe with iteration
+    // t+1's next, on two streams (captured as a fork / join):
+    //   stream A: OBS1(t), CUR1(t) -> ev_a; NEXT1(t+1); wait ev_b; tick
+    //   stream B: wait ev_a; OBS2(t); NEXT2(t+1) -> ev_b
+    // NEXT1(t+1) reads only what OBS1(t) wrote and writes player 1's x / avg /
+    // b / V, which OBS2(t) does not touch (it reads x1' = xpost); NEXT2(t+1)
+    // follows OBS2(t) in stream order.  Schedules of t+1 via tofs = 1.
+    template <class R>
+    void body_t() {
+        cudaStream_t A = h->stream, B = h->stream2;
+        CUDA_OK(cudaEventRecord(h->ev_fork, A));
+        CUDA_OK(cudaStreamWaitEvent(B, h->ev_fork, 0));
+        st = A;
+        observe_part<R>(true, false);
+        CUDA_OK(cudaEventRecord(h->ev_a, A));
+        CUDA_OK(cudaStreamWaitEvent(B, h->ev_a, 0));
+        st = B;
+        observe_part<R>(false, true);
+        tofs = 1;
+        next_part<R>(false, true);
+        CUDA_OK(cudaEventRecord(h->ev_b, B));
+        st = A;
+        next_part<R>(true, false);
+        tofs = 0;
+        CUDA_OK(cudaStreamWaitEvent(A, h->ev_b, 0));
+        tick();
+        st = nullptr;
+    }
+    void body() {
+        if (h->f32) body_t<float>();
+        else body_t<double>();
+    }
+    void prologue() {  // next of both players (iteration t)
+        if (h->f32) next_part<float>(true, true);
+        else next_part<double>(true, true);
+    }
+    void epilogue() {  // observe of the last iteration, then the tick
+        if (h->f32) observe_part<float>(true, true);
+        else observe_part<double>(true, true);
+        tick();
     }
 };
 
@@ -1741,21 +1813,35 @@ static void ensure_schedule(scfr_handle* h, int64_t upto) {
     CUDA_OK(copy_sync(h->nfsched.p, nf.data(), nf.size() * sizeof(double), cudaMemcpyHostToDevice));
     h->w_host.swap(w);
     h->cap = (int)cap;
-    if (h->exec) {
-        cudaGraphExecDestroy(h->exec);
-        h->exec = nullptr;
-    }
+    for (cudaGraphExec_t* e : {&h->exec, &h->exec_pro, &h->exec_body, &h->exec_epi})
+        if (*e) {
+            cudaGraphExecDestroy(*e);
+            *e = nullptr;
+        }
+}
+
+template <class F>
+static cudaGraphExec_t capture(scfr_handle* h, int64_t& nodes, F&& body) {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    Launcher L(h);
+    CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    body(L);
+    CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
+    CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    nodes = L.count;
+    return exec;
 }
 
 static void build_graph(scfr_handle* h) {
-    cudaGraph_t graph;
-    Launcher L(h);
-    CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    L.iteration();
-    CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
-    CUDA_OK(cudaGraphInstantiate(&h->exec, graph, 0));
-    cudaGraphDestroy(graph);
-    h->nodes_per_iter = L.count;
+    h->exec = capture(h, h->nodes_per_iter, [](Launcher& L) { L.iteration(); });
+}
+
+static void build_overlap_graphs(scfr_handle* h) {
+    h->exec_pro = capture(h, h->nodes_pro, [](Launcher& L) { L.prologue(); });
+    h->exec_body = capture(h, h->nodes_body, [](Launcher& L) { L.body(); });
+    h->exec_epi = capture(h, h->nodes_epi, [](Launcher& L) { L.epilogue(); });
 }
 
 static void set_device(const scfr_handle* h) { CUDA_OK(cudaSetDevice(h->device)); }
@@ -2159,6 +2245,16 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // top-down passes recompute the top's x from ancestor chains
             prepare_top(h.get(), 0);
             prepare_top(h.get(), 1);
+            // alt mode: player 1's next overlaps player 2's observe
+            const char* nov = std::getenv("SCFR_NO_OVERLAP");
+            if (h->mode == SCFR_MODE_ALT && h->fuse && !(nov && nov[0] == '1') && h->P[0].J > 0 &&
+                h->P[1].J > 0) {
+                CUDA_OK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+                CUDA_OK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+                CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+                CUDA_OK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+                h->overlap = true;
+            }
         }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
@@ -2208,6 +2304,14 @@ int scfr_step(scfr_handle* h, int64_t n) {
         CUDA_OK(cudaEventRecord(h->ev0, h->stream));
         if (is_persistent(h->engine)) {
             h->launches += launch_persistent(h, n);
+        } else if (h->use_graph && h->overlap) {
+            // prologue, n - 1 overlapped bodies, epilogue: the state is back at
+            // an iteration boundary when the call returns
+            if (!h->exec_body) build_overlap_graphs(h);
+            CUDA_OK(cudaGraphLaunch(h->exec_pro, h->stream));
+            for (int64_t i = 1; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->exec_body, h->stream));
+            CUDA_OK(cudaGraphLaunch(h->exec_epi, h->stream));
+            h->launches += h->nodes_pro + (n - 1) * h->nodes_body + h->nodes_epi;
         } else if (h->use_graph) {
             if (!h->exec) build_graph(h);
             for (int64_t i = 0; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->exec, h->stream));
@@ -2276,13 +2380,15 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
 int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int* count) {
     return guarded([&] {
         if (!h || !out || !count) fail(SCFR_EINVAL, "bad arguments");
-        if (n < 1) fail(SCFR_EINVAL, "n_iter must be >= 1");
+        if (n < 1 || (h->overlap && n < 2)) fail(SCFR_EINVAL, "n_iter must be >= 1 (>= 2 when overlapped)");
         if (is_persistent(h->engine)) fail(SCFR_EINVAL, "the timeline covers the level engine's launches");
         set_device(h);
         add_weights(h, n);
         preset_constant_rows(h);
-        // capture a recording copy of the iteration graph
-        std::vector<std::pair<int, double>> kinds;
+        // a recording copy of the iteration graph (the overlapped body when
+        // the handle runs overlapped iterations: prologue, n - 1 recorded
+        // bodies, epilogue)
+        std::vector<LaunchBase::TlRec> kinds;
         DevBuf<unsigned long long> buf;
         {
             AllocStream alloc_on(h->stream);
@@ -2294,7 +2400,8 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        L.iteration();
+        if (h->overlap) L.body();
+        else L.iteration();
         CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
         CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -2303,30 +2410,39 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
             cudaGraphExecDestroy(exec);
             fail(SCFR_EINVAL, "%d launches per iteration exceed the output capacity", m);
         }
+        if (h->overlap) {
+            if (!h->exec_body) build_overlap_graphs(h);
+            CUDA_OK(cudaGraphLaunch(h->exec_pro, h->stream));
+        }
+        const int64_t rec = h->overlap ? n - 1 : n;
         std::vector<unsigned long long> host(2 * m);
         std::vector<double> st(m, 0.0), en(m, 0.0);
-        for (int64_t i = 0; i < n; ++i) {
+        for (int64_t i = 0; i < rec; ++i) {
             CUDA_OK(cudaMemsetAsync(buf.p, 0, 2 * m * sizeof(unsigned long long), h->stream));
             CUDA_OK(cudaGraphLaunch(exec, h->stream));
             CUDA_OK(cudaMemcpyAsync(host.data(), buf.p, 2 * m * sizeof(unsigned long long),
                                     cudaMemcpyDeviceToHost, h->stream));
             CUDA_OK(cudaStreamSynchronize(h->stream));
-            const unsigned long long t0 = ~host[0];
+            unsigned long long t0 = ~0ull;
+            for (int k = 0; k < m; ++k) t0 = std::min(t0, ~host[2 * k]);
             for (int k = 0; k < m; ++k) {
                 st[k] += (double)(long long)(~host[2 * k] - t0) / 1e3;
                 en[k] += (double)(long long)(host[2 * k + 1] - t0) / 1e3;
             }
         }
+        if (h->overlap) CUDA_OK(cudaGraphLaunch(h->exec_epi, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
         cudaGraphExecDestroy(exec);
         h->timed = false;
         h->t += n;
-        h->launches += n * m;
+        h->launches += h->overlap ? h->nodes_pro + rec * m + h->nodes_epi : n * m;
         for (int k = 0; k < m; ++k) {
-            std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[kinds[k].first]);
-            out[k].kind = kinds[k].first;
-            out[k].bytes = kinds[k].second;
-            out[k].start_us = st[k] / (double)n;
-            out[k].end_us = en[k] / (double)n;
+            std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[kinds[k].kind]);
+            out[k].kind = kinds[k].kind;
+            out[k].stream = kinds[k].stream;
+            out[k].bytes = kinds[k].bytes;
+            out[k].start_us = st[k] / (double)rec;
+            out[k].end_us = en[k] / (double)rec;
         }
         *count = m;
     });

@@ -72,7 +72,7 @@ class KernelStat(C.Structure):
 
 
 class KernelSpan(C.Structure):
-    _fields_ = [("name", C.c_char * 16), ("kind", C.c_int32), ("bytes", C.c_double),
+    _fields_ = [("name", C.c_char * 16), ("kind", C.c_int32), ("stream", C.c_int32), ("bytes", C.c_double),
                 ("start_us", C.c_double), ("end_us", C.c_double)]
 
 

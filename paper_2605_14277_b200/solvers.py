@@ -216,18 +216,22 @@ class Solver:
 
     def timeline(self, n: int = 3) -> list[dict]:
         """Run n real iterations through a recording copy of the iteration
-        graph; one entry per launch: kind, algorithmic bytes, mean start / end
-        (us from the iteration's first start, %globaltimer) and the exclusive
-        span end_i - end_(i-1), which partitions the in-graph step."""
+        graph (the overlapped two-stream body when the handle overlaps alt
+        iterations); one entry per launch: kind, stream, algorithmic bytes,
+        mean start / end (us from the iteration's first start, %globaltimer),
+        own duration, and the exclusive span: launches ordered by end time
+        partition the step, each instant belonging to the launch that
+        finishes next."""
         spans = (N.KernelSpan * 4096)()
         cnt = C.c_int()
         N.check(N.lib().scfr_timeline(self._h, int(n), spans, 4096, C.byref(cnt)))
-        out, prev = [], 0.0
-        for k in range(cnt.value):
-            sp = spans[k]
-            out.append({"kind": sp.name.decode(), "bytes": float(sp.bytes), "start_us": float(sp.start_us),
-                        "end_us": float(sp.end_us), "excl_us": float(sp.end_us) - prev})
-            prev = float(sp.end_us)
+        out = [{"kind": spans[k].name.decode(), "stream": int(spans[k].stream), "bytes": float(spans[k].bytes),
+                "start_us": float(spans[k].start_us), "end_us": float(spans[k].end_us)} for k in range(cnt.value)]
+        prev = 0.0
+        for e in sorted(out, key=lambda e: e["end_us"]):
+            e["own_us"] = e["end_us"] - e["start_us"]
+            e["excl_us"] = max(0.0, e["end_us"] - prev)
+            prev = max(prev, e["end_us"])
         return out
 
     # -- reads -----------------------------------------------------------------

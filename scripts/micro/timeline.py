@@ -14,8 +14,9 @@ s.synchronize()
 tl = s.timeline(n)
 s.step(20)
 s.synchronize()
-print(f"graph step {s.last_step_ms() / 20 * 1e3:.1f} us; timeline end {tl[-1]['end_us']:.1f} us; launches {len(tl)}")
+end = max(e["end_us"] for e in tl)
+print(f"graph step {s.last_step_ms() / 20 * 1e3:.1f} us; timeline end {end:.1f} us; launches {len(tl)}")
 for k, e in enumerate(tl):
-    gbs = e["bytes"] / (e["excl_us"] * 1e3) if e["excl_us"] > 0 else 0
-    print(f"{k:3d} {e['kind']:>8} start {e['start_us']:7.1f} end {e['end_us']:7.1f} excl {e['excl_us']:6.1f} us "
-          f"{e['bytes'] / 1e6:7.2f} MB {gbs:7.1f} GB/s")
+    gbs = e["bytes"] / (e["own_us"] * 1e3) if e["own_us"] > 0 else 0
+    print(f"{k:3d} s{e['stream']} {e['kind']:>8} start {e['start_us']:7.1f} end {e['end_us']:7.1f} "
+          f"own {e['own_us']:6.1f} excl {e['excl_us']:6.1f} us {e['bytes'] / 1e6:7.2f} MB {gbs:7.1f} GB/s")

@@ -108,12 +108,13 @@ def test_group_mode_bit_exact(gpu, key, monkeypatch):
 
 # Level-engine modes forced onto every eligible level, each checked against
 # the reference digests: the cp.async-pipelined group kernels (all pass
-# kinds), parent pairs, and the plain launches without the top recompute /
-# fused leaf rows.
+# kinds), parent pairs, the plain launches without the top recompute /
+# fused leaf rows, and alt iterations without the two-stream overlap.
 MODES = {
     "pipelined": {"SCFR_GROUP_NJ": "0", "SCFR_PIPE_NJ": "0", "SCFR_PIPE_KINDS": "31"},
     "pairs": {"SCFR_GROUP_NJ": "0", "SCFR_PAIR": "1"},
     "unfused": {"SCFR_NO_TOP": "1", "SCFR_NO_LEAF_FUSE": "1"},
+    "sequential": {"SCFR_NO_OVERLAP": "1"},
 }
 
 
