@@ -144,6 +144,24 @@ typedef struct scfr_flat_game {
     scfr_game game;
     int64_t num_infosets;
 } scfr_flat_game;
+/* Native reader of the reference's JSON-lines game file (pkg/games.py:554-648):
+ * parses and validates (the checks and messages of games.load_game +
+ * games.validate_game, first violation reported) straight into the compiler's
+ * flat arrays, with the names: labels[label_off[i] .. label_off[i+1]) is node
+ * i's label_from_parent, infoset_names[infoset_off[k] ..) infoset id k's label.
+ * On SCFR_EGAME: err_line >= 1 for a file-level error (GameParseError),
+ * err_node >= 0 for a tree violation (GameValidationError). */
+typedef struct scfr_parsed_game {
+    scfr_flat_game flat;
+    const char* name;
+    const char* labels;
+    const int64_t* label_off;      /* [num_nodes + 1] */
+    const char* infoset_names;
+    const int64_t* infoset_off;    /* [num_infosets + 1] */
+} scfr_parsed_game;
+int scfr_parse_game_jsonl(const char* text, int64_t len, scfr_parsed_game** out, int64_t* err_line,
+                          int64_t* err_node);
+void scfr_parsed_game_free(scfr_parsed_game* g);
 int scfr_generate_liars_dice(int faces, scfr_flat_game** out);
 int scfr_generate_goofspiel(int cards, scfr_flat_game** out);
 void scfr_flat_game_free(scfr_flat_game* g);

@@ -220,6 +220,48 @@ def flat_goofspiel(cards: int = 5) -> FlatGame:
     return _from_native(N.lib().scfr_generate_goofspiel, cards, f"goofspiel_{cards}")
 
 
+def load_game_flat(text: str) -> FlatGame:
+    """A JSON-lines game file (the reference format, pkg/games.py:554-648)
+    read, validated and flattened natively (csrc/jsonl.cpp): the same checks
+    and errors as ``games.load_game`` (GameParseError with the line,
+    GameValidationError with the node), without building Python node
+    objects.  The result feeds ``GameBundle`` directly."""
+    from .games import GameParseError, GameValidationError
+    raw = text.encode("utf-8")
+    out = C.POINTER(N.ParsedGameC)()
+    line, node = C.c_int64(-1), C.c_int64(-1)
+    L = N.lib()
+    status = L.scfr_parse_game_jsonl(raw, len(raw), C.byref(out), C.byref(line), C.byref(node))
+    if status == N.EGAME:
+        msg = L.scfr_last_error().decode(errors="replace")
+        if line.value >= 1:
+            raise GameParseError(msg, int(line.value))
+        raise GameValidationError(msg, int(node.value) if node.value >= 0 else None)
+    N.check(status)
+    try:
+        pg = out.contents
+        g = pg.flat.game
+        n = int(g.num_nodes)
+        m = int(np.ctypeslib.as_array(g.child_ptr, shape=(n + 1,))[-1])
+        flat = FlatGame(pg.name.decode("utf-8"), N.view_i8(g.kind, n), N.view_i64(g.parent, n),
+                        N.view_i64(g.child_ptr, n + 1), N.view_i64(g.child_idx, m),
+                        N.view_i8(g.player, n), N.view_i64(g.infoset, n),
+                        N.view_f64(g.prob, n), N.view_f64(g.payoff, n))
+        k = int(pg.flat.num_infosets)
+
+        def strings(base, off, count):
+            offs = N.view_i64(off, count + 1)
+            blob = C.string_at(base, int(offs[-1])) if count and offs[-1] else b""
+            return [blob[offs[i]:offs[i + 1]].decode("utf-8") for i in range(count)]
+
+        flat.infoset_labels = strings(pg.infoset_names, pg.infoset_off, k)
+        labels = strings(pg.labels, pg.label_off, n)
+        flat.action_labels = [None] + labels[1:]
+    finally:
+        L.scfr_parsed_game_free(out)
+    return flat
+
+
 class GameBundle:
     """Iteration-invariant structure of one game (pkg/solvers.py:309-336).
 

@@ -66,6 +66,11 @@ class FlatGameC(C.Structure):
     _fields_ = [("game", Game), ("num_infosets", C.c_int64)]
 
 
+class ParsedGameC(C.Structure):
+    _fields_ = [("flat", FlatGameC), ("name", C.c_char_p), ("labels", C.c_void_p), ("label_off", i64p),
+                ("infoset_names", C.c_void_p), ("infoset_off", i64p)]
+
+
 class KernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 16), ("launches", C.c_int64), ("ms", C.c_double),
                 ("bytes", C.c_double)]
@@ -95,6 +100,8 @@ _SIGS = {
     "scfr_generate_liars_dice": ([C.c_int, C.POINTER(C.POINTER(FlatGameC))], C.c_int),
     "scfr_generate_goofspiel": ([C.c_int, C.POINTER(C.POINTER(FlatGameC))], C.c_int),
     "scfr_flat_game_free": ([C.POINTER(FlatGameC)], None),
+    "scfr_parse_game_jsonl": ([C.c_char_p, C.c_int64, C.POINTER(C.POINTER(ParsedGameC)), i64p, i64p], C.c_int),
+    "scfr_parsed_game_free": ([C.POINTER(ParsedGameC)], None),
     "scfr_create": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.POINTER(Csr),
                      C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "scfr_nccl_unique_id": ([C.c_char_p], C.c_int),

@@ -80,3 +80,17 @@ def test_solve_matches_reference_records(gpu, tmp_path, capsys):
     strat = [json.loads(s) for s in (tmp_path / "solve.strategy.jsonl").read_text().splitlines()]
     assert len(strat) == 24
     assert "exploitability=7.269106e-03" in capsys.readouterr().out
+
+
+def test_info_from_a_game_file_matches_builtin(tmp_path, capsys):
+    """A JSON-lines file goes through the native reader (csrc/jsonl.cpp)."""
+    from paper_2605_14277_b200.games import save_game
+    path = tmp_path / "kuhn.jsonl"
+    path.write_text(save_game(kuhn_poker()))
+    assert cli.main(["info", "--game", "kuhn"]) == 0
+    want = capsys.readouterr().out
+    assert cli.main(["info", "--game", str(path)]) == 0
+    assert capsys.readouterr().out == want
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text(path.read_text().replace('"prob": 0.5', '"prob": 0.25', 1))
+    assert cli.main(["info", "--game", str(bad)]) == cli.EXIT_DATA
