@@ -214,6 +214,14 @@ int scfr_create_sharded(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
 /* Runs n full iterations (_step semantics incl. t++ for both players) on the
  * handle's stream; asynchronous. */
 int scfr_step(scfr_handle* h, int64_t n_iter);
+/* Caller-computed per-iteration scalars for the next n iterations (t+1 ..
+ * t+n) of one solve (solve = -1: every solve): the averaging weight w_t
+ * (reference float(t)**gamma, pkg/solvers.py:172) and the DCFR factors
+ * pf_t / nf_t for positive / negative regrets (pkg/solvers.py:82-94).  A NULL
+ * array keeps the library's values (libm pow, the reference's semantics).
+ * Entries must be finite (SCFR_EINVAL). */
+int scfr_set_schedule(scfr_handle* h, int solve, const double* w_t, const double* pf_t, const double* nf_t,
+                      int64_t n);
 /* The engine the handle runs (SCFR_ENGINE_*; AUTO resolved at creation). */
 int scfr_engine(const scfr_handle* h, int* engine);
 int scfr_synchronize(scfr_handle* h);

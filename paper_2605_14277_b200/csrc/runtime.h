@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges are no-ops unless a profiler injects
+
 #include "common.h"
 #include "kernels.cuh"
 
@@ -24,6 +26,15 @@
 namespace scfr {
 
 constexpr int TPB = 128;
+
+// NVTX range over a scope (host API entry points and create stages), so an
+// nsys / ncu timeline shows where host time goes around the kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Process-wide host<->device byte counters (scfr_transfer_bytes).
 inline std::atomic<int64_t> g_h2d{0}, g_d2h{0};
@@ -317,7 +328,7 @@ struct scfr_handle {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int cap = 0;                 // schedule capacity (iterations)
-    std::vector<double> w_host;  // [B][cap]
+    std::vector<double> w_host, pf_host, nf_host;  // [B][cap] schedules (t^gamma, DCFR factors)
     scfr::DevBuf<double> wsched, pfsched, nfsched;
     scfr::DevBuf<long long> tdev;
     scfr::DevBuf<int> nonfinite;

@@ -1789,6 +1789,17 @@ static void keep_pool_resident(int device) {
     done[device] = 1;
 }
 
+// Per-iteration scalars of every solve, [B][cap] on the host and the device:
+// the averaging weight t^gamma and the DCFR factors, from libm pow like the
+// reference (or the caller's values, scfr_set_schedule).  Growing the
+// capacity keeps the entries already there.
+static void upload_schedule(scfr_handle* h) {
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    CUDA_OK(copy_sync(h->wsched.p, h->w_host.data(), h->w_host.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OK(copy_sync(h->pfsched.p, h->pf_host.data(), h->pf_host.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_OK(copy_sync(h->nfsched.p, h->nf_host.data(), h->nf_host.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
 static void ensure_schedule(scfr_handle* h, int64_t upto) {
     if (upto <= h->cap) return;
     AllocStream alloc_on(h->stream);
@@ -1796,23 +1807,32 @@ static void ensure_schedule(scfr_handle* h, int64_t upto) {
     while (cap < upto) cap *= 2;
     if (cap >= (1ll << 31)) fail(SCFR_EINVAL, "iteration count too large");
     const int B = h->B;
+    const int64_t old = h->cap;
     std::vector<double> w((size_t)B * cap), pf((size_t)B * cap), nf((size_t)B * cap);
     for (int k = 0; k < B; ++k)
         for (int64_t i = 0; i < cap; ++i) {
+            const size_t q = (size_t)k * cap + i;
+            if (i < old) {  // (keeps caller-set entries)
+                const size_t o = (size_t)k * old + i;
+                w[q] = h->w_host[o];
+                pf[q] = h->pf_host[o];
+                nf[q] = h->nf_host[o];
+                continue;
+            }
             const int64_t t = i + 1;  // reference RegretState.t during iteration i+1
-            w[(size_t)k * cap + i] = tpow(t, h->gamma[k]);
-            pf[(size_t)k * cap + i] = dfactor(t, h->alpha[k]);
-            nf[(size_t)k * cap + i] = dfactor(t, h->beta[k]);
+            w[q] = tpow(t, h->gamma[k]);
+            pf[q] = dfactor(t, h->alpha[k]);
+            nf[q] = dfactor(t, h->beta[k]);
         }
     CUDA_OK(cudaStreamSynchronize(h->stream));
     h->wsched.alloc(w.size());
     h->pfsched.alloc(pf.size());
     h->nfsched.alloc(nf.size());
-    CUDA_OK(copy_sync(h->wsched.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CUDA_OK(copy_sync(h->pfsched.p, pf.data(), pf.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CUDA_OK(copy_sync(h->nfsched.p, nf.data(), nf.size() * sizeof(double), cudaMemcpyHostToDevice));
     h->w_host.swap(w);
+    h->pf_host.swap(pf);
+    h->nf_host.swap(nf);
     h->cap = (int)cap;
+    upload_schedule(h);
     for (cudaGraphExec_t* e : {&h->exec, &h->exec_pro, &h->exec_body, &h->exec_epi})
         if (*e) {
             cudaGraphExecDestroy(*e);
@@ -2041,6 +2061,7 @@ static void prepare_top(scfr_handle* h, int k) {
 static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                         const scfr_csr* UT, const scfr_config* cfg, int device,
                         const char* nccl_id, int rank, int world, scfr_handle** out) {
+    NvtxRange nvtx("scfr_create");
     {
         if (!out || !cfg || !p1 || !p2 || !U || !UT) fail(SCFR_EINVAL, "NULL argument");
         if (nccl_id) {
@@ -2099,6 +2120,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         const char* trace = std::getenv("SCFR_TRACE");
         auto t_prev = std::chrono::steady_clock::now();
         auto stage = [&](const char* what) {  // SCFR_TRACE=1: create-time breakdown on stderr
+            nvtxMarkA(what);
             if (!(trace && trace[0] == '1')) return;
             const auto now = std::chrono::steady_clock::now();
             std::fprintf(stderr, "[scfr_create] %-12s %8.2f ms\n", what,
@@ -2294,6 +2316,7 @@ int scfr_engine(const scfr_handle* h, int* engine) {
 }
 
 int scfr_step(scfr_handle* h, int64_t n) {
+    NvtxRange nvtx("scfr_step");
     return guarded([&] {
         if (!h) fail(SCFR_EINVAL, "handle is NULL");
         if (n < 0) fail(SCFR_EINVAL, "n_iter must be >= 0");
@@ -2378,6 +2401,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
 }
 
 int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int* count) {
+    NvtxRange nvtx("scfr_timeline");
     return guarded([&] {
         if (!h || !out || !count) fail(SCFR_EINVAL, "bad arguments");
         if (n < 1 || (h->overlap && n < 2)) fail(SCFR_EINVAL, "n_iter must be >= 1 (>= 2 when overlapped)");
@@ -2448,6 +2472,28 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
     });
 }
 
+int scfr_set_schedule(scfr_handle* h, int solve, const double* w, const double* pf, const double* nf, int64_t n) {
+    return guarded([&] {
+        if (!h) fail(SCFR_EINVAL, "handle is NULL");
+        if (n < 0) fail(SCFR_EINVAL, "n must be >= 0");
+        if (solve < -1 || solve >= h->B) fail(SCFR_EINVAL, "solve out of range");
+        if (n == 0 || (!w && !pf && !nf)) return;
+        for (int64_t i = 0; i < n; ++i)
+            if ((w && !std::isfinite(w[i])) || (pf && !std::isfinite(pf[i])) || (nf && !std::isfinite(nf[i])))
+                fail(SCFR_EINVAL, "schedule entry %lld is not finite", (long long)i);
+        set_device(h);
+        ensure_schedule(h, h->t + n);
+        for (int k = solve < 0 ? 0 : solve; k < (solve < 0 ? h->B : solve + 1); ++k)
+            for (int64_t i = 0; i < n; ++i) {
+                const size_t q = (size_t)k * h->cap + h->t + i;
+                if (w) h->w_host[q] = w[i];
+                if (pf) h->pf_host[q] = pf[i];
+                if (nf) h->nf_host[q] = nf[i];
+            }
+        upload_schedule(h);
+    });
+}
+
 int scfr_synchronize(scfr_handle* h) {
     return guarded([&] {
         if (!h) fail(SCFR_EINVAL, "handle is NULL");
@@ -2460,6 +2506,7 @@ int scfr_synchronize(scfr_handle* h) {
 // and of the host counters: a coarse-to-fine time-to-target search replays
 // from it instead of paying a best response after every iteration.
 int scfr_snapshot(scfr_handle* h, int restore) {
+    NvtxRange nvtx("scfr_snapshot");
     return guarded([&] {
         if (!h) fail(SCFR_EINVAL, "handle is NULL");
         if (restore != 0 && restore != 1) fail(SCFR_EINVAL, "restore must be 0 (save) or 1 (restore)");
@@ -2508,6 +2555,7 @@ int scfr_avg_weight(const scfr_handle* h, int player, int solve, double* out) {
 }
 
 int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* host_out) {
+    NvtxRange nvtx("scfr_read_state");
     return guarded([&] {
         check_player(h, player, solve);
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
@@ -2533,6 +2581,7 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
 }
 
 int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
+    NvtxRange nvtx("scfr_read_average");
     return guarded([&] {
         check_player(h, player, solve);
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
@@ -2561,6 +2610,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
 }
 
 int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl, double* br1, double* br2) {
+    NvtxRange nvtx("scfr_exploitability");
     return guarded([&] {
         check_player(h, 1, solve);
         if (which != 0 && which != 1) fail(SCFR_EINVAL, "which must be 0 (average) or 1 (current)");

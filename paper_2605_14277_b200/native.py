@@ -109,6 +109,7 @@ _SIGS = {
                              C.POINTER(Config), C.c_int, C.c_char_p, C.c_int, C.c_int,
                              C.POINTER(C.c_void_p)], C.c_int),
     "scfr_step": ([C.c_void_p, C.c_int64], C.c_int),
+    "scfr_set_schedule": ([C.c_void_p, C.c_int, f64p, f64p, f64p, C.c_int64], C.c_int),
     "scfr_engine": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "scfr_synchronize": ([C.c_void_p], C.c_int),
     "scfr_snapshot": ([C.c_void_p, C.c_int], C.c_int),

@@ -163,6 +163,18 @@ class Solver:
     def step(self, n: int = 1) -> None:
         N.check(N.lib().scfr_step(self._h, int(n)))
 
+    def set_schedule(self, w=None, pos_factor=None, neg_factor=None, solve: int = -1) -> None:
+        """Caller-computed scalars for the next len(...) iterations: averaging
+        weights w_t (float(t)**gamma in the reference) and DCFR factors for
+        positive / negative regrets.  None keeps the library's libm values."""
+        arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (w, pos_factor, neg_factor)]
+        sizes = {a.shape[0] for a in arrs if a is not None}
+        if len(sizes) > 1:
+            raise ValueError("schedule arrays must have one length")
+        n = sizes.pop() if sizes else 0
+        ptrs = [None if a is None else N.ptr(a, C.c_double) for a in arrs]
+        N.check(N.lib().scfr_set_schedule(self._h, int(solve), *ptrs, n))
+
     def synchronize(self) -> None:
         N.check(N.lib().scfr_synchronize(self._h))
 

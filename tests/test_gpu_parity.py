@@ -317,3 +317,25 @@ def test_snapshot_restore_replays_bit_exact(gpu, engine):
     for k, v in _state(s).items():
         np.testing.assert_array_equal(v, first[k])
         assert digest(v) == rec["digests"][k], k
+
+
+@pytest.mark.parametrize("engine", ["levels", "persistent"])
+def test_set_schedule_reproduces_other_parameters(gpu, engine):
+    """scfr_set_schedule: a DCFR solve given the weights and factors of
+    other (alpha, beta, gamma) equals the solve created with them, bit for
+    bit (state and the host-side average weight)."""
+    from paper_2605_14277_b200.solvers import discount_factors
+    n = 60
+    target = SolverConfig("dcfr", alpha=2.5, beta=-0.5, gamma=3.0)
+    ref = Solver(bundle("leduc"), target, device=gpu, engine=engine)
+    ref.step(n)
+    s = Solver(bundle("leduc"), SolverConfig("dcfr", alpha=1.5, beta=0.0, gamma=2.0), device=gpu, engine=engine)
+    ts = range(1, n + 1)
+    s.set_schedule(w=[float(t) ** 3.0 for t in ts], pos_factor=[discount_factors(t, 2.5, -0.5)[0] for t in ts],
+                   neg_factor=[discount_factors(t, 2.5, -0.5)[1] for t in ts])
+    s.step(n)
+    for k, v in _state(ref).items():
+        np.testing.assert_array_equal(_state(s)[k], v, err_msg=k)
+    assert s.avg_weight() == ref.avg_weight()
+    with pytest.raises(ValueError):
+        s.set_schedule(w=[float("inf")])
