@@ -12,9 +12,13 @@ reference's own (tests/test_gpu_goof5.py).
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload ...]
 
 N = 1: the Goofspiel-5 solve on one GPU.  N > 1 (torchrun, one rank per GPU):
-config 4 — the SAME single solve with the payoff SpMV row-sharded over the
-ranks and an NCCL all-gather of u each iteration (strong scaling; value =
-that solve's iterations/s over the max-over-ranks device time).  Every line
+the SAME single solve (strong scaling; value = that solve's iterations/s over
+the max-over-ranks device time) with the tree passes subtree-sharded
+(``--mode subtree``, default: each rank runs the trunk and its own subtrees,
+NCCL broadcasts of the subtree roots' values) or with the
+payoff SpMV row-sharded and u all-gathered (``--mode sharded``, config 4).
+``--mode subtree|sharded`` at N = 1 runs that path over a 1-rank NCCL
+communicator.  Every line
 also carries ``sweep``: config 5, 256 distinct Leduc DCFR(alpha, beta, gamma)
 solves split over the N ranks (no collective), in solve-iterations/s.
 
@@ -376,12 +380,16 @@ def run_ours(args):
     desc, kind, variant = WORKLOADS[args.workload]
     bundle = make_bundle(kind)
     cfg = SolverConfig(variant)
-    sharded = ws > 1 and args.mode == "sharded"
+    mode = args.mode or ("subtree" if ws > 1 else "single")
+    sharded = mode in ("sharded", "subtree")  # one solve over the ranks (strong scaling)
 
     def make_solver():
-        if sharded:  # config 4: one solve, payoff SpMV rows split over the ranks
-            from paper_2605_14277_b200.distributed import sharded_solver
-            return sharded_solver(bundle, cfg, device=device)
+        if mode in ("sharded", "subtree"):
+            from paper_2605_14277_b200.distributed import nccl_unique_id, sharded_solver, subtree_solver
+            if dist is None:  # N = 1: a 1-rank NCCL communicator
+                return Solver(bundle, cfg, device=device, engine="levels", subtree=mode == "subtree",
+                              shard=(nccl_unique_id(), 0, 1))
+            return (subtree_solver if mode == "subtree" else sharded_solver)(bundle, cfg, device=device)
         return Solver(bundle, cfg, device=device, dtype=args.dtype)
 
     # process-level warm-up (CUDA context, lazy module load) outside any timing
@@ -494,7 +502,8 @@ def run_ours(args):
         "config": {"workload": desc, "variant": variant, "mode": cfg.mode, "gamma": cfg.gamma,
                    "seqs_per_player": [p.num_seqs for p in bundle.procs],
                    "nnz_U": bundle.payoff.nnz,
-                   "parallelism": (f"row-sharded payoff SpMV + NCCL all-gather x{ws} (config 4)" if sharded
+                   "parallelism": (f"subtree-sharded tree passes + NCCL root broadcasts x{ws}" if mode == "subtree"
+                                   else f"row-sharded payoff SpMV + NCCL all-gather x{ws} (config 4)" if sharded
                                    else f"independent replicas x{ws}" if ws > 1 else "1 gpu"),
                    "l2": "working set > L2 (no flush needed)",
                    "engine": s.engine},
@@ -569,8 +578,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-suite", action="store_true", help="skip the per-game section")
-    ap.add_argument("--mode", choices=("sharded", "replicas"), default="sharded",
-                    help="N>1: one row-sharded solve (config 4, strong; default) or independent replicas")
+    ap.add_argument("--mode", choices=("subtree", "sharded", "replicas", "single"), default=None,
+                    help="one solve with subtree-sharded tree passes (default for N>1), one row-sharded "
+                         "solve (config 4), independent replicas, or a plain one-GPU handle (default for N=1)")
     ap.add_argument("--no-sweep", action="store_true", help="skip config 5 (the 256-solve sweep)")
     ap.add_argument("--sweep-iters", type=int, default=1000)
     args = ap.parse_args()

@@ -210,6 +210,31 @@ int scfr_nccl_unique_id(char* out128);
 int scfr_create_sharded(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                         const scfr_csr* UT, const scfr_config* cfg, int device,
                         const char* nccl_unique_id, int rank, int world, scfr_handle** out);
+/* Multi-GPU subtree-sharded tree passes (the split PAPER.md
+ * :102-108 names: replicate the trunk, give each rank whole subtrees).  Each
+ * player's trunk (the levels above a split level holding <= 4096 decision
+ * points) is computed by every rank; below it rank r owns a contiguous range
+ * of subtree roots of each player, chosen (scfr_subtree_plan) so that its
+ * payoff rows read only its own subtrees' and the trunk's strategies.  Every
+ * level launch covers only the rank's decision points; after each bottom-up
+ * launch of a split level the roots' values are exchanged over NCCL (one
+ * in-place broadcast per rank, inside the CUDA graph), so the trunk sees
+ * exactly the one-GPU values and iterates stay bit-identical to one GPU.
+ * Reads (state, averages, exploitability, expected value) first gather the
+ * subtree state of every rank.  Fused level engine, fp64, batch 1.
+ * Collective like scfr_create_sharded.  SCFR_EINVAL when the game has no such
+ * split (trunk rows coupled to subtree columns, fewer closed root blocks than
+ * ranks, ...). */
+int scfr_create_subtree(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                        const scfr_csr* UT, const scfr_config* cfg, int device,
+                        const char* nccl_unique_id, int rank, int world, scfr_handle** out);
+/* Host-only planner of the subtree mode (no GPU needed): the split level of
+ * each player (ls_out[2], merged-level index), the root boundaries of every
+ * rank (cuts_out[2 * (world + 1)]: player k's rank r owns level-ls roots
+ * [cuts[k*(world+1)+r], cuts[k*(world+1)+r+1])) and, if seqs_out is not NULL,
+ * the subtree sequences of each rank (seqs_out[2 * world]). */
+int scfr_subtree_plan(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, int world,
+                      int32_t* ls_out, int64_t* cuts_out, int64_t* seqs_out);
 
 /* Runs n full iterations (_step semantics incl. t++ for both players) on the
  * handle's stream; asynchronous. */

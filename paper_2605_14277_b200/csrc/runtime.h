@@ -372,10 +372,21 @@ struct scfr_handle {
     bool timed = false;
     scfr::PersistentPlan plan;
     scfr::Snapshot snap;
-    // Row-sharded payoff SpMV (scfr_create_sharded): NCCL communicator
-    // (ncclComm_t) over `world` ranks, this handle being `rank`.
+    // Multi-GPU modes: NCCL communicator (ncclComm_t) over `world` ranks,
+    // this handle being `rank`; the row-sharded payoff SpMV
+    // (scfr_create_sharded) or, with `subtree`, the subtree-sharded tree
+    // passes (scfr_create_subtree, subtree.h): launches of levels >= sub_ls[k]
+    // cover DPs [sub_jb[k][l][rank], sub_jb[k][l][rank + 1]) (sequences
+    // sub_sb), the roots' V is broadcast after bottom-up split launches, and
+    // reads gather the other ranks' subtrees first (sub_stale)
     void* comm = nullptr;
     int world = 1, rank = 0;
+    bool subtree = false, sub_stale = false;
+    int sub_ls[2] = {-1, -1};
+    int sub_sim = 1;    // SCFR_SUBTREE_SIM (world 1): ranks simulated by split launches
+    int sub_view = -1;  // SCFR_SUBTREE_VIEW (world 1, timing): one rank's launches of a larger plan
+    std::vector<std::vector<int>> sub_jb[2], sub_sb[2];
+    bool rowshard() const { return comm && !subtree; }
     // Tile engine (SCFR_ENGINE_TILED): per-player plans and the payoff rows
     // in the tile numbering (rows of U for player 1, of Uᵀ for player 2).
     scfr::TilePlayer tp[2];

@@ -30,10 +30,11 @@
 #include <vector>
 
 #include <dlfcn.h>
-#include <nccl.h>  // types only: the library is dlopen'ed by the sharded mode
+#include <nccl.h>  // types only: the library is dlopen'ed by the multi-GPU modes
 
 #include "host_par.h"
 #include "runtime.h"
+#include "subtree.h"
 
 namespace scfr {
 
@@ -1091,6 +1092,9 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -1111,6 +1115,9 @@ static const NcclApi& nccl() {
     api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     loaded = true;
@@ -1129,6 +1136,38 @@ static const NcclApi& nccl() {
 static void allgather_rows(scfr_handle* h, double* full, int chunk) {
     NCCL_OK(nccl().AllGather(full + (size_t)h->rank * chunk, full, (size_t)chunk, ncclDouble,
                              (ncclComm_t)h->comm, h->stream));
+}
+
+// Subtree mode: every rank broadcasts its own range [b[r], b[r+1]) of `buf`
+// (elements of `esize` bytes) in place, one NCCL group on `s`.
+static void broadcast_ranges(scfr_handle* h, void* buf, size_t esize, const std::vector<int>& b, cudaStream_t s) {
+    char* base = static_cast<char*>(buf);
+    const ncclDataType_t ty = esize == 8 ? ncclDouble : ncclFloat;
+    for (int r = 0; r < h->world; ++r) {
+        const size_t cnt = (size_t)(b[r + 1] - b[r]);
+        if (cnt) {
+            void* p = base + (size_t)b[r] * esize;
+            NCCL_OK(nccl().Broadcast(p, p, cnt, ty, r, (ncclComm_t)h->comm, s));
+        }
+    }
+}
+
+// Subtree mode, before a read: the other ranks' subtree state (every state
+// vector of every forest level) broadcast by its owners, so that the handle
+// holds the one-GPU state.
+static void gather_subtrees(scfr_handle* h) {
+    if (!h->subtree || !h->sub_stale || h->sub_sim > 1 || h->sub_view >= 0) return;
+    NCCL_OK(nccl().GroupStart());
+    for (int k = 0; k < 2; ++k) {
+        Player& P = h->P[k];
+        for (int l = h->sub_ls[k]; l >= 0 && l < P.levels(); ++l) {
+            for (DevBuf<double>* v : {&P.r, &P.b, &P.x, &P.xpost, &P.avg, &P.u, &P.bcur})
+                if (v->n) broadcast_ranges(h, v->p, sizeof(double), h->sub_sb[k][l], h->stream);
+            broadcast_ranges(h, P.V.p, sizeof(double), h->sub_jb[k][l], h->stream);
+        }
+    }
+    NCCL_OK(nccl().GroupEnd());
+    h->sub_stale = false;
 }
 
 // --- per-iteration launch sequence --------------------------------------
@@ -1361,11 +1400,33 @@ struct Launcher : LaunchBase {
         else return M.data.p;
     }
 
-    // One launch over level la of A and level lb of Bp (either may be absent).
+    // One launch over level la of A and level lb of Bp (either may be absent);
+    // subtree mode: a bottom-up launch of a split level is followed by the
+    // exchange of the roots' V (also on a rank whose own range is empty).
     template <class R>
     void level(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
                R* xa, R* xb, bool do_rm, const R* vca = nullptr, const R* vcb = nullptr, int skipa = 0,
                int skipb = 0) {
+        // SCFR_SUBTREE_SIM=W at world 1: a forest level runs as W launches, one
+        // per rank range of a W-rank plan (tests the range restriction on one GPU)
+        const bool forest = h->subtree && ((A && la >= 0 && la >= h->sub_ls[0]) || (Bp && lb >= 0 && lb >= h->sub_ls[1]));
+        const int parts = forest && h->sub_sim > 1 ? h->sub_sim : 1;
+        for (int part = 0; part < parts; ++part)
+            level_launch<R>(lk, kk, A, la, Bp, lb, ua, ub, xa, xb, do_rm, vca, vcb, skipa, skipb, part);
+        if (!h->subtree || h->sub_sim > 1 || h->sub_view >= 0 || (lk != LK_OBS && lk != LK_PRED)) return;
+        const bool ea = A && la >= 0 && la == h->sub_ls[0];
+        const bool eb = Bp && lb >= 0 && lb == h->sub_ls[1];
+        if (!ea && !eb) return;
+        cudaStream_t s = st ? st : h->stream;
+        NCCL_OK(nccl().GroupStart());
+        if (ea) broadcast_ranges(h, A->V.p, sizeof(R), h->sub_jb[0][la], s);
+        if (eb) broadcast_ranges(h, Bp->V.p, sizeof(R), h->sub_jb[1][lb], s);
+        NCCL_OK(nccl().GroupEnd());
+    }
+
+    template <class R>
+    void level_launch(int lk, int kk, Player* A, int la, Player* Bp, int lb, const R* ua, const R* ub,
+                      R* xa, R* xb, bool do_rm, const R* vca, const R* vcb, int skipa, int skipb, int part) {
         // a level already computed by its child level's pair launch
         if (A && la >= 0 && la == paired_[0] && lk == paired_kind_[0]) la = -1;
         if (Bp && lb >= 0 && lb == paired_[1] && lk == paired_kind_[1]) lb = -1;
@@ -1387,6 +1448,23 @@ struct Launcher : LaunchBase {
         };
         attach_top(t0, A, la);
         attach_top(t1, Bp, lb);
+        if (h->subtree) {  // this rank's DPs of a forest level
+            const int rk = h->sub_sim > 1 ? part : h->sub_view >= 0 ? h->sub_view : h->rank;
+            auto own = [&](TaskT<R>& t, Player* P, int l) {
+                const int k = P == &h->P[0] ? 0 : 1;
+                if (part > 0) t.top = nullptr;  // (simulated ranks: the first part wrote the top)
+                if (!P || l < 0 || l >= P->levels()) return;
+                if (l < h->sub_ls[k]) {
+                    if (part > 0) t.n = 0;  // the trunk runs once
+                    return;
+                }
+                const std::vector<int>& jb = h->sub_jb[k][l];
+                t.lo = jb[rk];
+                t.n = jb[rk + 1] - t.lo;
+            };
+            own(t0, A, la);
+            own(t1, Bp, lb);
+        }
         const bool fused_here = lk == LK_OBS && fuse_spmv();
         if (t0.n == 0 && t1.n == 0) return;
         const bool fused = fused_here;
@@ -1609,7 +1687,7 @@ struct Launcher : LaunchBase {
                 payoff_data<R>(M), x, sx, out + M.row0, so, neg ? 1 : 0, h->nonfinite.p);
         });
         if constexpr (sizeof(R) == 8)
-            if (h->comm) allgather_rows(h, out, M.chunk);
+            if (h->rowshard()) allgather_rows(h, out, M.chunk);
     }
 
     void iteration() {
@@ -1933,7 +2011,7 @@ static void solve_spmv(scfr_handle* h, const DevCsr& M, const double* x, double*
                                                             M.data.p, x, 0, out + M.row0, 0,
                                                             neg ? 1 : 0, nullptr);
     CUDA_OK(cudaGetLastError());
-    if (h->comm) allgather_rows(h, out, M.chunk);
+    if (h->rowshard()) allgather_rows(h, out, M.chunk);
 }
 
 static double best_response(scfr_handle* h, int player, const double* x_opp) {
@@ -2058,22 +2136,64 @@ static void prepare_top(scfr_handle* h, int k) {
     tp.on = true;
 }
 
+// Subtree mode: the partition (subtree.h) on the structure this create
+// converted; every rank must launch the level that recomputes a player's top
+// (its top_prologue writes the whole top's x).
+static void plan_subtree_mode(scfr_handle* h, const scfr_csr* U) {
+    HostProcess H[2];
+    for (int k = 0; k < 2; ++k) {
+        const Player& P = h->P[k];
+        if (!P.h_seq_ptr || !P.h_dp_parent || P.J == 0)
+            fail(SCFR_EINVAL, "the subtree-sharded mode needs decision points for both players");
+        H[k] = HostProcess{P.h_seq_ptr->data(), P.h_dp_parent->data(), &P.lvl, P.J, P.S};
+    }
+    SubtreePlan plan;
+    const char* sim = std::getenv("SCFR_SUBTREE_SIM");
+    h->sub_sim = h->world == 1 && sim ? std::max(1, std::atoi(sim)) : 1;
+    // SCFR_SUBTREE_VIEW="W,r" (world 1, timing only): launch exactly rank r's
+    // ranges of a W-rank plan, no exchange: one rank's per-iteration kernel
+    // time at N = W (the values are not a solve: other ranks' roots are stale)
+    int vw = 1;
+    if (const char* v = std::getenv("SCFR_SUBTREE_VIEW"))
+        if (h->world == 1 && std::sscanf(v, "%d,%d", &vw, &h->sub_view) == 2 && vw >= 1 && h->sub_view >= 0 &&
+            h->sub_view < vw) {
+            h->sub_sim = 1;
+        } else {
+            vw = 1;
+            h->sub_view = -1;
+        }
+    plan_subtrees(H, U, h->world * h->sub_sim * vw, plan);
+    for (int k = 0; k < 2; ++k) {
+        h->sub_ls[k] = plan.ls[k];
+        h->sub_jb[k] = std::move(plan.jb[k]);
+        h->sub_sb[k] = std::move(plan.sb[k]);
+        const TopPlayer& tp = h->top[k];
+        if (tp.on && tp.ls >= h->sub_ls[k]) {
+            const std::vector<int>& jb = h->sub_jb[k][tp.ls];
+            for (int r = 0; r < h->world * h->sub_sim * vw; ++r)
+                if (jb[r + 1] == jb[r])
+                    fail(SCFR_EINVAL, "rank %d holds no level-%d decision point of player %d", r, tp.ls, k + 1);
+        }
+    }
+}
+
 static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                         const scfr_csr* UT, const scfr_config* cfg, int device,
-                        const char* nccl_id, int rank, int world, scfr_handle** out) {
+                        const char* nccl_id, int rank, int world, scfr_handle** out, bool subtree = false) {
     NvtxRange nvtx("scfr_create");
     {
         if (!out || !cfg || !p1 || !p2 || !U || !UT) fail(SCFR_EINVAL, "NULL argument");
+        const char* mname = subtree ? "subtree-sharded" : "row-sharded";
         if (nccl_id) {
             if (world < 1 || rank < 0 || rank >= world) fail(SCFR_EINVAL, "bad rank / world size");
-            if (cfg->batch != 1) fail(SCFR_EINVAL, "the row-sharded mode runs a single solve (batch 1)");
+            if (cfg->batch != 1) fail(SCFR_EINVAL, "the %s mode runs a single solve (batch 1)", mname);
             if (cfg->engine != SCFR_ENGINE_AUTO && cfg->engine != SCFR_ENGINE_LEVELS)
-                fail(SCFR_EINVAL, "the row-sharded mode runs on the level engine");
+                fail(SCFR_EINVAL, "the %s mode runs on the level engine", mname);
         }
         if (cfg->variant < SCFR_CFR || cfg->variant > SCFR_PCFR_PLUS) fail(SCFR_EINVAL, "unknown variant");
         if (cfg->dtype != SCFR_DTYPE_F64 && cfg->dtype != SCFR_DTYPE_F32) fail(SCFR_EINVAL, "unknown dtype");
         if (cfg->dtype == SCFR_DTYPE_F32) {
-            if (nccl_id) fail(SCFR_EINVAL, "the fp32 mode does not run the row-sharded mode");
+            if (nccl_id) fail(SCFR_EINVAL, "the fp32 mode does not run the %s mode", mname);
             if (cfg->engine != SCFR_ENGINE_AUTO && cfg->engine != SCFR_ENGINE_LEVELS)
                 fail(SCFR_EINVAL, "the fp32 mode runs on the level engine");
         }
@@ -2138,6 +2258,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         pa.reserve((size_t)(U->rows + UT->rows) * 4 + (size_t)std::max<int64_t>(U->nnz, 1) * 24 + 8192);
         pa.reset();
         const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
+        const int wc = subtree ? 1 : w, rc = subtree ? 0 : rk;  // payoff rows held: all in the subtree mode
         {
             // two independent pipelines, each on half the host threads:
             // player 1 then U (its rows are player 1's sequences), and
@@ -2151,8 +2272,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                     switch (k) {
                         case 0: upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32); break;
                         case 1: upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32); break;
-                        case 2: upload_csr(U, h->U, h->stream, h->f32, w, rk); break;
-                        default: upload_csr(UT, h->UT, h->stream, h->f32, w, rk); break;
+                        case 2: upload_csr(U, h->U, h->stream, h->f32, wc, rc); break;
+                        default: upload_csr(UT, h->UT, h->stream, h->f32, wc, rc); break;
                     }
                 } catch (...) {
                     err[k] = std::current_exception();
@@ -2167,14 +2288,14 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             t3.join();
             for (auto& e : err)
                 if (e) std::rethrow_exception(e);
-            csr_level_info(U, h->U, h->P[0], h->stream, w == 1);  // U's rows: player 1's sequences
-            csr_level_info(UT, h->UT, h->P[1], h->stream, w == 1);
+            csr_level_info(U, h->U, h->P[0], h->stream, wc == 1);  // U's rows: player 1's sequences
+            csr_level_info(UT, h->UT, h->P[1], h->stream, wc == 1);
             CUDA_OK(cudaStreamSynchronize(h->stream));
         }
         stage("players+payoff");
         if (nccl_id) {
             // u and the BR gradient are gathered as world x chunk (padded) vectors
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < 2 && !subtree; ++k) {
                 Player& P = h->P[k];
                 const size_t pad = (size_t)w * (k == 0 ? h->U.chunk : h->UT.chunk);
                 if (pad > (size_t)P.S) {
@@ -2191,6 +2312,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             h->comm_destroy = [](void* c) { nccl().CommDestroy((ncclComm_t)c); };
             h->world = w;
             h->rank = rk;
+            h->subtree = subtree;
         }
         stage("payoff");
         h->tdev.alloc(1);
@@ -2214,7 +2336,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (const char* pnj = std::getenv("SCFR_PIPE_NJ")) h->pipe_nj = std::atoll(pnj);
         if (const char* pk = std::getenv("SCFR_PIPE_KINDS")) h->pipe_kinds = std::atoi(pk);
         const char* npr = std::getenv("SCFR_PAIR");  // opt-in: measured slower
-        h->pair = npr && npr[0] == '1';
+        h->pair = npr && npr[0] == '1' && !subtree;
         if (const char* gnj = std::getenv("SCFR_GROUP_NJ")) h->group_nj = std::atoll(gnj);
         const char* nsw = std::getenv("SCFR_NO_SMALL_WARP");
         h->small_warp = !(nsw && nsw[0] == '1');
@@ -2224,7 +2346,8 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         const char* ntw = std::getenv("SCFR_NO_TD_WARP");
         h->td_warp = !(ntw && ntw[0] == '1');
         const char* nfz = std::getenv("SCFR_NO_FUSE");
-        h->fuse = !(nfz && nfz[0] == '1') && !h->comm;  // sharded: SpMV + all-gather instead
+        h->fuse = !(nfz && nfz[0] == '1') && !h->rowshard();  // row-sharded: SpMV + all-gather instead
+        if (subtree && !h->fuse) fail(SCFR_EINVAL, "the subtree-sharded mode runs the fused level engine");
         if (const char* wc = std::getenv("SCFR_WAVE_CTAS")) {
             h->wave_ctas = std::max(1, std::atoi(wc));
             h->wave_ctas_env = true;
@@ -2242,7 +2365,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         if (h->engine == SCFR_ENGINE_PERSISTENT || h->engine == SCFR_ENGINE_PERSISTENT_GRID ||
             h->engine == SCFR_ENGINE_PERSISTENT_CLUSTER)
             prepare_persistent(h.get());
-        if (h->engine == SCFR_ENGINE_LEVELS && !h->comm && h->fuse && h->P[0].J > 0 && h->P[1].J > 0) {
+        if (h->engine == SCFR_ENGINE_LEVELS && !h->rowshard() && h->fuse && h->P[0].J > 0 && h->P[1].J > 0) {
             // structurally empty payoff rows: u is a constant ±0.0 (kernels.cuh ld_u)
             const char* nue = std::getenv("SCFR_NO_EMPTY_ROWS");
             h->u_empty_skip = !(nue && nue[0] == '1');
@@ -2258,7 +2381,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             h->bcur_on = !(nb && nb[0] == '1');
             if (h->bcur_on) h->P[0].bcur.alloc(val_slots((size_t)h->P[0].S * h->B, h->f32));
         }
-        if (h->engine == SCFR_ENGINE_LEVELS && !h->comm) {
+        if (h->engine == SCFR_ENGINE_LEVELS && !h->rowshard()) {
             // forced leaf levels: skip their top-down launches (k_expand_leaf)
             const bool l1 = leaf_single(h.get(), h->P[0]), l2 = leaf_single(h.get(), h->P[1]);
             h->leaf_x = l1 || l2;
@@ -2270,7 +2393,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // alt mode: player 1's next overlaps player 2's observe
             const char* nov = std::getenv("SCFR_NO_OVERLAP");
             if (h->mode == SCFR_MODE_ALT && h->fuse && !(nov && nov[0] == '1') && h->P[0].J > 0 &&
-                h->P[1].J > 0) {
+                h->P[1].J > 0 && !subtree) {
                 CUDA_OK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
@@ -2278,6 +2401,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                 h->overlap = true;
             }
         }
+        if (subtree) plan_subtree_mode(h.get(), U);
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
         stage("engine");
@@ -2288,6 +2412,15 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
 int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U, const scfr_csr* UT,
                 const scfr_config* cfg, int device, scfr_handle** out) {
     return guarded([&] { create_impl(p1, p2, U, UT, cfg, device, nullptr, 0, 1, out); });
+}
+
+int scfr_create_subtree(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
+                        const scfr_csr* UT, const scfr_config* cfg, int device,
+                        const char* nccl_id, int rank, int world, scfr_handle** out) {
+    return guarded([&] {
+        if (!nccl_id) fail(SCFR_EINVAL, "NULL NCCL unique id");
+        create_impl(p1, p2, U, UT, cfg, device, nccl_id, rank, world, out, true);
+    });
 }
 
 int scfr_nccl_unique_id(char* out) {
@@ -2348,6 +2481,7 @@ int scfr_step(scfr_handle* h, int64_t n) {
         CUDA_OK(cudaEventRecord(h->ev1, h->stream));
         h->timed = true;
         h->t += n;
+        h->sub_stale = h->subtree;
     });
 }
 
@@ -2380,6 +2514,7 @@ int scfr_profile_step(scfr_handle* h, int64_t n, scfr_kernel_stat* out, int cap,
         CUDA_OK(cudaStreamSynchronize(h->stream));
         h->timed = false;
         h->t += n;
+        h->sub_stale = h->subtree;
         h->launches += issued;
         for (int k = 0; k < KK_COUNT; ++k) {
             std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[k]);
@@ -2459,6 +2594,7 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
         cudaGraphExecDestroy(exec);
         h->timed = false;
         h->t += n;
+        h->sub_stale = h->subtree;
         h->launches += h->overlap ? h->nodes_pro + rec * m + h->nodes_epi : n * m;
         for (int k = 0; k < m; ++k) {
             std::snprintf(out[k].name, sizeof out[k].name, "%s", kKernelNames[kinds[k].kind]);
@@ -2535,6 +2671,7 @@ int scfr_snapshot(scfr_handle* h, int restore) {
             CUDA_OK(cudaMemcpyAsync(h->tdev.p, sn.tdev.p, sizeof(long long), cudaMemcpyDeviceToDevice, h->stream));
             h->t = sn.t;
             h->avg_weight = sn.avg_weight;
+            h->sub_stale = h->subtree;
         }
     });
 }
@@ -2560,6 +2697,7 @@ int scfr_read_state(scfr_handle* h, int player, int solve, int which, double* ho
         check_player(h, player, solve);
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
         set_device(h);
+        gather_subtrees(h);
         Player& P = h->P[player - 1];
         const double* src = nullptr;
         size_t off = 0, cnt = P.S;
@@ -2587,6 +2725,7 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
         if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
         set_device(h);
+        gather_subtrees(h);
         Player& P = h->P[player - 1];
         // avg_accum / avg_weight (IEEE division, as the reference's numpy divide)
         expand_leaves(h, player, P.avg, solve);
@@ -2603,6 +2742,7 @@ int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out) {
         if (!host_out) fail(SCFR_EINVAL, "NULL argument");
         if (h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
         set_device(h);
+        gather_subtrees(h);
         Player& P = h->P[player - 1];
         expand_leaves(h, player, P.x, solve);
         read_to_host(h, host_out, orig_order(h, player, P.x.p, solve), P.S);
@@ -2616,6 +2756,7 @@ int scfr_exploitability(scfr_handle* h, int solve, int which, double* expl, doub
         if (which != 0 && which != 1) fail(SCFR_EINVAL, "which must be 0 (average) or 1 (current)");
         if (which == 1 && h->t == 0) fail(SCFR_EINVAL, "no iteration has run yet");
         set_device(h);
+        gather_subtrees(h);
         // br1 against x2, then br2 against x1 (pkg/metrics.py:59-68); xbar
         // buffers are per player so both profiles can be live at once.
         const double* x2 = profile(h, 2, solve, which);
@@ -2639,6 +2780,7 @@ int scfr_expected_value(scfr_handle* h, int solve, double* out) {
         check_player(h, 1, solve);
         if (!out) fail(SCFR_EINVAL, "NULL argument");
         set_device(h);
+        gather_subtrees(h);
         const double* x2 = profile(h, 2, solve, 0);
         Player& A = h->P[0];
         solve_spmv(h, h->U, x2, A.g.p, false);

@@ -1,6 +1,6 @@
 """Multi-GPU plumbing (one process per GPU, torch.distributed for control).
 
-Two modes:
+Three modes:
 
 * Row-sharded payoff SpMV for one big solve (BASELINE config 4):
   ``sharded_solver(bundle, config)``.  Every rank keeps the full
@@ -10,6 +10,13 @@ Two modes:
   NCCL inside the iteration (C-ABI ``scfr_create_sharded``) — no reduction
   collective, so iterates are bit-identical to one GPU.  torch.distributed
   only broadcasts the 128-byte NCCL unique id.
+* Subtree-sharded tree passes for one big solve: ``subtree_solver(bundle,
+  config)``.  Every rank computes the small trunk of each player; below each
+  player's split level rank k owns a contiguous range of whole subtrees
+  (``subtree_plan``), chosen so its payoff rows read only its own subtrees'
+  strategies.  Launches cover only the rank's decision points; the subtree
+  roots' values are exchanged (NCCL, in the graph) after each bottom-up
+  launch of a split level, so iterates are bit-identical to one GPU.
 * Independent solves (BASELINE config 5): ``sweep_slice(params, world, k)``
   gives rank k a contiguous slice of the (alpha, beta, gamma) grid, solved as
   one batched handle per GPU; no collective on the data path.
@@ -69,4 +76,38 @@ def sharded_solver(bundle: GameBundle, config: SolverConfig, device: int | None 
         device = int(os.environ.get("LOCAL_RANK", "0"))
     uid = broadcast_unique_id(group)
     return Solver(bundle, config, device=device, engine="levels",
+                  shard=(uid, dist.get_rank(group), dist.get_world_size(group)))
+
+
+def subtree_plan(bundle: GameBundle, world: int) -> dict:
+    """The subtree partition (C-ABI scfr_subtree_plan; host only, no GPU):
+    ``ls`` = each player's split level (merged-level index), ``cuts[k]`` =
+    the world+1 root boundaries of player k+1 (rank r owns level-ls roots
+    [cuts[k][r], cuts[k][r+1])), ``seqs[k]`` = subtree sequences per rank.
+    Raises ValueError (SCFR_EINVAL) for games the subtree mode cannot split."""
+    import numpy as np
+    if world < 1:
+        raise ValueError("bad world size")
+    p1, p2, U, _ = bundle._c
+    ls = (C.c_int32 * 2)()
+    cuts = np.zeros(2 * (world + 1), dtype=np.int64)
+    seqs = np.zeros(2 * world, dtype=np.int64)
+    N.check(N.lib().scfr_subtree_plan(C.byref(p1), C.byref(p2), C.byref(U), int(world), ls,
+                                      N.ptr(cuts, C.c_int64), N.ptr(seqs, C.c_int64)))
+    return {"ls": (int(ls[0]), int(ls[1])),
+            "cuts": (cuts[:world + 1].tolist(), cuts[world + 1:].tolist()),
+            "seqs": (seqs[:world].tolist(), seqs[world:].tolist())}
+
+
+def subtree_solver(bundle: GameBundle, config: SolverConfig, device: int | None = None,
+                   group=None) -> Solver:
+    """A Solver whose tree passes are subtree-sharded over the torch.distributed
+    group (C-ABI scfr_create_subtree): each rank computes the trunk and its own
+    subtrees, exchanging the subtree roots' values over NCCL.  All ranks must
+    step / query it together."""
+    import torch.distributed as dist
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    uid = broadcast_unique_id(group)
+    return Solver(bundle, config, device=device, engine="levels", subtree=True,
                   shard=(uid, dist.get_rank(group), dist.get_world_size(group)))

@@ -108,6 +108,11 @@ _SIGS = {
     "scfr_create_sharded": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.POINTER(Csr),
                              C.POINTER(Config), C.c_int, C.c_char_p, C.c_int, C.c_int,
                              C.POINTER(C.c_void_p)], C.c_int),
+    "scfr_create_subtree": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.POINTER(Csr),
+                             C.POINTER(Config), C.c_int, C.c_char_p, C.c_int, C.c_int,
+                             C.POINTER(C.c_void_p)], C.c_int),
+    "scfr_subtree_plan": ([C.POINTER(Tfsdp), C.POINTER(Tfsdp), C.POINTER(Csr), C.c_int,
+                           C.POINTER(C.c_int32), i64p, i64p], C.c_int),
     "scfr_step": ([C.c_void_p, C.c_int64], C.c_int),
     "scfr_set_schedule": ([C.c_void_p, C.c_int, f64p, f64p, f64p, C.c_int64], C.c_int),
     "scfr_engine": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),

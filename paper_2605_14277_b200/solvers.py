@@ -107,9 +107,12 @@ class Solver:
     """
 
     def __init__(self, bundle: GameBundle, config: SolverConfig, device: int = 0,
-                 batch_params=None, engine: str = "auto", shard=None, dtype: str = "f64"):
-        """``shard=(nccl_unique_id, rank, world)`` selects the row-sharded
-        multi-GPU mode (see distributed.sharded_solver).  ``dtype="f32"``
+                 batch_params=None, engine: str = "auto", shard=None, dtype: str = "f64",
+                 subtree: bool = False):
+        """``shard=(nccl_unique_id, rank, world)`` selects a multi-GPU mode:
+        the row-sharded payoff (distributed.sharded_solver) or, with
+        ``subtree=True``, the subtree-sharded tree passes
+        (distributed.subtree_solver).  ``dtype="f32"``
         runs the iteration in fp32 (same operation order, fp32 rounding;
         level engine); reads and exploitability stay fp64."""
         if dtype not in N.DTYPE_CODE:
@@ -146,14 +149,17 @@ class Solver:
         h = C.c_void_p()
         p1, p2, U, UT = bundle._c
         self.shard = None
+        self.subtree = bool(subtree)
+        if subtree and shard is None:
+            raise ValueError("subtree=True needs shard=(nccl_unique_id, rank, world)")
         if shard is not None:
             uid, rank, world = shard
             if len(uid) != 128:
                 raise ValueError("NCCL unique id must be 128 bytes")
             self.shard = (int(rank), int(world))
-            N.check(L.scfr_create_sharded(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT),
-                                          C.byref(cfg), int(device), uid, int(rank), int(world),
-                                          C.byref(h)))
+            create = L.scfr_create_subtree if subtree else L.scfr_create_sharded
+            N.check(create(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT),
+                           C.byref(cfg), int(device), uid, int(rank), int(world), C.byref(h)))
         else:
             N.check(L.scfr_create(C.byref(p1), C.byref(p2), C.byref(U), C.byref(UT),
                                   C.byref(cfg), int(device), C.byref(h)))
