@@ -19,6 +19,7 @@
 // (kernels.cuh), so iterates are bit-identical across engines.
 
 #include <algorithm>
+#include <cstring>
 #include <type_traits>
 
 #include <cooperative_groups.h>
@@ -58,6 +59,7 @@ struct PArgs {
     long long* tdev;
     unsigned* barrier;
     long long* trace;  // SCFR_PHASE_TRACE=1: per-phase clock64 deltas (CTA 0, thread 0)
+    const unsigned char* csr;  // SmemPlan::csr block (SMEM engine)
 };
 
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
@@ -318,6 +320,21 @@ __device__ __forceinline__ void small_warp_item(int kind, const SmemPlan& sp, in
         pred_dp_warp<LdS>(P.T, j, P.u, P.r, P.b, P.V, a.plus != 0, lane);
 }
 
+// Payoff row from the shared-memory copy: the same products and the same
+// left-to-right sum as spmv_range (((0 + d0*x0) + d1*x1) + ...), d = the
+// value table entry of the non-zero.
+__device__ __forceinline__ double spmv_row_smem(const SmemPlan& sp, int ptr, int col, int vid, const double* x,
+                                                int row) {
+    const int* p = reinterpret_cast<const int*>(g_smem + ptr);
+    const unsigned short* c = reinterpret_cast<const unsigned short*>(g_smem + col);
+    const unsigned short* v = reinterpret_cast<const unsigned short*>(g_smem + vid);
+    const double* tab = reinterpret_cast<const double*>(g_smem + sp.tab);
+    double acc = 0.0;
+    const int k1 = p[row + 1];
+    for (int k = p[row]; k < k1; ++k) acc = dadd(acc, dmul(tab[v[k]], x[c[k]]));
+    return acc;
+}
+
 template <int MAXA, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PArgs a,
                                                    const __grid_constant__ SmemPlan sp) {
@@ -326,6 +343,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
     for (int i = threadIdx.x; i < a.nphase; i += blockDim.x) prog[i] = a.prog[i];
     stage<0>(a, sptrs<0>(sp), solve, true);
     stage<1>(a, sptrs<1>(sp), solve, true);
+    if (sp.csr_bytes) {
+        const int4* src = reinterpret_cast<const int4*>(a.csr);
+        int4* dst = reinterpret_cast<int4*>(g_smem + sp.csr);
+        for (int i = threadIdx.x; i < sp.csr_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
     __syncthreads();
     const int rank = threadIdx.x, size = blockDim.x;
     const int warp = rank >> 5, lane = rank & 31, nwarps = size >> 5;
@@ -359,12 +381,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
                     const bool first = ph.kind == PH_SPMV_U || (ph.kind == PH_SPMV_BOTH && i < a.Urows);
                     double acc;
                     if (first) {
-                        acc = spmv_row<LdS>(a.Uip, a.Uix, a.Ud, sptrs<1>(sp).x, i);
+                        acc = sp.csr_bytes ? spmv_row_smem(sp, sp.uptr, sp.ucol, sp.uvid, sptrs<1>(sp).x, i)
+                                           : spmv_row<LdS>(a.Uip, a.Uix, a.Ud, sptrs<1>(sp).x, i);
                         sptrs<0>(sp).u[i] = acc;
                     } else {
                         const SPtrs P0 = sptrs<0>(sp);
                         const int row = ph.kind == PH_SPMV_BOTH ? i - a.Urows : i;
-                        acc = dmul(-1.0, spmv_row<LdS>(a.Tip, a.Tix, a.Td, a.alt ? P0.xpost : P0.x, row));
+                        const double* x1 = a.alt ? P0.xpost : P0.x;
+                        acc = dmul(-1.0, sp.csr_bytes ? spmv_row_smem(sp, sp.tptr, sp.tcol, sp.tvid, x1, row)
+                                                      : spmv_row<LdS>(a.Tip, a.Tix, a.Td, x1, row));
                         sptrs<1>(sp).u[row] = acc;
                     }
                     if (!isfinite(acc)) atomicOr(a.nonfinite, 1);
@@ -398,7 +423,8 @@ static constexpr auto kGrid = k_persistent<PM_GRID, 8, 128>;
 static constexpr int kClusterThreads = 256;
 static constexpr auto kClu = k_persistent<PM_CLUSTER, 8, kClusterThreads>;
 static constexpr int kSmallThreads = 256;
-static constexpr auto kSmall = k_small<2, kSmallThreads>;
+static constexpr auto kSmall2 = k_small<2, kSmallThreads>;
+static constexpr auto kSmall3 = k_small<3, kSmallThreads>;
 static constexpr int kSmemLimit = 220 * 1024;
 
 // Byte layout of one solve in the SMEM engine; returns the total size.
@@ -425,12 +451,95 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
         o.dp_parent = take(4 * J);
     }
     sp.prog = take(sizeof(Phase) * h->plan.host_program.size());
+    sp.csr_bytes = 0;
+    const size_t blob = h->plan.csr_blob.n;
+    if (blob && off + blob <= (size_t)kSmemLimit) {  // the payoff rows too, when they fit
+        sp.csr = take(blob);
+        sp.csr_bytes = (int)blob;
+        sp.uptr += sp.csr;
+        sp.ucol += sp.csr;
+        sp.uvid += sp.csr;
+        sp.tptr += sp.csr;
+        sp.tcol += sp.csr;
+        sp.tvid += sp.csr;
+        sp.tab += sp.csr;
+    }
     sp.bytes = off > (size_t)INT32_MAX ? INT32_MAX : (int)off;
     return sp.bytes;
 }
 
+// The SMEM engine's copy of U and Uᵀ (offsets into the blob set in sp):
+// int32 row pointers, uint16 columns, uint16 ids into a table of the
+// distinct values (Leduc: 5 520 non-zeros, 12 distinct values; 2 x 26 KB
+// instead of 2 x 70 KB).  Empty when a matrix has >= 65 536 columns or the
+// values >= 65 536 distinct entries.
+static void compact_payoff(scfr_handle* h, SmemPlan& sp) {
+    PersistentPlan& pl = h->plan;
+    const DevCsr* M[2] = {&h->U, &h->UT};
+    std::vector<int> ip[2], ix[2];
+    std::vector<double> d[2];
+    for (int k = 0; k < 2; ++k) {
+        if (M[k]->cols >= 65536 || M[k]->nnz >= (1 << 24)) return;
+        ip[k].resize(M[k]->rows + 1);
+        ix[k].resize(M[k]->nnz);
+        d[k].resize(M[k]->nnz);
+        CUDA_OK(cudaMemcpyAsync(ip[k].data(), M[k]->indptr.p, ip[k].size() * 4, cudaMemcpyDeviceToHost, h->stream));
+        if (M[k]->nnz) {
+            CUDA_OK(cudaMemcpyAsync(ix[k].data(), M[k]->indices.p, ix[k].size() * 4, cudaMemcpyDeviceToHost, h->stream));
+            CUDA_OK(cudaMemcpyAsync(d[k].data(), M[k]->data.p, d[k].size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        }
+    }
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    std::vector<double> tab;  // distinct values, by bit pattern (-0.0 and 0.0 stay apart)
+    std::vector<std::pair<uint64_t, int>> seen;
+    std::vector<unsigned short> vid[2];
+    for (int k = 0; k < 2; ++k) {
+        vid[k].resize(d[k].size());
+        for (size_t e = 0; e < d[k].size(); ++e) {
+            uint64_t bits;
+            std::memcpy(&bits, &d[k][e], 8);
+            int id = -1;
+            for (const auto& s : seen)
+                if (s.first == bits) {
+                    id = s.second;
+                    break;
+                }
+            if (id < 0) {
+                if (tab.size() >= 4096) return;  // (linear probe: keep the table small)
+                id = (int)tab.size();
+                tab.push_back(d[k][e]);
+                seen.emplace_back(bits, id);
+            }
+            vid[k][e] = (unsigned short)id;
+        }
+    }
+    std::vector<unsigned char> blob;
+    auto put = [&](const void* p, size_t bytes) {
+        const int at = (int)blob.size();
+        blob.resize((blob.size() + bytes + 15) & ~size_t(15));
+        if (bytes) std::memcpy(blob.data() + at, p, bytes);
+        return at;
+    };
+    std::vector<unsigned short> col[2];
+    for (int k = 0; k < 2; ++k) col[k].assign(ix[k].begin(), ix[k].end());
+    sp.uptr = put(ip[0].data(), ip[0].size() * 4);
+    sp.ucol = put(col[0].data(), col[0].size() * 2);
+    sp.uvid = put(vid[0].data(), vid[0].size() * 2);
+    sp.tptr = put(ip[1].data(), ip[1].size() * 4);
+    sp.tcol = put(col[1].data(), col[1].size() * 2);
+    sp.tvid = put(vid[1].data(), vid[1].size() * 2);
+    sp.tab = put(tab.data(), tab.size() * 8);
+    pl.csr_blob.alloc(blob.size());
+    CUDA_OK(copy_async(pl.csr_blob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, h->stream));
+}
+
 // Same rule as the level engine: few DPs, >= 8 child-DP references per DP.
 static bool fat_level(const Player& P, int l) {
+    static const bool off = [] {  // SCFR_SMALL_NO_WARP=1: thread per DP everywhere (A/B)
+        const char* e = std::getenv("SCFR_SMALL_NO_WARP");
+        return e && e[0] == '1';
+    }();
+    if (off) return false;
     return (P.lvl_nj[l] <= 4096 && P.lvl_nc[l] >= 8.0 * P.lvl_nj[l]) ||
            (P.lvl_maxa[l] >= kWideActions && P.lvl_maxa[l] <= 32);
 }
@@ -531,10 +640,15 @@ void prepare_persistent(scfr_handle* h) {
     } else {
         pl.ctas = h->B;
         const char* env_small = std::getenv("SCFR_NO_SMEM");
+        const char* env_csr = std::getenv("SCFR_NO_SMEM_PAYOFF");  // A/B: payoff rows from global memory
+        if (!(env_csr && env_csr[0] == '1')) compact_payoff(h, pl.smem);
         pl.small = plan_smem(h, pl.smem) <= kSmemLimit && !(env_small && env_small[0] == '1');
         if (pl.small) {
             pl.threads = kSmallThreads;
-            CUDA_OK(cudaFuncSetAttribute(kSmall, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            int maxa = 2;  // SCFR_SMALL_MAXA: actions held in registers (A/B)
+            if (const char* e = std::getenv("SCFR_SMALL_MAXA")) maxa = std::atoi(e) == 3 ? 3 : 2;
+            pl.small_kern = maxa == 3 ? (const void*)kSmall3 : (const void*)kSmall2;
+            CUDA_OK(cudaFuncSetAttribute(pl.small_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem.bytes));
         }
     }
@@ -584,6 +698,7 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
     a.tdev = h->tdev.p;
     a.barrier = pl.barrier.p;
     a.trace = nullptr;
+    a.csr = pl.csr_blob.p;
     const char* tr = std::getenv("SCFR_PHASE_TRACE");
     DevBuf<long long> trace_buf;
     if (tr && tr[0] == '1' && pl.small) {
@@ -616,8 +731,13 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
             CUDA_OK(cudaLaunchCooperativeKernel((const void*)kGrid, dim3(pl.ctas),
                                                 dim3(pl.threads), args, 0, h->stream));
         } else {
-            if (pl.small) kSmall<<<pl.ctas, pl.threads, pl.smem.bytes, h->stream>>>(a, pl.smem);
-            else kCta<<<pl.ctas, pl.threads, 0, h->stream>>>(a);
+            if (pl.small) {
+                void* args[] = {&a, &pl.smem};
+                CUDA_OK(cudaLaunchKernel(pl.small_kern, dim3(pl.ctas), dim3(pl.threads), args, pl.smem.bytes,
+                                         h->stream));
+            } else {
+                kCta<<<pl.ctas, pl.threads, 0, h->stream>>>(a);
+            }
             CUDA_OK(cudaGetLastError());
         }
         ++launches;

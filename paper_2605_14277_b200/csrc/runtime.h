@@ -184,6 +184,11 @@ struct SmemPlan {
     SmemSide p[2];
     int prog;  // byte offset of the staged phase program
     int bytes;
+    // the payoff rows staged in shared memory (0 bytes: read from global):
+    // per matrix int32 row pointers, uint16 columns and uint16 ids into one
+    // table of the distinct payoff values (csrc/persistent.cu compact_payoff)
+    int csr, csr_bytes;
+    int uptr, ucol, uvid, tptr, tcol, tvid, tab;
 };
 
 struct PersistentPlan {
@@ -191,11 +196,13 @@ struct PersistentPlan {
     bool cluster = false;  // one solve per thread-block cluster of csize CTAs
     int csize = 0;
     bool small = false;  // CTA mode with state + structure resident in shared memory
+    const void* small_kern = nullptr;  // its kernel (k_small<MAXA>)
     SmemPlan smem{};
     int ctas = 0, threads = 0;
     std::vector<Phase> host_program;
     DevBuf<Phase> program;
     DevBuf<unsigned> barrier;  // {count, generation}
+    DevBuf<unsigned char> csr_blob;  // SmemPlan::csr block, staged into shared memory
 };
 
 // Programmatic Dependent Launch (sm_90+): let the next kernel in the stream

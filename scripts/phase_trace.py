@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["SCFR_PHASE_TRACE"] = "1"
 from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, kuhn_poker, leduc_poker  # noqa
 
-for name, game, variant in (("kuhn", kuhn_poker(), "cfr"), ("leduc", leduc_poker(), "cfr+")):
+for name, game, variant in (("kuhn", kuhn_poker(), "cfr"), ("leduc", leduc_poker(), "cfr+"), ("leduc", leduc_poker(), "pcfr+")):
     s = Solver(GameBundle(game), SolverConfig(variant), engine="persistent")
     s.step(5)
     s.synchronize()
