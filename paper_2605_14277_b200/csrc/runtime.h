@@ -128,6 +128,7 @@ struct Player {
     std::vector<int> lvl;                        // DP level starts (process depth), size L+1
     std::vector<double> lvl_ns, lvl_nj, lvl_nc;  // per level: sequences, DPs, child-DP refs
     std::vector<int> lvl_maxa;                   // per level: widest DP (actions)
+    std::vector<int> lvl_pmin;                   // per level: smallest parent sequence of its DPs
     std::vector<int> lvl_s0;                     // per level: first sequence
     std::vector<DevTree> lvl_shape;              // per level: affine shape (pointers unset)
     // int32 host structure, valid only while scfr_create runs (host scratch

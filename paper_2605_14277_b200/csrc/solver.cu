@@ -702,7 +702,7 @@ static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::
 // up to 70 ms on a busy host.)
 struct LevelStat {
     int maxa, mina, par_ok, aff_ok;
-    int c0, cfirst0, pc, pad;
+    int c0, cfirst0, pc, pmin;  // pmin: smallest parent sequence of the level's DPs
     unsigned long long nc;
 };
 
@@ -736,14 +736,17 @@ __global__ void k_level_stats_j(int J, int L, const int* __restrict__ lvl, const
         const int mx = (int)__reduce_max_sync(full, on ? (unsigned)n : 0u);
         const int mn = (int)__reduce_min_sync(full, on ? (unsigned)n : 0xffffffffu);
         const int ak = (int)__reduce_and_sync(full, on ? (unsigned)ok : 1u);
+        const int pm = (int)__reduce_min_sync(full, on ? (unsigned)dp_parent[j] : 0x7fffffffu);
         if ((threadIdx.x & 31) == 0) {
             atomicMax(&st[l0].maxa, mx);
             atomicMin(&st[l0].mina, mn);
+            atomicMin(&st[l0].pmin, pm);
             if (!ak) atomicAnd(&st[l0].par_ok, 0);
         }
     } else if (on) {
         atomicMax(&st[l].maxa, n);
         atomicMin(&st[l].mina, n);
+        atomicMin(&st[l].pmin, dp_parent[j]);
         if (!ok) atomicAnd(&st[l].par_ok, 0);
     }
     if (lp >= 0) {
@@ -777,6 +780,7 @@ static void level_shapes(Player& P, const std::vector<int>& seq_ptr, const std::
     const int L = P.levels(), J = P.J, S = P.S;
     P.lvl_maxa.assign(L, 0);
     P.lvl_nc.assign(L, 0.0);
+    P.lvl_pmin.assign(L, INT32_MAX);
     P.lvl_shape.assign(L, DevTree{nullptr, nullptr, nullptr});
     if (L == 0) {
         CUDA_OK(cudaStreamSynchronize(s));
@@ -787,7 +791,7 @@ static void level_shapes(Player& P, const std::vector<int>& seq_ptr, const std::
         meta[l] = P.lvl[l];
         meta[L + l] = P.lvl_s0[l];
     }
-    std::vector<LevelStat> st(L, LevelStat{0, INT32_MAX, 1, 1, 0, 0, 1, 0, 0ull});
+    std::vector<LevelStat> st(L, LevelStat{0, INT32_MAX, 1, 1, 0, 0, 1, INT32_MAX, 0ull});
     DevBuf<int> dmeta;
     DevBuf<LevelStat> dst;
     dmeta.alloc(meta.size());
@@ -806,6 +810,7 @@ static void level_shapes(Player& P, const std::vector<int>& seq_ptr, const std::
         const LevelStat& t = st[l];
         P.lvl_maxa[l] = t.maxa;
         P.lvl_nc[l] = (double)t.nc;
+        P.lvl_pmin[l] = t.pmin;
         DevTree& sh = P.lvl_shape[l];
         const int j0 = P.lvl[l];
         sh.j_lo = j0;
@@ -2098,8 +2103,8 @@ static void prepare_top(scfr_handle* h, int k) {
     for (int l = lmax; l >= 1; --l) {
         if (P.lvl[l] > kTopDPs) continue;
         const int Stop = sp[P.lvl[l]];
-        bool ok = true;  // DPs below level l hang under forest sequences only
-        for (int q = P.lvl[l + 1]; q < P.J && ok; ++q) ok = par[q] >= Stop;
+        bool ok = true;  // DPs below level l hang under forest sequences only (per-level minima)
+        for (int m = l + 1; m < L && ok; ++m) ok = P.lvl_pmin[m] >= Stop;
         if (ok) {
             ls = l;
             break;
@@ -2260,9 +2265,9 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
         const int w = nccl_id ? world : 1, rk = nccl_id ? rank : 0;
         const int wc = subtree ? 1 : w, rc = subtree ? 0 : rk;  // payoff rows held: all in the subtree mode
         {
-            // two independent pipelines, each on half the host threads:
-            // player 1 then U (its rows are player 1's sequences), and
-            // player 2 then Uᵀ on a second thread
+            // four concurrent tasks (player 1, player 2, U, Uᵀ), a quarter of
+            // the host threads each (2/3 for the players' validation measured
+            // no better: the host is memory-bound across the four)
             const int quarter = std::max(1, host_threads() / 4);
             std::exception_ptr err[4];
             auto task = [&](int k) {
@@ -2376,6 +2381,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                     h->neg_zero_rows.emplace_back(s0, P2.lvl_s0[l] + (int)P2.lvl_ns[l] - s0);
                 }
         }
+        stage("engine choice");
         if (h->engine == SCFR_ENGINE_LEVELS && predictive(h->variant) && h->mode == SCFR_MODE_ALT) {
             const char* nb = std::getenv("SCFR_NO_BCUR");
             h->bcur_on = !(nb && nb[0] == '1');
@@ -2387,9 +2393,11 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             h->leaf_x = l1 || l2;
             if (l2) build_iter_indices(h.get(), h->U, h->P[1]);   // U's columns: player 2's sequences
             if (l1) build_iter_indices(h.get(), h->UT, h->P[0]);  // Uᵀ's columns: player 1's
+            stage("leaf columns");
             // top-down passes recompute the top's x from ancestor chains
             prepare_top(h.get(), 0);
             prepare_top(h.get(), 1);
+            stage("top");
             // alt mode: player 1's next overlaps player 2's observe
             const char* nov = std::getenv("SCFR_NO_OVERLAP");
             if (h->mode == SCFR_MODE_ALT && h->fuse && !(nov && nov[0] == '1') && h->P[0].J > 0 &&
@@ -2402,6 +2410,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             }
         }
         if (subtree) plan_subtree_mode(h.get(), U);
+        stage("streams");
         CUDA_OK(cudaStreamSynchronize(h->stream));
         for (Player& P : h->P) P.h_seq_ptr = P.h_dp_parent = nullptr;  // scratch is reused
         stage("engine");

@@ -65,6 +65,33 @@ def test_corrupt_decision_process_rejected(gpu):
     assert rc == native.EINVAL
 
 
+def test_depth_order_and_child_groups_rejected(gpu):
+    """The fused validation pass (upload_player): DPs out of depth order, and
+    a parent sequence whose child DPs do not form one contiguous group."""
+    b = bundle("leduc")
+    p = b.procs[0]
+    dpn = np.asarray(p.dp_node)
+    depth = np.array(p.depth, dtype=np.int64)
+    dd = depth[dpn]
+    j = int(np.flatnonzero(np.diff(dd) > 0)[-1]) + 1  # first DP of the deepest level
+    depth[dpn[j]] = 10_000  # deeper than the DPs after it
+    t = p.as_c()
+    t.depth = depth.ctypes.data_as(C.POINTER(C.c_int64))
+    rc, _ = _raw_create(b, _cfg(), p1=t)
+    assert rc == native.EINVAL
+    assert b"ordered by depth" in native.lib().scfr_last_error()
+    par = np.array(p.dp_parent_seq, dtype=np.int64)
+    # DPs a, b, c where a and c share a parent and b's differs: give c a's parent
+    ps = par.tolist()
+    k = next(i for i in range(2, len(ps)) if ps[i - 2] != ps[i - 1] and ps[i - 1] != ps[i] and ps[i - 2] < ps[i])
+    par[k] = par[k - 2]
+    t = p.as_c()
+    t.dp_parent_seq = par.ctypes.data_as(C.POINTER(C.c_int64))
+    rc, _ = _raw_create(b, _cfg(), p1=t)
+    assert rc == native.EINVAL
+    assert b"not contiguous" in native.lib().scfr_last_error()
+
+
 def test_bad_column_index_rejected(gpu):
     b = bundle("kuhn")
     U = b.payoff
