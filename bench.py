@@ -483,8 +483,9 @@ def run_ours(args):
         try:
             with open(tfile) as fh:
                 tj = json.load(fh)
-            if args.workload in tj and dname in tj[args.workload]:
-                traffic = tj[args.workload][dname]
+            tw = tj.get(args.workload, {})
+            # the longest launch of the kind (ncu_summary.py "<kind>@top"), else the kind's mean
+            traffic = tw.get(dname + "@top", tw.get(dname))
         except Exception:
             traffic = None
 

@@ -26,7 +26,7 @@ LK = {0: "td_avg", 1: "td", 2: "cur", 3: "obs", 4: "pred"}
 
 
 def kind_of(name: str, predictive: bool) -> str:
-    m = re.search(r"k_level(?:_g)?<(\d+)", name)
+    m = re.search(r"k_level(?:_gp?)?<(\d+)", name)
     if m:
         k = LK[int(m.group(1))]
         if k == "obs" and not predictive:
@@ -63,14 +63,17 @@ def main():
         d[r[col["Metric Name"]]] = val * scale
     seq = list(launches.values())
     ticks = [i for i, d in enumerate(seq) if "k_tick" in d["name"]]
-    # the last tick-to-tick window holding only iteration kernels (creates,
-    # reads and checks run other kernels between iterations)
-    for a, b in reversed(list(zip(ticks, ticks[1:]))):
+    # the longest tick-to-tick window holding only iteration kernels (creates,
+    # reads and checks run other kernels between iterations; with overlapped
+    # alt iterations the last window is the epilogue, a partial iteration)
+    best = None
+    for a, b in zip(ticks, ticks[1:]):
         win = seq[a + 1:b + 1]
         if all("k_level" in d["name"] or "k_tick" in d["name"] or "k_spmv" in d["name"]
-               or "k_avg0" in d["name"] for d in win):
-            seq = win
-            break
+               or "k_avg0" in d["name"] for d in win) and (best is None or len(win) >= len(best)):
+            best = win
+    if best is not None:
+        seq = best
     pred = args.variant in ("pcfr", "pcfr+")
     agg: dict = {}
     for d in seq:
@@ -89,6 +92,14 @@ def main():
         print(f"| {k} | {a['launches']} | {a['seconds'] * 1e6:.1f} | {a['seconds'] / total:.2f} | "
               f"{per:.3e} | {gbs:.0f} |")
         out[k] = per
+    # the longest launch of each kind (bench.py's roofline names the longest
+    # launch of the step): its own DRAM bytes, key "<kind>@top"
+    for k in list(out):
+        ds = [d for d in seq if kind_of(d["name"], pred) == k]
+        top = max(ds, key=lambda d: d.get("gpu__time_duration.sum", 0.0))
+        out[k + "@top"] = top.get("dram__bytes_read.sum", 0.0) + top.get("dram__bytes_write.sum", 0.0)
+        print(f"longest {k}: {top['name'][:60]} grid {top['grid']} {top.get('gpu__time_duration.sum', 0) * 1e6:.1f} us "
+              f"{out[k + '@top'] / 1e6:.2f} MB DRAM")
     db = {}
     if os.path.exists(args.out):
         with open(args.out) as fh:
