@@ -350,8 +350,11 @@ struct scfr_handle {
     // player 1's next of t+1 on a second stream beside player 2's observe and
     // next), epilogue (observe of the last iteration)
     bool overlap = false;
+    int prio_hi = 0;  // the overlapped body's critical stream (B) launch priority (SCFR_NO_PRIO=1: 0)
+    int64_t prio_nj = 1000;  // ... for its launches of at most this many DPs (the top levels)
     cudaStream_t stream2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    bool next1_after = false;
     cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
     int64_t nodes_pro = 0, nodes_body = 0, nodes_epi = 0;
     int64_t launches = 0;
@@ -419,7 +422,7 @@ struct scfr_handle {
         for (cudaGraphExec_t e : {exec_pro, exec_body, exec_epi})
             if (e) cudaGraphExecDestroy(e);
         if (stream2) cudaStreamSynchronize(stream2);
-        for (cudaEvent_t e : {ev_fork, ev_a, ev_b})
+        for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_c})
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
         if (ev0) cudaEventDestroy(ev0);
@@ -437,6 +440,7 @@ struct LaunchBase {
     int64_t count = 0;
     cudaStream_t st = nullptr;  // launch stream (null: the handle's)
     int tofs = 0;               // KParams::tofs of the launches
+    int prio = 0;               // launch priority attribute (0: none; lower = more urgent)
     unsigned long long* tl = nullptr;  // scfr_timeline buffer while capturing its graph
     struct TlRec {
         int kind;
@@ -475,11 +479,16 @@ struct LaunchBase {
         cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st ? st : h->stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (prio) {  // (graphs honour it: instantiated with UseNodePriority)
+            attr[1].id = cudaLaunchAttributePriority;
+            attr[1].val.priority = prio;
+            cfg.numAttrs = 2;
+        }
         CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args...));
     }
     template <class... KArgs, class... Args>

@@ -1297,6 +1297,7 @@ KParams LaunchBase::kparams(bool do_rm) const {
 
 struct Launcher : LaunchBase {
     explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
+    cudaEvent_t mark_first = nullptr;  // recorded after the next level launch (body_t)
     // predictive alt mode: player 1's OBS regret-matches into bcur (instead
     // of b, which PRED still needs) and CUR reads it as a plain TD
     void* bcur_ = nullptr;
@@ -1418,6 +1419,10 @@ struct Launcher : LaunchBase {
         const int parts = forest && h->sub_sim > 1 ? h->sub_sim : 1;
         for (int part = 0; part < parts; ++part)
             level_launch<R>(lk, kk, A, la, Bp, lb, ua, ub, xa, xb, do_rm, vca, vcb, skipa, skipb, part);
+        if (mark_first) {  // overlapped body: the event after stream B's first launch
+            CUDA_OK(cudaEventRecord(mark_first, st ? st : h->stream));
+            mark_first = nullptr;
+        }
         if (!h->subtree || h->sub_sim > 1 || h->sub_view >= 0 || (lk != LK_OBS && lk != LK_PRED)) return;
         const bool ea = A && la >= 0 && la == h->sub_ls[0];
         const bool eb = Bp && lb >= 0 && lb == h->sub_ls[1];
@@ -1662,6 +1667,14 @@ struct Launcher : LaunchBase {
                 }
             }
         }
+        // overlapped body: only stream B's small (latency-bound) launches jump
+        // the queue; its big ones share the SMs with NEXT1's (SCFR_PRIO_NJ)
+        struct PrioGuard {
+            int& p;
+            int saved;
+            ~PrioGuard() { p = saved; }
+        } pg{prio, prio};
+        if (prio && (int64_t)t0.n + t1.n > h->prio_nj) prio = 0;
         if (pkern) {
             int occ = 0;
             CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pkern, TPB, psmem));
@@ -1833,12 +1846,19 @@ struct Launcher : LaunchBase {
         observe_part<R>(true, false);
         CUDA_OK(cudaEventRecord(h->ev_a, A));
         CUDA_OK(cudaStreamWaitEvent(B, h->ev_a, 0));
+        // stream B carries the critical chain from here on: its blocks are
+        // scheduled ahead of NEXT1's when both are pending
         st = B;
+        prio = h->prio_hi;
+        if (h->next1_after) mark_first = h->ev_c;
         observe_part<R>(false, true);
         tofs = 1;
         next_part<R>(false, true);
         CUDA_OK(cudaEventRecord(h->ev_b, B));
+        prio = 0;
         st = A;
+        // SCFR_NEXT1_AFTER=1: NEXT1 starts once OBS2's big first launch is done
+        if (h->next1_after) CUDA_OK(cudaStreamWaitEvent(A, h->ev_c, 0));
         next_part<R>(true, false);
         tofs = 0;
         CUDA_OK(cudaStreamWaitEvent(A, h->ev_b, 0));
@@ -1931,7 +1951,7 @@ static cudaGraphExec_t capture(scfr_handle* h, int64_t& nodes, F&& body) {
     CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     body(L);
     CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
-    CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+    CUDA_OK(cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(graph);
     nodes = L.count;
     return exec;
@@ -2406,7 +2426,14 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+                CUDA_OK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
+                const char* n1a = std::getenv("SCFR_NEXT1_AFTER");
+                h->next1_after = n1a && n1a[0] == '1';
                 h->overlap = true;
+                int lo = 0, hi = 0;
+                const char* npr2 = std::getenv("SCFR_NO_PRIO");
+                if (!(npr2 && npr2[0] == '1') && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) h->prio_hi = hi;
+                if (const char* pn = std::getenv("SCFR_PRIO_NJ")) h->prio_nj = std::atoll(pn);
             }
         }
         if (subtree) plan_subtree_mode(h.get(), U);
@@ -2571,7 +2598,7 @@ int scfr_timeline(scfr_handle* h, int64_t n, scfr_kernel_span* out, int cap, int
         if (h->overlap) L.body();
         else L.iteration();
         CUDA_OK(cudaStreamEndCapture(h->stream, &graph));
-        CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+        CUDA_OK(cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority));
         cudaGraphDestroy(graph);
         const int m = (int)kinds.size();
         if (m > 4096 || m > cap) {
