@@ -308,6 +308,18 @@ __device__ __forceinline__ void small_item(int kind, const SmemPlan& sp, int j, 
     }
 }
 
+// One DP of a top-down phase (thread mode), inline.
+template <int K>
+__device__ __forceinline__ void small_td_item(int kind, const SmemPlan& sp, int j, double w) {
+    const SPtrs P = sptrs<K>(sp);
+    if (kind == PH_TD_AVG) {
+        if (j == 0) P.avg[0] = dadd(dmul(w, P.x[0]), P.avg[0]);
+        td_dp<LdS>(P.T, j, P.b, P.x, P.avg, w);
+    } else {
+        td_dp<LdS>(P.T, j, P.b, P.xpost, nullptr, 0.0);
+    }
+}
+
 // One DP of a fat OBS/PRED phase, warp-wide (lane = action).
 template <int K>
 __device__ __forceinline__ void small_warp_item(int kind, const SmemPlan& sp, int j,
@@ -335,7 +347,7 @@ __device__ __forceinline__ double spmv_row_smem(const SmemPlan& sp, int ptr, int
     return acc;
 }
 
-template <int MAXA, int THREADS>
+template <int MAXA, int THREADS, bool OOL = false>
 __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PArgs a,
                                                    const __grid_constant__ SmemPlan sp) {
     const int solve = blockIdx.x;
@@ -362,7 +374,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
             const Phase ph = prog[p];
             const int total = ph.n1 + ph.n2;
             if (ph.kind < PH_SPMV_U) {
-                if (ph.warp1 | ph.warp2) {  // fat OBS/PRED level: one warp per DP, lane = action
+                if constexpr (OOL) {  // out of line: one call per player and phase
+                    const bool wp = ph.warp1 | ph.warp2;  // fat OBS/PRED level: warps over the DPs
+                    if (ph.kind == PH_TD_AVG || ph.kind == PH_TD_POST) {  // short: stay inline
+#pragma unroll 1
+                        for (int i = rank; i < total; i += size) {
+                            if (i < ph.n1) small_td_item<0>(ph.kind, sp, ph.lo1 + i, w);
+                            else small_td_item<1>(ph.kind, sp, ph.lo2 + (i - ph.n1), w);
+                        }
+                        goto phase_done;
+                    }
+                    const int who = wp ? warp : rank, many = wp ? nwarps : size;
+                    if (ph.n1 > 0) {
+                        const SPtrs P = sptrs<0>(sp);
+                        phase_dps<MAXA, LdS>(ph.kind, P.T, ph.lo1, ph.n1, who, many, P.u, P.r, P.b, P.x, P.xpost,
+                                             P.avg, P.V, w, a.post, pf, nf, a.pred, a.plus, a.nonfinite, wp);
+                    }
+                    if (ph.n2 > 0) {
+                        const SPtrs P = sptrs<1>(sp);
+                        const int b1 = (who + many - ph.n1 % many) % many;  // continue the combined item order
+                        phase_dps<MAXA, LdS>(ph.kind, P.T, ph.lo2, ph.n2, b1, many, P.u, P.r, P.b, P.x, P.xpost,
+                                             P.avg, P.V, w, a.post, pf, nf, a.pred, a.plus, a.nonfinite, wp);
+                    }
+                } else if (ph.warp1 | ph.warp2) {  // fat OBS/PRED level: one warp per DP, lane = action
 #pragma unroll 1
                     for (int i = warp; i < total; i += nwarps) {
                         if (i < ph.n1) small_warp_item<0>(ph.kind, sp, ph.lo1 + i, a, pf, nf, lane);
@@ -395,6 +429,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
                     if (!isfinite(acc)) atomicOr(a.nonfinite, 1);
                 }
             }
+        phase_done:
             if (ph.first_avg && rank == 0) {
                 const SPtrs P0 = sptrs<0>(sp), P1 = sptrs<1>(sp);
                 if (a.J[0] == 0) P0.avg[0] = dadd(dmul(w, P0.x[0]), P0.avg[0]);
@@ -425,6 +460,8 @@ static constexpr auto kClu = k_persistent<PM_CLUSTER, 8, kClusterThreads>;
 static constexpr int kSmallThreads = 256;
 static constexpr auto kSmall2 = k_small<2, kSmallThreads>;
 static constexpr auto kSmall3 = k_small<3, kSmallThreads>;
+static constexpr auto kSmallO2 = k_small<2, kSmallThreads, true>;
+static constexpr auto kSmallO3 = k_small<3, kSmallThreads, true>;
 static constexpr int kSmemLimit = 220 * 1024;
 
 // Byte layout of one solve in the SMEM engine; returns the total size.
@@ -645,9 +682,20 @@ void prepare_persistent(scfr_handle* h) {
         pl.small = plan_smem(h, pl.smem) <= kSmemLimit && !(env_small && env_small[0] == '1');
         if (pl.small) {
             pl.threads = kSmallThreads;
-            int maxa = 2;  // SCFR_SMALL_MAXA: actions held in registers (A/B)
-            if (const char* e = std::getenv("SCFR_SMALL_MAXA")) maxa = std::atoi(e) == 3 ? 3 : 2;
-            pl.small_kern = maxa == 3 ? (const void*)kSmall3 : (const void*)kSmall2;
+            // OBS / PRED / CUR phases out of line with 3 actions in registers
+            // (Leduc's DPs have 2 or 3: no divergent generic path), top-down
+            // phases inline.  SCFR_SMALL_OOL=0 / SCFR_SMALL_MAXA=2: the fully
+            // inlined kernel / 2 actions in registers (A/B).
+            // Games of at most 2 actions (Kuhn) keep the inlined kernel: the
+            // calls cost more than the divergence they remove (7.0 vs 6.1 us).
+            const bool two = std::max(h->P[0].max_actions, h->P[1].max_actions) <= 2;
+            int maxa = two ? 2 : 3;
+            if (const char* e = std::getenv("SCFR_SMALL_MAXA")) maxa = std::atoi(e) == 2 ? 2 : 3;
+            const char* ool = std::getenv("SCFR_SMALL_OOL");
+            if (ool ? ool[0] != '0' : !two)
+                pl.small_kern = maxa == 3 ? (const void*)kSmallO3 : (const void*)kSmallO2;
+            else
+                pl.small_kern = maxa == 3 ? (const void*)kSmall3 : (const void*)kSmall2;
             CUDA_OK(cudaFuncSetAttribute(pl.small_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem.bytes));
         }
