@@ -2001,11 +2001,27 @@ static void read_to_host(scfr_handle* h, double* host_out, const double* dev, si
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return;
     }
-    CUDA_OK(copy_async(stage, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_OK(cudaStreamSynchronize(h->stream));
-    parallel_chunks((int64_t)count, 1 << 16, [&](int, int64_t lo, int64_t hi) {
-        std::memcpy(host_out + lo, stage + lo, (hi - lo) * sizeof(double));
+    // chunked: the copy out of chunk i overlaps the DMA of the chunks after it
+    constexpr int kParts = 8;
+    static cudaEvent_t ev[kParts] = {};
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     });
+    const size_t per = (count + kParts - 1) / kParts;
+    for (int i = 0; i < kParts; ++i) {
+        const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
+        if (n) CUDA_OK(copy_async(stage + lo, dev + lo, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaEventRecord(ev[i], h->stream));
+    }
+    for (int i = 0; i < kParts; ++i) {
+        const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
+        CUDA_OK(cudaEventSynchronize(ev[i]));
+        if (!n) continue;
+        parallel_chunks((int64_t)n, 1 << 16, [&](int, int64_t a, int64_t b) {
+            std::memcpy(host_out + lo + a, stage + lo + a, (b - a) * sizeof(double));
+        });
+    }
 }
 
 static void check_player(const scfr_handle* h, int player, int solve) {
