@@ -17,15 +17,27 @@ cases = [
     ("levels sim cfr", liars, SolverConfig("cfr", mode="sim"), "levels", {}),
     ("levels pipelined groups", goof3, SolverConfig("pcfr+"), "levels",
      {"SCFR_GROUP_NJ": "0", "SCFR_PIPE_NJ": "0", "SCFR_PIPE_KINDS": "31"}),
-    ("persistent (SMEM)", leduc, SolverConfig("cfr+"), "persistent", {}),
+    ("persistent (SMEM, out-of-line phases, payoff in SMEM)", leduc, SolverConfig("cfr+"), "persistent", {}),
+    ("persistent (SMEM, pcfr+)", leduc, SolverConfig("pcfr+"), "persistent", {}),
+    ("persistent (SMEM, inlined, payoff from global)", leduc, SolverConfig("dcfr"), "persistent",
+     {"SCFR_SMALL_OOL": "0", "SCFR_NO_SMEM_PAYOFF": "1"}),
     ("persistent grid barrier", leduc, SolverConfig("cfr+"), "persistent_grid", {}),
     ("persistent cluster barrier", leduc, SolverConfig("pcfr+"), "persistent_cluster", {}),
     ("tiled", goof3, SolverConfig("pcfr+"), "tiled", {}),
 ]
+# subtree-sharded mode over a 1-rank NCCL communicator, and its range-restricted launches
+from paper_2605_14277_b200.distributed import nccl_unique_id  # noqa: E402
+cases += [
+    ("subtree world 1", goof3, SolverConfig("pcfr+"), "subtree", {}),
+    ("subtree simulated 3 ranks", goof3, SolverConfig("cfr", mode="sim"), "subtree", {"SCFR_SUBTREE_SIM": "3"}),
+]
 for name, b, cfg, engine, env in cases:
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
-    s = Solver(b, cfg, engine=engine)
+    if engine == "subtree":
+        s = Solver(b, cfg, engine="levels", subtree=True, shard=(nccl_unique_id(), 0, 1))
+    else:
+        s = Solver(b, cfg, engine=engine)
     s.step(4)
     e, _ = s.exploitability("average")
     s.synchronize()
