@@ -141,6 +141,8 @@ struct Player {
     DevBuf<double> g, W, xbar;                 // best-response scratch, one solve
     DevBuf<double> wide;                       // fp32 mode: a widened read of one vector
     DevBuf<double> bcur;                       // player 1, predictive alt mode: OBS's regret matching, read by CUR
+    DevBuf<double> PV;                         // predictive variants: PRED's DP values (OBS keeps V), so the
+                                               // two passes' levels can overlap (solver.cu body_t)
     DevTree tree() const { return DevTree{seq_ptr.p, dp_parent.p, child.p}; }
     int levels() const { return (int)lvl.size() - 1; }
 };
@@ -354,6 +356,11 @@ struct scfr_handle {
     int64_t prio_nj = 1000;  // ... for its launches of at most this many DPs (the top levels)
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    // player 2's observe above its deepest launch on stream3, gating PRED2
+    // level by level (ev_lv[l]: OBS2 of level l done); opt-in SCFR_OBS_SIDE=1
+    cudaStream_t stream3 = nullptr;
+    static constexpr int kSideLevels = 16;
+    cudaEvent_t ev_side = nullptr, ev_lv[kSideLevels] = {};
     bool next1_after = false;
     cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
     int64_t nodes_pro = 0, nodes_body = 0, nodes_epi = 0;
@@ -422,9 +429,13 @@ struct scfr_handle {
         for (cudaGraphExec_t e : {exec_pro, exec_body, exec_epi})
             if (e) cudaGraphExecDestroy(e);
         if (stream2) cudaStreamSynchronize(stream2);
-        for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_c})
+        if (stream3) cudaStreamSynchronize(stream3);
+        for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_c, ev_side})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_lv)
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
+        if (stream3) cudaStreamDestroy(stream3);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);

@@ -1298,6 +1298,12 @@ KParams LaunchBase::kparams(bool do_rm) const {
 struct Launcher : LaunchBase {
     explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
     cudaEvent_t mark_first = nullptr;  // recorded after the next level launch (body_t)
+    // body_t: player 2's observe levels above its first launch go to obs_side
+    // (event ev_lv[l] after level l), and its PRED / TD wait for them
+    cudaStream_t obs_side = nullptr;
+    bool side_lv[scfr_handle::kSideLevels] = {};
+    int side_last = -1;
+    bool pred_gate = false;
     // predictive alt mode: player 1's OBS regret-matches into bcur (instead
     // of b, which PRED still needs) and CUR reads it as a plain TD
     void* bcur_ = nullptr;
@@ -1429,8 +1435,9 @@ struct Launcher : LaunchBase {
         if (!ea && !eb) return;
         cudaStream_t s = st ? st : h->stream;
         NCCL_OK(nccl().GroupStart());
-        if (ea) broadcast_ranges(h, A->V.p, sizeof(R), h->sub_jb[0][la], s);
-        if (eb) broadcast_ranges(h, Bp->V.p, sizeof(R), h->sub_jb[1][lb], s);
+        auto vbuf = [&](Player* P) { return lk == LK_PRED && P->PV.n ? P->PV.p : P->V.p; };
+        if (ea) broadcast_ranges(h, vbuf(A), sizeof(R), h->sub_jb[0][la], s);
+        if (eb) broadcast_ranges(h, vbuf(Bp), sizeof(R), h->sub_jb[1][lb], s);
         NCCL_OK(nccl().GroupEnd());
     }
 
@@ -1444,6 +1451,10 @@ struct Launcher : LaunchBase {
         TaskT<R> t1 = Bp ? task<R>(*Bp, lb, ub, xb) : TaskT<R>{};
         t0.Vc = vca;
         t1.Vc = vcb;
+        if (lk == LK_PRED) {  // PRED's values in their own buffer (PV) when there is one
+            if (A && A->PV.n) t0.V = vals<R>(A->PV);
+            if (Bp && Bp->PV.n) t1.V = vals<R>(Bp->PV);
+        }
         if (bcur_ && A == &h->P[0]) {
             if (lk == LK_OBS) t0.bw = static_cast<R*>(bcur_);
             else if (lk == LK_TD) t0.b = static_cast<R*>(bcur_);
@@ -1749,6 +1760,9 @@ struct Launcher : LaunchBase {
             };
             for (int k = 0; k < L; ++k) {
                 const int la = LA - 1 - k, lb = LB - 1 - k;
+                // body_t: PRED of player 2's level waits for its observe there
+                if (pred_gate && pb && lb >= 0 && lb < scfr_handle::kSideLevels && side_lv[lb])
+                    CUDA_OK(cudaStreamWaitEvent(st ? st : h->stream, h->ev_lv[lb], 0));
                 level<R>(LK_PRED, KK_PRED, pa, sa && la == LA - 1 ? -1 : la, pb, sb && lb == LB - 1 ? -1 : lb,
                          Au, Bu, Ax, Bx, false, sa && la == LA - 2 ? vc(A, Au) : nullptr,
                          sb && lb == LB - 2 ? vc(Bp, Bu) : nullptr);
@@ -1760,6 +1774,8 @@ struct Launcher : LaunchBase {
                     run1(k_avg0<R>, dim3(h->B), P->S, (const R*)vals<R>(P->x), vals<R>(P->avg),
                          (const double*)h->wsched.p, h->cap, (const long long*)h->tdev.p);
                 });
+        // body_t: the top-down pass follows all of player 2's observe (the join)
+        if (pred_gate && side_last >= 0) CUDA_OK(cudaStreamWaitEvent(st ? st : h->stream, h->ev_lv[side_last], 0));
         // forced leaf levels: their x / avg are the parents' (k_expand_leaf)
         const bool xa = h->leaf_x && leaf_single(A), xb = h->leaf_x && leaf_single(Bp);
         for (int k = 0; k < L; ++k)
@@ -1822,10 +1838,28 @@ struct Launcher : LaunchBase {
         if (part2) {
             if (!fused) spmv<R>(h->UT, Axp, A.S, Bu, Bp.S, true);  // u2 = -Uᵀ x1'
             lf_[1] = leaf_fusable(Bp);
-            for (int k = 0; k < LB; ++k)
-                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, lf_[1] && k == 0 ? -1 : LB - 1 - k,
-                         nullptr, Bu, nullptr, Bx, !pr, nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0,
-                         ob && k == 0);
+            int launched = 0;
+            for (int k = 0; k < LB; ++k) {
+                const int lb = lf_[1] && k == 0 ? -1 : LB - 1 - k;
+                const bool side = obs_side && lb >= 0 && launched > 0 && lb < scfr_handle::kSideLevels;
+                cudaStream_t keep = st;
+                if (side) {
+                    if (side_last < 0) {  // fork after the deepest launch
+                        CUDA_OK(cudaEventRecord(h->ev_side, st));
+                        CUDA_OK(cudaStreamWaitEvent(obs_side, h->ev_side, 0));
+                    }
+                    st = obs_side;
+                }
+                level<R>(LK_OBS, pr ? KK_OBS : KK_OBS_RM, nullptr, -1, &Bp, lb, nullptr, Bu, nullptr, Bx, !pr,
+                         nullptr, ob && k == 1 ? leaf_u(Bp, Bu) : nullptr, 0, ob && k == 0);
+                if (side) {
+                    CUDA_OK(cudaEventRecord(h->ev_lv[lb], obs_side));
+                    side_lv[lb] = true;
+                    side_last = lb;
+                }
+                st = keep;
+                if (lb >= 0) ++launched;
+            }
             lf_[1] = false;
         }
     }
@@ -1851,9 +1885,15 @@ struct Launcher : LaunchBase {
         st = B;
         prio = h->prio_hi;
         if (h->next1_after) mark_first = h->ev_c;
+        obs_side = h->stream3;
+        side_last = -1;
+        for (bool& b : side_lv) b = false;
         observe_part<R>(false, true);
+        obs_side = nullptr;
         tofs = 1;
+        pred_gate = h->stream3 != nullptr;
         next_part<R>(false, true);
+        pred_gate = false;
         CUDA_OK(cudaEventRecord(h->ev_b, B));
         prio = 0;
         st = A;
@@ -2443,6 +2483,17 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
+                // predictive variants, opt-in (SCFR_OBS_SIDE=1; measured slower, 130.5 vs
+                // 122.9 us: the graph's third branch delays PRED2's level 2 behind
+                // stream A's work): player 2's small observe levels on a third
+                // stream beside PRED2's deep ones, PRED in its own value buffer
+                const char* os3 = std::getenv("SCFR_OBS_SIDE");
+                if (predictive(h->variant) && os3 && os3[0] == '1') {
+                    for (Player& P : h->P) P.PV.alloc(val_slots((size_t)std::max(P.J, 1) * h->B, h->f32));
+                    CUDA_OK(cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking));
+                    CUDA_OK(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+                    for (auto& e : h->ev_lv) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                }
                 const char* n1a = std::getenv("SCFR_NEXT1_AFTER");
                 h->next1_after = n1a && n1a[0] == '1';
                 h->overlap = true;

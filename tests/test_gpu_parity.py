@@ -115,6 +115,7 @@ MODES = {
     "pairs": {"SCFR_GROUP_NJ": "0", "SCFR_PAIR": "1"},
     "unfused": {"SCFR_NO_TOP": "1", "SCFR_NO_LEAF_FUSE": "1"},
     "sequential": {"SCFR_NO_OVERLAP": "1"},
+    "obs_side": {"SCFR_OBS_SIDE": "1"},  # (predictive alt cases: OBS2's top levels on a third stream)
 }
 
 
