@@ -304,6 +304,7 @@ constexpr int kTopMax = 8;  // top levels
 struct TopInfo {
     int ls, Stop;      // top levels, top sequences [0, Stop)
     const int* anc;    // [Stop][ls] ancestor sequences top-down (-1 pad; bit 30: forced level, b = 1.0)
+    int pro;           // 1: the level-ls launch also writes the top's x (top_prologue); 0: nobody reads it
 };
 struct TopPlayer {
     bool on = false;
@@ -415,8 +416,11 @@ struct scfr_handle {
     int tile_staged = 1;     // SCFR_TILE_STAGE=0: no shared-memory staging (A/B)
     size_t tile_smem_up = 0, tile_smem_down = 0;
     std::vector<std::pair<const void*, int>> tile_occ;  // resident CTAs per SM, per tile kernel
-    // The level engine's top (prepare_top; SCFR_NO_TOP=1: off)
+    // The level engine's top (prepare_top; SCFR_NO_TOP=1: off), and player 1's
+    // deeper top for its current-strategy pass (alt mode: x1' is read only by
+    // player 2's payoff rows, all of which read level-ls sequences; no prologue)
     scfr::TopPlayer top[2];
+    scfr::TopPlayer top_cur;
     void (*comm_destroy)(void*) = nullptr;  // set with comm (NCCL is dlopen'ed)
     ~scfr_handle() {
         // in-flight async copies / kernels may still use buffers that the

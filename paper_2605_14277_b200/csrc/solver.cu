@@ -122,6 +122,7 @@ template <int KIND, class R>
 __device__ __forceinline__ void top_prologue(const TaskT<R>& t, int blk, R w) {
     const size_t so = (size_t)blockIdx.y * t.S;
     const TopInfo* tp = t.top;
+    if (!tp->pro) return;
     const R* src = t.b + so;
     for (int s = 1 + blk * TPB + (int)threadIdx.x; s < tp->Stop; s += t.nblk * TPB) {
         const R xa = top_x(tp, src, s);
@@ -1298,6 +1299,7 @@ KParams LaunchBase::kparams(bool do_rm) const {
 struct Launcher : LaunchBase {
     explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
     cudaEvent_t mark_first = nullptr;  // recorded after the next level launch (body_t)
+    bool cur_top_ = false;  // player 1's current-strategy pass: its deeper top (h->top_cur)
     // body_t: player 2's observe levels above its first launch go to obs_side
     // (event ev_lv[l] after level l), and its PRED / TD wait for them
     cudaStream_t obs_side = nullptr;
@@ -1464,7 +1466,7 @@ struct Launcher : LaunchBase {
         // the top-down launch of level ls of a player with a top recomputes the top
         auto attach_top = [&](TaskT<R>& t, Player* P, int l) {
             if (!P || (lk != LK_TD_AVG && lk != LK_TD)) return;
-            const TopPlayer& tp = h->top[P == &h->P[0] ? 0 : 1];
+            const TopPlayer& tp = cur_top_ && P == &h->P[0] ? h->top_cur : h->top[P == &h->P[0] ? 0 : 1];
             if (tp.on && l == tp.ls) t.top = tp.info.p;
         };
         attach_top(t0, A, la);
@@ -1830,9 +1832,12 @@ struct Launcher : LaunchBase {
             // current_strategy of player 1 into xpost: TD of the b that OBS
             // already regret-matched (into b, or into bcur for the predictive
             // variants), or RM on the fly (SCFR_NO_BCUR=1)
+            const int fc = h->top_cur.on ? h->top_cur.ls : fa;  // (prepare_cur_top)
+            cur_top_ = h->top_cur.on;
             for (int k = 0; k < LA; ++k)
-                level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : skip(k, fa),
+                level<R>(pr && !bc ? LK_CUR : LK_TD, pr ? KK_CUR : KK_TD, &A, xa && k == LA - 1 ? -1 : skip(k, fc),
                          nullptr, -1, nullptr, nullptr, Axp, nullptr, false);
+            cur_top_ = false;
             bcur_ = nullptr;
         }
         if (part2) {
@@ -2159,6 +2164,53 @@ extern "C" {
 // order, and writes the top's x (and average) once.  Bottom-up passes keep
 // launching every level (completing the top in-kernel by last arrival
 // measured slower than the launches it saved: DESIGN.md §4).
+static void build_top(scfr_handle* h, int k, int ls, int pro, TopPlayer& tp);
+
+__global__ void k_min_index(int n, const int* __restrict__ ix, int* __restrict__ out) {
+    int m = INT32_MAX;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = min(m, ix[i]);
+    m = __reduce_min_sync(0xffffffffu, (unsigned)m);
+    if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
+// Alternating mode: player 1's x' (xpost) is read only through player 2's
+// fused payoff rows.  When every such row reads sequences of the level just
+// below player 1's top (Goofspiel-5: level 3 after the leaf mapping), the
+// current-strategy pass skips that level too: its one launch recomputes each
+// DP's parent x' from a one-level-longer ancestor chain, and x' above it is
+// never written (TopInfo::pro = 0).  One launch fewer on the alternating
+// critical path, but opt-in (SCFR_CUR_TOP=1): the longer chains cost more
+// than the launch (Goofspiel-5 124.4 vs 122.1 us, bit-exact either way).
+static void prepare_cur_top(scfr_handle* h) {
+    const char* on = std::getenv("SCFR_CUR_TOP");
+    if (!(on && on[0] == '1')) return;
+    if (h->mode != SCFR_MODE_ALT || !h->fuse || h->P[0].J == 0 || h->P[1].J == 0 || !h->top[0].on) return;
+    if (predictive(h->variant) && !h->bcur_on) return;  // (CUR regret-matches on the fly: no chain source)
+    Player& P = h->P[0];
+    const int L = P.levels(), lc = h->top[0].ls + 1;
+    const bool xa = h->leaf_x && leaf_single(h, P);
+    if (lc > kTopMax || lc > (xa ? L - 2 : L - 1)) return;
+    const std::vector<int>& sp = *P.h_seq_ptr;
+    const int Stop = sp[P.lvl[lc]];
+    for (int m = lc + 1; m < L; ++m)  // DPs below hang under level->=lc sequences only
+        if (P.lvl_pmin[m] < Stop) return;
+    // every column of player 2's rows (after the leaf mapping) at or below level lc
+    const DevCsr& M = h->UT;
+    if (M.nnz > 0) {
+        DevBuf<int> mn;
+        mn.alloc(1);
+        const int init = INT32_MAX;
+        CUDA_OK(copy_async(mn.p, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
+        k_min_index<<<std::min(grid_for(M.nnz), 4 * h->num_sms), TPB, 0, h->stream>>>(M.nnz, M.iter_indices(), mn.p);
+        CUDA_OK(cudaGetLastError());
+        int v = 0;
+        CUDA_OK(copy_async(&v, mn.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        if (v < Stop) return;
+    }
+    build_top(h, 0, lc, 0, h->top_cur);
+}
+
 static void prepare_top(scfr_handle* h, int k) {
     int kTopDPs = 4096;  // SCFR_TOP_DPS: the cap (A/B: Goofspiel-5 137.4 us at 505 top DPs vs 142.1 us at 24505)
     if (const char* e = std::getenv("SCFR_TOP_DPS")) kTopDPs = std::atoi(e);
@@ -2187,6 +2239,14 @@ static void prepare_top(scfr_handle* h, int k) {
         }
     }
     if (ls == 0) return;
+    build_top(h, k, ls, 1, h->top[k]);
+}
+
+// The ancestor chains of every sequence above level ls of player k (TopInfo).
+static void build_top(scfr_handle* h, int k, int ls, int pro, TopPlayer& tp) {
+    Player& P = h->P[k];
+    const std::vector<int>& sp = *P.h_seq_ptr;
+    const std::vector<int>& par = *P.h_dp_parent;
     const int Jtop = P.lvl[ls], Stop = sp[Jtop];
     std::vector<int> sdp(std::max(Stop, 1), -1), lvl_of(Jtop, 0);
     for (int q = 0; q < Jtop; ++q)
@@ -2203,10 +2263,10 @@ static void prepare_top(scfr_handle* h, int k) {
             anc[(size_t)s * ls + i] = a | (P.lvl_shape[lvl_of[sdp[a]]].un == 1 ? 1 << 30 : 0);
         }
     }
-    TopPlayer& tp = h->top[k];
     TopInfo info{};
     info.ls = ls;
     info.Stop = Stop;
+    info.pro = pro;
     tp.anc.alloc(anc.size());
     CUDA_OK(copy_async(tp.anc.p, anc.data(), anc.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
     info.anc = tp.anc.p;
@@ -2473,6 +2533,7 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // top-down passes recompute the top's x from ancestor chains
             prepare_top(h.get(), 0);
             prepare_top(h.get(), 1);
+            prepare_cur_top(h.get());
             stage("top");
             // alt mode: player 1's next overlaps player 2's observe
             const char* nov = std::getenv("SCFR_NO_OVERLAP");

@@ -116,6 +116,7 @@ MODES = {
     "unfused": {"SCFR_NO_TOP": "1", "SCFR_NO_LEAF_FUSE": "1"},
     "sequential": {"SCFR_NO_OVERLAP": "1"},
     "obs_side": {"SCFR_OBS_SIDE": "1"},  # (predictive alt cases: OBS2's top levels on a third stream)
+    "cur_top": {"SCFR_CUR_TOP": "1"},  # (alt cases: player 1's current strategy from a deeper top)
 }
 
 
