@@ -308,6 +308,34 @@ __device__ __forceinline__ void small_item(int kind, const SmemPlan& sp, int j, 
     }
 }
 
+// A whole top-down pass in one phase (PH_TDC_*): sequence s's x from its
+// ancestor chain, x = b_a·(…·(b_0·x[0])), the products td_dp forms level by
+// level, in the same order (x[0] = 1.0 is never written).
+constexpr int kChainMax = 8;
+template <int K>
+__device__ __forceinline__ void small_chain_item(int kind, const SmemPlan& sp, int s, double w) {
+    const SPtrs P = sptrs<K>(sp);
+    const int* pseq = reinterpret_cast<const int*>(g_smem + sp.p[K].sdp);  // parent sequence, pseq[0] = 0
+    const int depth = sp.chain;  // the longest chain (uniform: no divergence)
+    int anc[kChainMax];
+    int q = s;
+#pragma unroll
+    for (int i = 0; i < kChainMax; ++i) {  // s, its parent sequence, ... (0 past the root)
+        anc[i] = q;
+        if (i < depth) q = pseq[q];
+    }
+    double x = 1.0;
+#pragma unroll
+    for (int i = kChainMax - 1; i >= 0; --i)
+        if (i < depth && anc[i] != 0) x = dmul(P.b[anc[i]], x);
+    if (kind == PH_TDC_AVG) {
+        P.x[s] = x;
+        P.avg[s] = dadd(dmul(w, x), P.avg[s]);
+    } else {
+        P.xpost[s] = x;
+    }
+}
+
 // One DP of a top-down phase (thread mode), inline.
 template <int K>
 __device__ __forceinline__ void small_td_item(int kind, const SmemPlan& sp, int j, double w) {
@@ -361,6 +389,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
         for (int i = threadIdx.x; i < sp.csr_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     __syncthreads();
+    if (sp.p[0].sdp) {  // chain phases: each sequence's parent sequence (0 -> 0)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int* spt = reinterpret_cast<const int*>(g_smem + sp.p[k].seq_ptr);
+            const int* dpp = reinterpret_cast<const int*>(g_smem + sp.p[k].dp_parent);
+            int* pseq = reinterpret_cast<int*>(g_smem + sp.p[k].sdp);
+            if (threadIdx.x == 0) pseq[0] = 0;
+            for (int j = threadIdx.x; j < a.J[k]; j += blockDim.x)
+                for (int s = spt[j]; s < spt[j + 1]; ++s) pseq[s] = dpp[j];
+        }
+        __syncthreads();
+    }
     const int rank = threadIdx.x, size = blockDim.x;
     const int warp = rank >> 5, lane = rank & 31, nwarps = size >> 5;
     long long t_last = clock64();
@@ -373,7 +413,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
         for (int p = 0; p < a.nphase; ++p) {
             const Phase ph = prog[p];
             const int total = ph.n1 + ph.n2;
-            if (ph.kind < PH_SPMV_U) {
+            if (ph.kind >= PH_TDC_AVG) {  // a whole top-down pass (sequences 1.. of each player)
+#pragma unroll 1
+                for (int i = rank; i < total; i += size) {
+                    if (i < ph.n1) small_chain_item<0>(ph.kind, sp, ph.lo1 + i, w);
+                    else small_chain_item<1>(ph.kind, sp, ph.lo2 + (i - ph.n1), w);
+                }
+                if (ph.kind == PH_TDC_AVG && rank == 0) {  // td_dp's avg[0] update at DP 0
+                    const SPtrs P0 = sptrs<0>(sp), P1 = sptrs<1>(sp);
+                    if (a.J[0] > 0) P0.avg[0] = dadd(dmul(w, P0.x[0]), P0.avg[0]);
+                    if (a.J[1] > 0) P1.avg[0] = dadd(dmul(w, P1.x[0]), P1.avg[0]);
+                }
+            } else if (ph.kind < PH_SPMV_U) {
                 if constexpr (OOL) {  // out of line: one call per player and phase
                     const bool wp = ph.warp1 | ph.warp2;  // fat OBS/PRED level: warps over the DPs
                     if (ph.kind == PH_TD_AVG || ph.kind == PH_TD_POST) {  // short: stay inline
@@ -465,7 +516,7 @@ static constexpr auto kSmallO3 = k_small<3, kSmallThreads, true>;
 static constexpr int kSmemLimit = 220 * 1024;
 
 // Byte layout of one solve in the SMEM engine; returns the total size.
-static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
+static int plan_smem(const scfr_handle* h, SmemPlan& sp, bool chain = false) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const int at = (int)off;
@@ -486,6 +537,7 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
         o.child = take(8 * S);
         o.seq_ptr = take(4 * (J + 1));
         o.dp_parent = take(4 * J);
+        o.sdp = chain ? take(4 * S) : 0;
     }
     sp.prog = take(sizeof(Phase) * h->plan.host_program.size());
     sp.csr_bytes = 0;
@@ -493,13 +545,14 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
     if (blob && off + blob <= (size_t)kSmemLimit) {  // the payoff rows too, when they fit
         sp.csr = take(blob);
         sp.csr_bytes = (int)blob;
-        sp.uptr += sp.csr;
-        sp.ucol += sp.csr;
-        sp.uvid += sp.csr;
-        sp.tptr += sp.csr;
-        sp.tcol += sp.csr;
-        sp.tvid += sp.csr;
-        sp.tab += sp.csr;
+        const int* rel = h->plan.csr_rel;
+        sp.uptr = sp.csr + rel[0];
+        sp.ucol = sp.csr + rel[1];
+        sp.uvid = sp.csr + rel[2];
+        sp.tptr = sp.csr + rel[3];
+        sp.tcol = sp.csr + rel[4];
+        sp.tvid = sp.csr + rel[5];
+        sp.tab = sp.csr + rel[6];
     }
     sp.bytes = off > (size_t)INT32_MAX ? INT32_MAX : (int)off;
     return sp.bytes;
@@ -510,7 +563,7 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp) {
 // distinct values (Leduc: 5 520 non-zeros, 12 distinct values; 2 x 26 KB
 // instead of 2 x 70 KB).  Empty when a matrix has >= 65 536 columns or the
 // values >= 65 536 distinct entries.
-static void compact_payoff(scfr_handle* h, SmemPlan& sp) {
+static void compact_payoff(scfr_handle* h) {
     PersistentPlan& pl = h->plan;
     const DevCsr* M[2] = {&h->U, &h->UT};
     std::vector<int> ip[2], ix[2];
@@ -559,13 +612,14 @@ static void compact_payoff(scfr_handle* h, SmemPlan& sp) {
     };
     std::vector<unsigned short> col[2];
     for (int k = 0; k < 2; ++k) col[k].assign(ix[k].begin(), ix[k].end());
-    sp.uptr = put(ip[0].data(), ip[0].size() * 4);
-    sp.ucol = put(col[0].data(), col[0].size() * 2);
-    sp.uvid = put(vid[0].data(), vid[0].size() * 2);
-    sp.tptr = put(ip[1].data(), ip[1].size() * 4);
-    sp.tcol = put(col[1].data(), col[1].size() * 2);
-    sp.tvid = put(vid[1].data(), vid[1].size() * 2);
-    sp.tab = put(tab.data(), tab.size() * 8);
+    int* rel = pl.csr_rel;
+    rel[0] = put(ip[0].data(), ip[0].size() * 4);
+    rel[1] = put(col[0].data(), col[0].size() * 2);
+    rel[2] = put(vid[0].data(), vid[0].size() * 2);
+    rel[3] = put(ip[1].data(), ip[1].size() * 4);
+    rel[4] = put(col[1].data(), col[1].size() * 2);
+    rel[5] = put(vid[1].data(), vid[1].size() * 2);
+    rel[6] = put(tab.data(), tab.size() * 8);
     pl.csr_blob.alloc(blob.size());
     CUDA_OK(copy_async(pl.csr_blob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, h->stream));
 }
@@ -603,14 +657,35 @@ static void push_levels(std::vector<Phase>& prog, int kind, const Player* A, con
     }
 }
 
-static std::vector<Phase> build_program(const scfr_handle* h) {
+// Longest ancestor chain of a sequence (DP levels above it, inclusive), from
+// the host structure of this create.
+static int chain_depth(const scfr_handle* h) {
+    int worst = 0;
+    for (const Player& P : h->P) {
+        if (!P.h_seq_ptr || !P.h_dp_parent) return INT32_MAX;
+        const std::vector<int>& sp = *P.h_seq_ptr;
+        const std::vector<int>& par = *P.h_dp_parent;
+        std::vector<int> sdepth(P.S, 0);  // DPs on the chain of each sequence
+        for (int j = 0; j < P.J; ++j) {
+            const int d = sdepth[par[j]] + 1;  // (parents precede their DPs)
+            for (int s = sp[j]; s < sp[j + 1]; ++s) sdepth[s] = d;
+            worst = std::max(worst, d);
+        }
+    }
+    return worst;
+}
+
+static std::vector<Phase> build_program(const scfr_handle* h, bool chain = false) {
     const Player* A = &h->P[0];
     const Player* Bp = &h->P[1];
     const bool pr = predictive(h->variant);
     std::vector<Phase> prog;
     if (pr) push_levels(prog, PH_PRED, A, Bp, true);
     const size_t first_td = prog.size();
-    push_levels(prog, PH_TD_AVG, A, Bp, false);
+    if (chain)
+        prog.push_back(Phase{PH_TDC_AVG, 1, A->S - 1, 1, Bp->S - 1, 0});
+    else
+        push_levels(prog, PH_TD_AVG, A, Bp, false);
     if (prog.size() == first_td) prog.push_back(Phase{PH_TD_AVG, 0, 0, 0, 0, 0});
     prog[first_td].first_avg = 1;
     if (h->mode == SCFR_MODE_SIM) {
@@ -619,7 +694,10 @@ static std::vector<Phase> build_program(const scfr_handle* h) {
     } else {
         prog.push_back(Phase{PH_SPMV_U, 0, h->U.rows, 0, 0, 0});
         push_levels(prog, PH_OBS, A, nullptr, true);
-        push_levels(prog, pr ? PH_CUR : PH_TD_POST, A, nullptr, false);
+        if (chain && !pr)
+            prog.push_back(Phase{PH_TDC_POST, 1, A->S - 1, 0, 0, 0});
+        else
+            push_levels(prog, pr ? PH_CUR : PH_TD_POST, A, nullptr, false);
         prog.push_back(Phase{PH_SPMV_UT, 0, h->UT.rows, 0, 0, 0});
         push_levels(prog, PH_OBS, nullptr, Bp, true);
     }
@@ -678,8 +756,21 @@ void prepare_persistent(scfr_handle* h) {
         pl.ctas = h->B;
         const char* env_small = std::getenv("SCFR_NO_SMEM");
         const char* env_csr = std::getenv("SCFR_NO_SMEM_PAYOFF");  // A/B: payoff rows from global memory
-        if (!(env_csr && env_csr[0] == '1')) compact_payoff(h, pl.smem);
+        if (!(env_csr && env_csr[0] == '1')) compact_payoff(h);
         pl.small = plan_smem(h, pl.smem) <= kSmemLimit && !(env_small && env_small[0] == '1');
+        // one top-down phase per pass from ancestor chains (SCFR_SMALL_NO_CHAIN=1: per level)
+        const char* nch = std::getenv("SCFR_SMALL_NO_CHAIN");
+        const int depth = pl.small && !(nch && nch[0] == '1') ? chain_depth(h) : INT32_MAX;
+        if (depth <= kChainMax) {
+            pl.smem.chain = depth;
+            pl.host_program = build_program(h, true);
+            if (plan_smem(h, pl.smem, true) <= kSmemLimit) {
+                pl.chain = true;
+            } else {
+                pl.host_program = build_program(h, false);
+                plan_smem(h, pl.smem, false);
+            }
+        }
         if (pl.small) {
             pl.threads = kSmallThreads;
             // OBS / PRED / CUR phases out of line with 3 actions in registers
@@ -795,7 +886,8 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
         CUDA_OK(cudaMemcpyAsync(cyc.data(), a.trace, cyc.size() * sizeof(long long),
                                 cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
-        static const char* names[] = {"td_avg", "td_post", "cur", "obs", "pred", "spmv_u", "spmv_ut", "spmv_both"};
+        static const char* names[] = {"td_avg", "td_post", "cur", "obs", "pred", "spmv_u", "spmv_ut", "spmv_both",
+                                      "tdc_avg", "tdc_post"};
         for (size_t p = 0; p < cyc.size(); ++p) {
             const Phase& ph = pl.host_program[p];
             std::fprintf(stderr, "[phase %2zu] %-9s n1=%6d n2=%6d  %9.1f cycles/iter\n", p,

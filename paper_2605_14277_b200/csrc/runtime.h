@@ -178,10 +178,14 @@ struct Phase {
     int warp1, warp2;  // run this player's DPs warp-per-DP (small fat OBS/PRED levels)
 };
 enum : int { PH_TD_AVG = 0, PH_TD_POST, PH_CUR, PH_OBS, PH_PRED, PH_SPMV_U, PH_SPMV_UT,
-             PH_SPMV_BOTH };
+             PH_SPMV_BOTH,
+             // SMEM engine only: a whole top-down pass in one phase, each sequence's
+             // x from its ancestor chain (items: sequences 1.. of each player)
+             PH_TDC_AVG, PH_TDC_POST };
 
 struct SmemSide {  // byte offsets of one player's arrays in the SMEM engine's buffer
     int r, b, x, xpost, avg, u, V, seq_ptr, dp_parent, child;
+    int sdp;  // sequence -> its DP's parent sequence (the chain top-down phases; 0 when absent)
 };
 struct SmemPlan {
     SmemSide p[2];
@@ -192,6 +196,7 @@ struct SmemPlan {
     // table of the distinct payoff values (csrc/persistent.cu compact_payoff)
     int csr, csr_bytes;
     int uptr, ucol, uvid, tptr, tcol, tvid, tab;
+    int chain;  // chain phases: the longest ancestor chain (DPs)
 };
 
 struct PersistentPlan {
@@ -206,6 +211,8 @@ struct PersistentPlan {
     DevBuf<Phase> program;
     DevBuf<unsigned> barrier;  // {count, generation}
     DevBuf<unsigned char> csr_blob;  // SmemPlan::csr block, staged into shared memory
+    int csr_rel[7] = {};             // uptr, ucol, uvid, tptr, tcol, tvid, tab within the blob
+    bool chain = false;              // SMEM engine: one top-down phase per pass (PH_TDC_*)
 };
 
 // Programmatic Dependent Launch (sm_90+): let the next kernel in the stream
