@@ -312,6 +312,19 @@ __device__ __forceinline__ void small_item(int kind, const SmemPlan& sp, int j, 
 // ancestor chain, x = b_a·(…·(b_0·x[0])), the products td_dp forms level by
 // level, in the same order (x[0] = 1.0 is never written).
 constexpr int kChainMax = 8;
+// PH_RMC: cur_dp's regret matching of DP j (S summed in action order), into bm.
+__device__ __forceinline__ void small_rm_item(const SmemPlan& sp, int j) {
+    const SPtrs P = sptrs<0>(sp);
+    double* bm = reinterpret_cast<double*>(g_smem + sp.p[0].bm);
+    const int s0 = P.T.seq_ptr[j], n = P.T.seq_ptr[j + 1] - s0;
+    double S = 0.0;
+    for (int s = s0; s < s0 + n; ++s) {
+        const double v = P.r[s];
+        S = dadd(S, v > 0.0 ? v : 0.0);
+    }
+    for (int s = s0; s < s0 + n; ++s) bm[s] = rm_prob(P.r[s], S, n);
+}
+
 template <int K>
 __device__ __forceinline__ void small_chain_item(int kind, const SmemPlan& sp, int s, double w) {
     const SPtrs P = sptrs<K>(sp);
@@ -324,10 +337,11 @@ __device__ __forceinline__ void small_chain_item(int kind, const SmemPlan& sp, i
         anc[i] = q;
         if (i < depth) q = pseq[q];
     }
+    const double* bsrc = kind == PH_TDC_CUR ? reinterpret_cast<const double*>(g_smem + sp.p[K].bm) : P.b;
     double x = 1.0;
 #pragma unroll
     for (int i = kChainMax - 1; i >= 0; --i)
-        if (i < depth && anc[i] != 0) x = dmul(P.b[anc[i]], x);
+        if (i < depth && anc[i] != 0) x = dmul(bsrc[anc[i]], x);
     if (kind == PH_TDC_AVG) {
         P.x[s] = x;
         P.avg[s] = dadd(dmul(w, x), P.avg[s]);
@@ -413,7 +427,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_small(const __grid_constant__ PA
         for (int p = 0; p < a.nphase; ++p) {
             const Phase ph = prog[p];
             const int total = ph.n1 + ph.n2;
-            if (ph.kind >= PH_TDC_AVG) {  // a whole top-down pass (sequences 1.. of each player)
+            if (ph.kind == PH_RMC) {  // regret matching of every player-1 DP (no level order)
+#pragma unroll 1
+                for (int i = rank; i < ph.n1; i += size) small_rm_item(sp, ph.lo1 + i);
+            } else if (ph.kind >= PH_TDC_AVG) {  // a whole top-down pass (sequences 1.. of each player)
 #pragma unroll 1
                 for (int i = rank; i < total; i += size) {
                     if (i < ph.n1) small_chain_item<0>(ph.kind, sp, ph.lo1 + i, w);
@@ -538,6 +555,7 @@ static int plan_smem(const scfr_handle* h, SmemPlan& sp, bool chain = false) {
         o.seq_ptr = take(4 * (J + 1));
         o.dp_parent = take(4 * J);
         o.sdp = chain ? take(4 * S) : 0;
+        o.bm = chain && k == 0 && predictive(h->variant) && h->mode == SCFR_MODE_ALT ? take(8 * S) : 0;
     }
     sp.prog = take(sizeof(Phase) * h->plan.host_program.size());
     sp.csr_bytes = 0;
@@ -694,10 +712,14 @@ static std::vector<Phase> build_program(const scfr_handle* h, bool chain = false
     } else {
         prog.push_back(Phase{PH_SPMV_U, 0, h->U.rows, 0, 0, 0});
         push_levels(prog, PH_OBS, A, nullptr, true);
-        if (chain && !pr)
+        if (chain && !pr) {
             prog.push_back(Phase{PH_TDC_POST, 1, A->S - 1, 0, 0, 0});
-        else
+        } else if (chain) {
+            prog.push_back(Phase{PH_RMC, 0, A->J, 0, 0, 0});
+            prog.push_back(Phase{PH_TDC_CUR, 1, A->S - 1, 0, 0, 0});
+        } else {
             push_levels(prog, pr ? PH_CUR : PH_TD_POST, A, nullptr, false);
+        }
         prog.push_back(Phase{PH_SPMV_UT, 0, h->UT.rows, 0, 0, 0});
         push_levels(prog, PH_OBS, nullptr, Bp, true);
     }
@@ -887,7 +909,7 @@ int64_t launch_persistent(scfr_handle* h, int64_t n) {
                                 cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         static const char* names[] = {"td_avg", "td_post", "cur", "obs", "pred", "spmv_u", "spmv_ut", "spmv_both",
-                                      "tdc_avg", "tdc_post"};
+                                      "tdc_avg", "tdc_post", "rmc", "tdc_cur"};
         for (size_t p = 0; p < cyc.size(); ++p) {
             const Phase& ph = pl.host_program[p];
             std::fprintf(stderr, "[phase %2zu] %-9s n1=%6d n2=%6d  %9.1f cycles/iter\n", p,

@@ -181,11 +181,15 @@ enum : int { PH_TD_AVG = 0, PH_TD_POST, PH_CUR, PH_OBS, PH_PRED, PH_SPMV_U, PH_S
              PH_SPMV_BOTH,
              // SMEM engine only: a whole top-down pass in one phase, each sequence's
              // x from its ancestor chain (items: sequences 1.. of each player)
-             PH_TDC_AVG, PH_TDC_POST };
+             PH_TDC_AVG, PH_TDC_POST,
+             // ... and player 1's current strategy (predictive alt): regret
+             // matching of every DP into bm, then the chain product with bm
+             PH_RMC, PH_TDC_CUR };
 
 struct SmemSide {  // byte offsets of one player's arrays in the SMEM engine's buffer
     int r, b, x, xpost, avg, u, V, seq_ptr, dp_parent, child;
     int sdp;  // sequence -> its DP's parent sequence (the chain top-down phases; 0 when absent)
+    int bm;   // player 1, chain CUR: the regret-matched strategy (0 when absent)
 };
 struct SmemPlan {
     SmemSide p[2];
