@@ -289,8 +289,11 @@ __device__ __forceinline__ void level_body_group(const TaskT<R>& t, int blk, con
 #ifndef SCFR_GROUP_MINB
 #define SCFR_GROUP_MINB 8
 #endif
+#ifndef SCFR_GROUP_MINB_OBS
+#define SCFR_GROUP_MINB_OBS SCFR_GROUP_MINB
+#endif
 template <int KIND, int N, class R>
-__global__ void __launch_bounds__(TPB, SCFR_GROUP_MINB) k_level_g(const __grid_constant__ TaskT<R> t0,
+__global__ void __launch_bounds__(TPB, (KIND == LK_OBS ? SCFR_GROUP_MINB_OBS : SCFR_GROUP_MINB)) k_level_g(const __grid_constant__ TaskT<R> t0,
                                                     const __grid_constant__ TaskT<R> t1,
                                                     const __grid_constant__ KParams kp) {
     pdl_launch_dependents();
