@@ -374,6 +374,8 @@ struct scfr_handle {
     static constexpr int kSideLevels = 16;
     cudaEvent_t ev_side = nullptr, ev_lv[kSideLevels] = {};
     bool next1_after = false;
+    static constexpr int kReadParts = 8;
+    cudaEvent_t rd_ev[kReadParts] = {};  // chunked device->host reads (read_to_host)
     cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
     int64_t nodes_pro = 0, nodes_body = 0, nodes_epi = 0;
     int64_t launches = 0;
@@ -448,6 +450,8 @@ struct scfr_handle {
         for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_c, ev_side})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_lv)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : rd_ev)
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
         if (stream3) cudaStreamDestroy(stream3);

@@ -2050,12 +2050,10 @@ static void read_to_host(scfr_handle* h, double* host_out, const double* dev, si
         return;
     }
     // chunked: the copy out of chunk i overlaps the DMA of the chunks after it
-    constexpr int kParts = 8;
-    static cudaEvent_t ev[kParts] = {};
-    static std::once_flag once;
-    std::call_once(once, [] {
-        for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    });
+    constexpr int kParts = scfr_handle::kReadParts;
+    cudaEvent_t* ev = h->rd_ev;  // (the handle's device)
+    if (!ev[0])
+        for (int i = 0; i < kParts; ++i) CUDA_OK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     const size_t per = (count + kParts - 1) / kParts;
     for (int i = 0; i < kParts; ++i) {
         const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;

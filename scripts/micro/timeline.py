@@ -1,14 +1,16 @@
-"""In-graph per-launch timeline of one Goofspiel-5 PCFR+ alt iteration
-(scfr_timeline): python scripts/micro/timeline.py [goof5] [n]"""
+"""In-graph per-launch timeline of one iteration (scfr_timeline):
+python scripts/micro/timeline.py [goof5|goof4|liars6] [n] [variant]"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
-from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, flat_goofspiel  # noqa: E402
+from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, flat_goofspiel, flat_liars_dice  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "goof5"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-s = Solver(GameBundle(flat_goofspiel(int(name[-1]))), SolverConfig("pcfr+"), engine="levels")
+variant = sys.argv[3] if len(sys.argv) > 3 else ("dcfr" if name.startswith("liars") else "pcfr+")
+game = flat_liars_dice(int(name[-1])) if name.startswith("liars") else flat_goofspiel(int(name[-1]))
+s = Solver(GameBundle(game), SolverConfig(variant), engine="levels")
 s.step(5)
 s.synchronize()
 tl = s.timeline(n)
