@@ -412,6 +412,7 @@ struct scfr_handle {
     // sub_sb), the roots' V is broadcast after bottom-up split launches, and
     // reads gather the other ranks' subtrees first (sub_stale)
     void* comm = nullptr;
+    void* comm2 = nullptr;  // subtree mode, overlapped alt body: stream2's communicator (ncclCommSplit)
     int world = 1, rank = 0;
     bool subtree = false, sub_stale = false;
     int sub_ls[2] = {-1, -1};
@@ -440,6 +441,8 @@ struct scfr_handle {
         // member destructors free: drain the stream first (also on a failed
         // create, where this destructor runs from the unique_ptr)
         if (stream) cudaStreamSynchronize(stream);
+        if (comm2 && comm_destroy) comm_destroy(comm2);
+        comm2 = nullptr;
         if (comm && comm_destroy) comm_destroy(comm);
         comm = nullptr;
         if (exec) cudaGraphExecDestroy(exec);

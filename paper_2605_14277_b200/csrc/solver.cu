@@ -1104,6 +1104,7 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -1127,6 +1128,7 @@ static const NcclApi& nccl() {
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     loaded = true;
@@ -1150,13 +1152,16 @@ static void allgather_rows(scfr_handle* h, double* full, int chunk) {
 // Subtree mode: every rank broadcasts its own range [b[r], b[r+1]) of `buf`
 // (elements of `esize` bytes) in place, one NCCL group on `s`.
 static void broadcast_ranges(scfr_handle* h, void* buf, size_t esize, const std::vector<int>& b, cudaStream_t s) {
+    // the second stream of an overlapped body has its own communicator: each
+    // communicator's collectives are issued in one stream order on every rank
+    ncclComm_t comm = (ncclComm_t)(s == h->stream2 && h->comm2 ? h->comm2 : h->comm);
     char* base = static_cast<char*>(buf);
     const ncclDataType_t ty = esize == 8 ? ncclDouble : ncclFloat;
     for (int r = 0; r < h->world; ++r) {
         const size_t cnt = (size_t)(b[r + 1] - b[r]);
         if (cnt) {
             void* p = base + (size_t)b[r] * esize;
-            NCCL_OK(nccl().Broadcast(p, p, cnt, ty, r, (ncclComm_t)h->comm, s));
+            NCCL_OK(nccl().Broadcast(p, p, cnt, ty, r, comm, s));
         }
     }
 }
@@ -2539,12 +2544,17 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // alt mode: player 1's next overlaps player 2's observe
             const char* nov = std::getenv("SCFR_NO_OVERLAP");
             if (h->mode == SCFR_MODE_ALT && h->fuse && !(nov && nov[0] == '1') && h->P[0].J > 0 &&
-                h->P[1].J > 0 && !subtree) {
+                h->P[1].J > 0) {
                 CUDA_OK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
+                if (subtree) {  // stream 2's root exchanges on a second communicator
+                    ncclComm_t c2 = nullptr;
+                    NCCL_OK(nccl().CommSplit((ncclComm_t)h->comm, 0, h->rank, &c2, nullptr));
+                    h->comm2 = c2;
+                }
                 // predictive variants, opt-in (SCFR_OBS_SIDE=1; measured slower, 130.5 vs
                 // 122.9 us: the graph's third branch delays PRED2's level 2 behind
                 // stream A's work): player 2's small observe levels on a third
