@@ -1,4 +1,4 @@
-"""One forest-mode solve (debug aid): python scripts/micro/forest_one.py goof3 cfr alt 1"""
+"""One level-engine solve (debug aid): python scripts/micro/mode_one.py goof3 cfr alt 1"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2605_14277_b200 import GameBundle, Solver, SolverConfig, flat_goofspiel
