@@ -367,13 +367,12 @@ struct scfr_handle {
     int prio_hi = 0;  // the overlapped body's critical stream (B) launch priority (SCFR_NO_PRIO=1: 0)
     int64_t prio_nj = 1000;  // ... for its launches of at most this many DPs (the top levels)
     cudaStream_t stream2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_b = nullptr;
     // player 2's observe above its deepest launch on stream3, gating PRED2
     // level by level (ev_lv[l]: OBS2 of level l done); opt-in SCFR_OBS_SIDE=1
     cudaStream_t stream3 = nullptr;
     static constexpr int kSideLevels = 16;
     cudaEvent_t ev_side = nullptr, ev_lv[kSideLevels] = {};
-    bool next1_after = false;
     static constexpr int kReadParts = 8;
     cudaEvent_t rd_ev[kReadParts] = {};  // chunked device->host reads (read_to_host)
     cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
@@ -450,7 +449,7 @@ struct scfr_handle {
             if (e) cudaGraphExecDestroy(e);
         if (stream2) cudaStreamSynchronize(stream2);
         if (stream3) cudaStreamSynchronize(stream3);
-        for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_c, ev_side})
+        for (cudaEvent_t e : {ev_fork, ev_a, ev_b, ev_side})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_lv)
             if (e) cudaEventDestroy(e);

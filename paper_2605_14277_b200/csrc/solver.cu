@@ -1306,7 +1306,6 @@ KParams LaunchBase::kparams(bool do_rm) const {
 
 struct Launcher : LaunchBase {
     explicit Launcher(scfr_handle* hh) : LaunchBase{hh} {}
-    cudaEvent_t mark_first = nullptr;  // recorded after the next level launch (body_t)
     bool cur_top_ = false;  // player 1's current-strategy pass: its deeper top (h->top_cur)
     // body_t: player 2's observe levels above its first launch go to obs_side
     // (event ev_lv[l] after level l), and its PRED / TD wait for them
@@ -1435,10 +1434,6 @@ struct Launcher : LaunchBase {
         const int parts = forest && h->sub_sim > 1 ? h->sub_sim : 1;
         for (int part = 0; part < parts; ++part)
             level_launch<R>(lk, kk, A, la, Bp, lb, ua, ub, xa, xb, do_rm, vca, vcb, skipa, skipb, part);
-        if (mark_first) {  // overlapped body: the event after stream B's first launch
-            CUDA_OK(cudaEventRecord(mark_first, st ? st : h->stream));
-            mark_first = nullptr;
-        }
         if (!h->subtree || h->sub_sim > 1 || h->sub_view >= 0 || (lk != LK_OBS && lk != LK_PRED)) return;
         const bool ea = A && la >= 0 && la == h->sub_ls[0];
         const bool eb = Bp && lb >= 0 && lb == h->sub_ls[1];
@@ -1897,7 +1892,6 @@ struct Launcher : LaunchBase {
         // scheduled ahead of NEXT1's when both are pending
         st = B;
         prio = h->prio_hi;
-        if (h->next1_after) mark_first = h->ev_c;
         obs_side = h->stream3;
         side_last = -1;
         for (bool& b : side_lv) b = false;
@@ -1910,8 +1904,6 @@ struct Launcher : LaunchBase {
         CUDA_OK(cudaEventRecord(h->ev_b, B));
         prio = 0;
         st = A;
-        // SCFR_NEXT1_AFTER=1: NEXT1 starts once OBS2's big first launch is done
-        if (h->next1_after) CUDA_OK(cudaStreamWaitEvent(A, h->ev_c, 0));
         next_part<R>(true, false);
         tofs = 0;
         CUDA_OK(cudaStreamWaitEvent(A, h->ev_b, 0));
@@ -2549,7 +2541,6 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
                 CUDA_OK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
-                CUDA_OK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
                 if (subtree) {  // stream 2's root exchanges on a second communicator
                     ncclComm_t c2 = nullptr;
                     NCCL_OK(nccl().CommSplit((ncclComm_t)h->comm, 0, h->rank, &c2, nullptr));
@@ -2566,8 +2557,6 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                     CUDA_OK(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
                     for (auto& e : h->ev_lv) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                 }
-                const char* n1a = std::getenv("SCFR_NEXT1_AFTER");
-                h->next1_after = n1a && n1a[0] == '1';
                 h->overlap = true;
                 int lo = 0, hi = 0;
                 const char* npr2 = std::getenv("SCFR_NO_PRIO");
