@@ -221,7 +221,8 @@ int scfr_create_sharded(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
  * in-place broadcast per rank, inside the CUDA graph), so the trunk sees
  * exactly the one-GPU values and iterates stay bit-identical to one GPU.
  * Reads (state, averages, exploitability, expected value) first gather the
- * subtree state of every rank.  Fused level engine, fp64, batch 1.
+ * subtree state of every rank; scfr_status reports what this rank computed
+ * (its subtrees and the trunk).  Fused level engine, fp64, batch 1.
  * Collective like scfr_create_sharded.  SCFR_EINVAL when the game has no such
  * split (trunk rows coupled to subtree columns, fewer closed root blocks than
  * ranks, ...). */
