@@ -172,7 +172,6 @@ inline void resize_pinned(std::vector<int>& v, size_t n) {
 
 struct HostScratch {  // per player (the two upload pipelines run concurrently)
     std::vector<int> sp[2], par[2];  // int32 seq_ptr / dp_parent
-    std::vector<int64_t> dpd[2];     // per DP: depth
 };
 inline HostScratch& host_scratch() {
     static HostScratch* s = new HostScratch();

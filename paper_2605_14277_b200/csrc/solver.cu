@@ -845,40 +845,75 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     HostScratch& hs = host_scratch();  // create_impl holds the arena lock
     std::vector<int>& seq_ptr = hs.sp[slot];
     std::vector<int>& dp_parent = hs.par[slot];
-    std::vector<int64_t>& dpd = hs.dpd[slot];  // depth of each DP's node
     resize_pinned(seq_ptr, J + 1);  // page-locked: uploaded below
     resize_pinned(dp_parent, std::max(J, 1));
-    dpd.resize(std::max(J, 1));
-    // Pass 1 (parallel over j): per-DP checks, int32 conversion.  Each chunk
-    // keeps its first offending j; the smallest one is reported.
+    // One pass (parallel over j): per-DP checks, int32 conversion, the depth
+    // order and level starts (a DP's level is its node's depth), and whether
+    // dp_parent_seq is non-decreasing.  Each chunk keeps its first offending
+    // j; the smallest one is reported.  Reads are sequential: dp_node rises
+    // with j in the reference's breadth-first numbering, so the depth reads
+    // stream too.
     struct Bad {
         int64_t j = INT64_MAX;
         int code = 0;
     };
     const int T = host_threads();
     std::vector<Bad> bad(T);
-    std::vector<int> maxa_c(T, 0);
+    std::vector<int> maxa_c(T, 0), order_bad(T, 0), mono_c(T, 1);
+    std::vector<std::vector<int>> starts(T);
+    const int64_t N = p->num_nodes;
     parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
         Bad bd;
-        int ma = 0;
-        for (int64_t j = lo; j < hi; ++j) {
-            const int64_t fs = p->dp_first_seq[j];
-            const int64_t expect = j == 0 ? 1 : p->dp_first_seq[j - 1] + p->dp_num_actions[j - 1];
-            const int64_t n = p->dp_num_actions[j], ps = p->dp_parent_seq[j], node = p->dp_node[j];
-            const int code = fs != expect ? 1 : n < 1 ? 2 : (ps < 0 || ps >= fs) ? 3
-                           : (node < 0 || node >= p->num_nodes) ? 4 : 0;
-            if (code) {
-                bd.j = j;
-                bd.code = code;
-                break;
+        int ma = 0, ob = 0, mono = 1;
+        std::vector<int>& st = starts[c];
+        st.clear();
+        const int64_t* __restrict__ dfs = p->dp_first_seq;
+        const int64_t* __restrict__ dna = p->dp_num_actions;
+        const int64_t* __restrict__ dps = p->dp_parent_seq;
+        const int64_t* __restrict__ dnd = p->dp_node;
+        const int64_t* __restrict__ dep = p->depth;
+        int* __restrict__ spo = seq_ptr.data();
+        int* __restrict__ pao = dp_parent.data();
+        // the previous DP's depth and parent (chunk boundary; its own chunk validates it)
+        int64_t pd = -1, pp = INT64_MIN;
+        if (lo > 0) {
+            const int64_t nd = dnd[lo - 1];
+            pd = nd >= 0 && nd < N ? dep[nd] : -1;
+            pp = dps[lo - 1];
+        }
+        int64_t j = lo;
+        while (j < hi) {
+            // a run of DPs at depth pd (no level start inside: nothing but
+            // loads, checks and the int32 stores in the loop)
+            int64_t d = pd;
+            for (; j < hi; ++j) {
+                const int64_t fs = dfs[j];
+                const int64_t expect = j == 0 ? 1 : dfs[j - 1] + dna[j - 1];
+                const int64_t n = dna[j], ps = dps[j], node = dnd[j];
+                const int code = fs != expect ? 1 : n < 1 ? 2 : (ps < 0 || ps >= fs) ? 3
+                               : (node < 0 || node >= N) ? 4 : 0;
+                if (code) {
+                    bd.j = j;
+                    bd.code = code;
+                    break;
+                }
+                ma = std::max(ma, (int)n);
+                spo[j] = (int)fs;
+                pao[j] = (int)ps;
+                mono &= ps >= pp;
+                pp = ps;
+                d = dep[node];
+                if (d != pd || j == 0) break;
             }
-            ma = std::max(ma, (int)n);
-            seq_ptr[j] = (int)fs;
-            dp_parent[j] = (int)ps;
-            dpd[j] = p->depth[node];
+            if (bd.code || j >= hi) break;
+            if (j > 0 && d < pd) ob = 1;
+            pd = d;
+            st.push_back((int)j++);
         }
         bad[c] = bd;
         maxa_c[c] = ma;
+        order_bad[c] = ob;
+        mono_c[c] = mono;
     });
     {
         Bad first;
@@ -893,17 +928,18 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     }
     seq_ptr[J] = S;
-    // Pass 2 (parallel): depth order, level starts, and each parent sequence's
-    // child DPs forming one contiguous group (a group start may not repeat).
-    {
+    // Each parent sequence's child DPs form one contiguous group: implied
+    // when dp_parent_seq is non-decreasing (Goofspiel, breadth-first
+    // numbering with one DP per observation); otherwise checked with a
+    // bitmap of group starts (a group start may not repeat).
+    bool mono = true;
+    for (int m : mono_c) mono = mono && m;
+    if (!mono) {
         const size_t W = ((size_t)S + 63) / 64;
         std::unique_ptr<std::atomic<uint64_t>[]> seen(new std::atomic<uint64_t>[W]());
-        std::vector<std::vector<int>> starts(T);
-        std::vector<int> order_bad(T, 0), group_bad(T, 0);
+        std::vector<int> group_bad(T, 0);
         parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
             for (int64_t j = lo; j < hi; ++j) {
-                if (j > 0 && dpd[j] < dpd[j - 1]) order_bad[c] = 1;
-                if (j == 0 || dpd[j] != dpd[j - 1]) starts[c].push_back((int)j);
                 const int ps = dp_parent[j];
                 if (j == 0 || dp_parent[j - 1] != ps) {
                     const uint64_t bit = 1ull << (ps & 63);
@@ -911,14 +947,14 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
                 }
             }
         });
-        for (int c = 0; c < T; ++c) {
+        for (int c = 0; c < T; ++c)
             if (group_bad[c]) fail(SCFR_EINVAL, "child decision points of a sequence are not contiguous");
-            if (order_bad[c]) fail(SCFR_EINVAL, "decision points are not ordered by depth");
-        }
-        P.lvl.clear();
-        for (auto& v : starts) P.lvl.insert(P.lvl.end(), v.begin(), v.end());
-        P.lvl.push_back(J);
     }
+    for (int c = 0; c < T; ++c)
+        if (order_bad[c]) fail(SCFR_EINVAL, "decision points are not ordered by depth");
+    P.lvl.clear();
+    for (auto& v : starts) P.lvl.insert(P.lvl.end(), v.begin(), v.end());
+    P.lvl.push_back(J);
     merge_levels(P, seq_ptr, dp_parent);
     trace_stage("validate+seq_ptr");
     const int L = (int)P.lvl.size() - 1;
@@ -999,16 +1035,24 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, i
         ix = ixv.data();
         dv = nullptr;
     }
+    // (restrict-qualified locals: the loops compile to plain streams)
     parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
-        for (int64_t i = lo; i < hi; ++i) ip[i] = (int)(m->indptr[r0 + i] - k0);
+        const int64_t* __restrict__ src = m->indptr + r0;
+        int* __restrict__ dst = ip;
+        for (int64_t i = lo; i < hi; ++i) dst[i] = (int)(src[i] - k0);
     });
     std::vector<int> badcol(host_threads(), 0);
     parallel_chunks(D.nnz, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
+        const int64_t* __restrict__ src = m->indices + k0;
+        int* __restrict__ dst = ix;
+        const int64_t cols = m->cols;
+        int bad = 0;
         for (int64_t k = lo; k < hi; ++k) {
-            const int64_t col = m->indices[k0 + k];
-            if (col < 0 || col >= m->cols) badcol[c] = 1;
-            ix[k] = (int)col;
+            const int64_t col = src[k];
+            bad |= col < 0 || col >= cols;
+            dst[k] = (int)col;
         }
+        badcol[c] = bad;
         if (dv) std::memcpy(dv + lo, m->data + k0 + lo, (hi - lo) * sizeof(double));
     });
     for (int b : badcol)
