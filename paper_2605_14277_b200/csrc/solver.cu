@@ -664,31 +664,17 @@ static void trace_stage(const char* what) {
 // current range unless one of its parents is a sequence of that range
 // (sequence s belongs to a DP >= start iff s >= seq_ptr[start]).
 // SCFR_NO_LEVEL_MERGE=1 keeps the node-depth levels.
-static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::vector<int>& dp_parent) {
+// lmax[l]: the largest parent sequence of node-depth level l's DPs (from
+// upload_player's validation pass).
+static void merge_levels(Player& P, const std::vector<int>& seq_ptr, const std::vector<int>& lmax) {
     const char* e = std::getenv("SCFR_NO_LEVEL_MERGE");  // per create (tests toggle it)
     const bool off = e && e[0] == '1';
     const int L = (int)P.lvl.size() - 1;
     if (off || L < 2) return;
-    const int T = host_threads();
-    std::vector<std::vector<int>> cmax(T);
-    parallel_chunks(P.J, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
-        std::vector<int> mx(L, -1);
-        if (lo < hi) {
-            int l = (int)(std::upper_bound(P.lvl.begin(), P.lvl.end(), (int)lo) - P.lvl.begin()) - 1;
-            for (int64_t j = lo; j < hi; ++j) {
-                while (j >= P.lvl[l + 1]) ++l;
-                mx[l] = std::max(mx[l], dp_parent[j]);
-            }
-        }
-        cmax[c] = std::move(mx);
-    });
     std::vector<int> merged{0};
     int start = 0;
     for (int l = 1; l < L; ++l) {
-        int mx = -1;
-        for (const auto& v : cmax)
-            if (!v.empty()) mx = std::max(mx, v[l]);
-        if (mx >= seq_ptr[start]) {
+        if (lmax[l] >= seq_ptr[start]) {
             start = P.lvl[l];
             merged.push_back(start);
         }
@@ -860,13 +846,18 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     const int T = host_threads();
     std::vector<Bad> bad(T);
     std::vector<int> maxa_c(T, 0), order_bad(T, 0), mono_c(T, 1);
-    std::vector<std::vector<int>> starts(T);
+    // per chunk: level starts, and the largest parent of each run of one
+    // depth (rmax[c][0]: the run continuing from the previous chunk)
+    std::vector<std::vector<int>> starts(T), rmax(T);
     const int64_t N = p->num_nodes;
     parallel_chunks(J, kGrain, [&](int c, int64_t lo, int64_t hi) {
         Bad bd;
         int ma = 0, ob = 0, mono = 1;
         std::vector<int>& st = starts[c];
+        std::vector<int>& rm = rmax[c];
         st.clear();
+        rm.clear();
+        int64_t run_max = -1;
         const int64_t* __restrict__ dfs = p->dp_first_seq;
         const int64_t* __restrict__ dna = p->dp_num_actions;
         const int64_t* __restrict__ dps = p->dp_parent_seq;
@@ -882,7 +873,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
             pp = dps[lo - 1];
         }
         int64_t j = lo;
-        while (j < hi) {
+        for (;;) {
             // a run of DPs at depth pd (no level start inside: nothing but
             // loads, checks and the int32 stores in the loop)
             int64_t d = pd;
@@ -904,10 +895,14 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
                 pp = ps;
                 d = dep[node];
                 if (d != pd || j == 0) break;
+                run_max = std::max(run_max, ps);
             }
-            if (bd.code || j >= hi) break;
+            if (bd.code) break;
+            rm.push_back((int)run_max);
+            if (j >= hi) break;
             if (j > 0 && d < pd) ob = 1;
             pd = d;
+            run_max = pp;
             st.push_back((int)j++);
         }
         bad[c] = bd;
@@ -953,9 +948,19 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     for (int c = 0; c < T; ++c)
         if (order_bad[c]) fail(SCFR_EINVAL, "decision points are not ordered by depth");
     P.lvl.clear();
-    for (auto& v : starts) P.lvl.insert(P.lvl.end(), v.begin(), v.end());
+    std::vector<int> lmax;
+    for (int c = 0; c < T; ++c) {
+        const std::vector<int>& st = starts[c];
+        const std::vector<int>& rm = rmax[c];
+        if (rm.empty()) continue;  // (chunk not run)
+        if (!lmax.empty()) lmax.back() = std::max(lmax.back(), rm[0]);
+        for (size_t i = 0; i < st.size(); ++i) {
+            P.lvl.push_back(st[i]);
+            lmax.push_back(rm[i + 1]);
+        }
+    }
     P.lvl.push_back(J);
-    merge_levels(P, seq_ptr, dp_parent);
+    merge_levels(P, seq_ptr, lmax);
     trace_stage("validate+seq_ptr");
     const int L = (int)P.lvl.size() - 1;
     P.lvl_ns.assign(L, 0);
