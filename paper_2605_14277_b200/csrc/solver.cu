@@ -706,43 +706,105 @@ __device__ __forceinline__ int find_level(const int* __restrict__ starts, int n,
     return lo;
 }
 
-__global__ void k_level_stats_j(int J, int L, const int* __restrict__ lvl, const int* __restrict__ lvl_s0,
-                                const int* __restrict__ seq_ptr, const int* __restrict__ dp_parent,
-                                const int2* __restrict__ child, LevelStat* __restrict__ st) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool on = j < J;
-    int l = 0, n = 0, ok = 1, lp = -1;
-    if (on) {
-        l = find_level(lvl, L, j);
-        n = seq_ptr[j + 1] - seq_ptr[j];
-        const int j0 = lvl[l], p0 = dp_parent[j0], pc = child[p0].y;
-        const int ps = dp_parent[j];
-        ok = ps == p0 + (j - j0) / pc;
-        if (ps != 0) lp = find_level(lvl_s0, L, ps);
-    }
+// Each block walks a contiguous chunk of DPs (threads strided inside it)
+// and keeps per-thread partials for the level it is in; a partial reaches
+// the level's record (warp-reduced, then one atomic per warp) only when the
+// thread's level changes and at the end.  Levels are long j ranges, so the
+// atomics per level drop from one per warp of the whole process (~70K on
+// Goofspiel-5's last level: 175 us of same-address contention) to a few per
+// block.
+struct StatAcc {
+    int l = -1, mx = 0, mn = INT32_MAX, pm = INT32_MAX, ak = 1;
+    int lp = -1;
+    unsigned long long nc = 0;
+};
+__device__ __forceinline__ void stats_flush_dp(StatAcc& a, LevelStat* st) {
+    // warp-uniform call: every lane flushes its own level's partial
     const unsigned full = 0xffffffffu;
-    const int l0 = __shfl_sync(full, l, 0);
-    if (__all_sync(full, !on || l == l0)) {
-        const int mx = (int)__reduce_max_sync(full, on ? (unsigned)n : 0u);
-        const int mn = (int)__reduce_min_sync(full, on ? (unsigned)n : 0xffffffffu);
-        const int ak = (int)__reduce_and_sync(full, on ? (unsigned)ok : 1u);
-        const int pm = (int)__reduce_min_sync(full, on ? (unsigned)dp_parent[j] : 0x7fffffffu);
-        if ((threadIdx.x & 31) == 0) {
+    const int l0 = __shfl_sync(full, a.l, 0);
+    if (__all_sync(full, a.l == l0)) {
+        const int mx = (int)__reduce_max_sync(full, (unsigned)a.mx);
+        const int mn = (int)__reduce_min_sync(full, (unsigned)a.mn);
+        const int pm = (int)__reduce_min_sync(full, (unsigned)a.pm);
+        const int ak = (int)__reduce_and_sync(full, (unsigned)a.ak);
+        if ((threadIdx.x & 31) == 0 && l0 >= 0) {
             atomicMax(&st[l0].maxa, mx);
             atomicMin(&st[l0].mina, mn);
             atomicMin(&st[l0].pmin, pm);
             if (!ak) atomicAnd(&st[l0].par_ok, 0);
         }
-    } else if (on) {
-        atomicMax(&st[l].maxa, n);
-        atomicMin(&st[l].mina, n);
-        atomicMin(&st[l].pmin, dp_parent[j]);
-        if (!ok) atomicAnd(&st[l].par_ok, 0);
+    } else if (a.l >= 0) {
+        atomicMax(&st[a.l].maxa, a.mx);
+        atomicMin(&st[a.l].mina, a.mn);
+        atomicMin(&st[a.l].pmin, a.pm);
+        if (!a.ak) atomicAnd(&st[a.l].par_ok, 0);
     }
-    if (lp >= 0) {
-        const unsigned m = __match_any_sync(__activemask(), lp);
-        if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&st[lp].nc, (unsigned long long)__popc(m));
+    a.mx = 0;
+    a.mn = INT32_MAX;
+    a.pm = INT32_MAX;
+    a.ak = 1;
+}
+__device__ __forceinline__ void stats_flush_nc(StatAcc& a, LevelStat* st) {
+    const unsigned full = 0xffffffffu;
+    const int l0 = __shfl_sync(full, a.lp, 0);
+    if (__all_sync(full, a.lp == l0)) {
+        unsigned long long v = a.nc;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(full, v, o);
+        if ((threadIdx.x & 31) == 0 && l0 >= 0 && v) atomicAdd(&st[l0].nc, v);
+    } else if (a.lp >= 0 && a.nc) {
+        atomicAdd(&st[a.lp].nc, a.nc);
     }
+    a.nc = 0;
+}
+
+__global__ void k_level_stats_j(int J, int L, const int* __restrict__ lvl, const int* __restrict__ lvl_s0,
+                                const int* __restrict__ seq_ptr, const int* __restrict__ dp_parent,
+                                const int2* __restrict__ child, LevelStat* __restrict__ st) {
+    const int per = (J + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * per, hi = min(J, lo + per);
+    StatAcc a;
+    int j0 = 0, l_end = -1, p0 = 0, pc = 1, lp_lo = 0, lp_hi = -1;
+    // warp-uniform trip count so the flushes' shuffles see every lane
+    for (int base = lo; base < hi; base += blockDim.x) {
+        const int j = base + (int)threadIdx.x;
+        const bool on = j < hi;
+        bool change_dp = false, change_nc = false;
+        int l = a.l, lp = a.lp, n = 0, ps = 0;
+        if (on) {
+            if (j >= l_end) {
+                l = find_level(lvl, L, j);
+                j0 = lvl[l];
+                l_end = l + 1 < L ? lvl[l + 1] : J;
+                p0 = dp_parent[j0];
+                pc = child[p0].y;
+            }
+            n = seq_ptr[j + 1] - seq_ptr[j];
+            ps = dp_parent[j];
+            if (ps != 0 && (ps < lp_lo || ps >= lp_hi)) {
+                lp = find_level(lvl_s0, L, ps);
+                lp_lo = lvl_s0[lp];
+                lp_hi = lp + 1 < L ? lvl_s0[lp + 1] : INT32_MAX;
+            }
+            change_dp = l != a.l;
+            change_nc = ps != 0 && lp != a.lp;
+        }
+        if (__any_sync(0xffffffffu, change_dp)) stats_flush_dp(a, st);
+        if (__any_sync(0xffffffffu, change_nc)) stats_flush_nc(a, st);
+        if (on) {
+            a.l = l;
+            a.mx = max(a.mx, n);
+            a.mn = min(a.mn, n);
+            a.pm = min(a.pm, ps);
+            a.ak &= ps == p0 + (j - j0) / pc;
+            if (ps != 0) {
+                a.lp = lp;
+                ++a.nc;
+            }
+        }
+    }
+    stats_flush_dp(a, st);
+    stats_flush_nc(a, st);
 }
 
 __global__ void k_level_stats_s(int S, int L, const int* __restrict__ lvl_s0, const int2* __restrict__ child,
@@ -789,7 +851,7 @@ static void level_shapes(Player& P, const std::vector<int>& seq_ptr, const std::
     CUDA_OK(copy_async(dmeta.p, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, s));
     CUDA_OK(copy_async(dst.p, st.data(), L * sizeof(LevelStat), cudaMemcpyHostToDevice, s));
     if (J > 0)
-        k_level_stats_j<<<grid_for(J), TPB, 0, s>>>(J, L, dmeta.p, dmeta.p + L, P.seq_ptr.p, P.dp_parent.p,
+        k_level_stats_j<<<std::min(grid_for(J), 1184), TPB, 0, s>>>(J, L, dmeta.p, dmeta.p + L, P.seq_ptr.p, P.dp_parent.p,
                                                  P.child.p, dst.p);
     if (S > 1) k_level_stats_s<<<grid_for(S - 1), TPB, 0, s>>>(S, L, dmeta.p + L, P.child.p, dst.p);
     k_level_stats_fin<<<grid_for(L), TPB, 0, s>>>(L, dmeta.p, dmeta.p + L, P.dp_parent.p, P.child.p, dst.p);
