@@ -2513,8 +2513,10 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // four concurrent tasks (player 1, player 2, U, Uᵀ), a quarter of
             // the host threads each (2/3 for the players' validation measured
             // no better: the host is memory-bound across the four)
+            // (+ a fifth: the first 4096 iterations' schedules, host libm pow,
+            // which the first scfr_step would otherwise compute)
             const int quarter = std::max(1, host_threads() / 4);
-            std::exception_ptr err[4];
+            std::exception_ptr err[5];
             auto task = [&](int k) {
                 try {
                     tl_host_threads = quarter;
@@ -2523,19 +2525,21 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                         case 0: upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32); break;
                         case 1: upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32); break;
                         case 2: upload_csr(U, h->U, h->stream, h->f32, wc, rc); break;
-                        default: upload_csr(UT, h->UT, h->stream, h->f32, wc, rc); break;
+                        case 3: upload_csr(UT, h->UT, h->stream, h->f32, wc, rc); break;
+                        default: ensure_schedule(h.get(), 1); break;
                     }
                 } catch (...) {
                     err[k] = std::current_exception();
                 }
             };
-            std::thread t1(task, 1), t2(task, 2), t3(task, 3);
+            std::thread t1(task, 1), t2(task, 2), t3(task, 3), t4(task, 4);
             const int saved = tl_host_threads;
             task(0);
             tl_host_threads = saved;
             t1.join();
             t2.join();
             t3.join();
+            t4.join();
             for (auto& e : err)
                 if (e) std::rethrow_exception(e);
             csr_level_info(U, h->U, h->P[0], h->stream, wc == 1);  // U's rows: player 1's sequences
