@@ -1072,6 +1072,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
 
 // Uploads rows [row0, row0 + chunk) of the CSR (all rows unless sharded; the
 // last shard may hold fewer), re-based so local row i is global row0 + i.
+void derive_transpose(const DevCsr& U, const scfr_csr* UT, DevCsr& T, cudaStream_t s, bool f32);  // transpose.cu
+
 static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, int world = 1, int rank = 0) {
     if (!m || m->rows < 0 || m->cols < 0 || m->nnz < 0) fail(SCFR_EINVAL, "bad csr");
     if (m->nnz >= (1ll << 31)) fail(SCFR_EINVAL, "csr too large for int32 indexing");
@@ -1171,7 +1173,13 @@ __global__ void k_row_len_stats(int rows, int L, const int* __restrict__ lvl_s0,
     }
 }
 
-static void csr_level_info(const scfr_csr* m, DevCsr& D, const Player& rowP, cudaStream_t s, bool unsharded) {
+void device_row_ptrs(const DevCsr& D, const std::vector<int>& rows, std::vector<int64_t>& out,
+                     cudaStream_t s);  // transpose.cu
+
+// from_device: D was derived on the device (transpose.cu): its row pointers
+// are read from the device copy, not from the caller's arrays.
+static void csr_level_info(const scfr_csr* m, DevCsr& D, const Player& rowP, cudaStream_t s, bool unsharded,
+                           bool from_device = false) {
     const int L = rowP.levels();
     D.h_rows.clear();  // level boundaries of the row player (global rows)
     D.h_ptr.clear();
@@ -1179,9 +1187,10 @@ static void csr_level_info(const scfr_csr* m, DevCsr& D, const Player& rowP, cud
         const int r = l < L ? rowP.lvl_s0[l] : rowP.S;
         if (r >= 0 && r <= m->rows && (D.h_rows.empty() || D.h_rows.back() < r)) {
             D.h_rows.push_back(r);
-            D.h_ptr.push_back(m->indptr[r]);
+            if (!from_device) D.h_ptr.push_back(m->indptr[r]);
         }
     }
+    if (from_device) device_row_ptrs(D, D.h_rows, D.h_ptr, s);
     D.lvl_rowc.assign(unsharded ? L : 0, -1);
     if (!unsharded || L == 0 || D.rows == 0) return;
     std::vector<int> meta(4 * L);  // lvl_s0, level ends, min (init), max (init)
@@ -2514,8 +2523,12 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             // the host threads each (2/3 for the players' validation measured
             // no better: the host is memory-bound across the four)
             // (+ a fifth: the first 4096 iterations' schedules, host libm pow,
-            // which the first scfr_step would otherwise compute)
-            const int quarter = std::max(1, host_threads() / 4);
+            // which the first scfr_step would otherwise compute).  Unsharded,
+            // Uᵀ is derived from U on the device afterwards (transpose.cu), so
+            // three uploads share the threads.
+            const char* hut = std::getenv("SCFR_HOST_UT");
+            const bool dev_ut = wc == 1 && !(hut && hut[0] == '1');
+            const int quarter = std::max(1, host_threads() / (dev_ut ? 3 : 4));
             std::exception_ptr err[5];
             auto task = [&](int k) {
                 try {
@@ -2532,18 +2545,24 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
                     err[k] = std::current_exception();
                 }
             };
-            std::thread t1(task, 1), t2(task, 2), t3(task, 3), t4(task, 4);
+            std::thread t1(task, 1), t2(task, 2), t4(task, 4);
+            std::thread t3;
+            if (!dev_ut) t3 = std::thread(task, 3);
             const int saved = tl_host_threads;
             task(0);
             tl_host_threads = saved;
             t1.join();
             t2.join();
-            t3.join();
+            if (t3.joinable()) t3.join();
             t4.join();
             for (auto& e : err)
                 if (e) std::rethrow_exception(e);
+            if (dev_ut) {
+                AllocStream alloc_t(h->stream);
+                derive_transpose(h->U, UT, h->UT, h->stream, h->f32);
+            }
             csr_level_info(U, h->U, h->P[0], h->stream, wc == 1);  // U's rows: player 1's sequences
-            csr_level_info(UT, h->UT, h->P[1], h->stream, wc == 1);
+            csr_level_info(UT, h->UT, h->P[1], h->stream, wc == 1, dev_ut);
             CUDA_OK(cudaStreamSynchronize(h->stream));
         }
         stage("players+payoff");
