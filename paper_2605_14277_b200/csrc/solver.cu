@@ -2532,13 +2532,15 @@ static void create_impl(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_c
             std::exception_ptr err[5];
             auto task = [&](int k) {
                 try {
+                    CUDA_OK(cudaSetDevice(h->device));  // (per-thread current device)
                     tl_host_threads = quarter;
-                    AllocStream alloc_k(h->stream);
+                    cudaStream_t sk = h->stream;  // (own streams per upload measured no faster: PCIe-bound)
+                    AllocStream alloc_k(sk);
                     switch (k) {
-                        case 0: upload_player(p1, h->P[0], h->B, h->stream, 0, h->f32); break;
-                        case 1: upload_player(p2, h->P[1], h->B, h->stream, 1, h->f32); break;
-                        case 2: upload_csr(U, h->U, h->stream, h->f32, wc, rc); break;
-                        case 3: upload_csr(UT, h->UT, h->stream, h->f32, wc, rc); break;
+                        case 0: upload_player(p1, h->P[0], h->B, sk, 0, h->f32); break;
+                        case 1: upload_player(p2, h->P[1], h->B, sk, 1, h->f32); break;
+                        case 2: upload_csr(U, h->U, sk, h->f32, wc, rc); break;
+                        case 3: upload_csr(UT, h->UT, sk, h->f32, wc, rc); break;
                         default: ensure_schedule(h.get(), 1); break;
                     }
                 } catch (...) {

@@ -143,3 +143,34 @@ def test_nonfinite_payoffs_raise_floating_point_error(gpu):
         s.step(8)
         with pytest.raises(FloatingPointError):
             s.check_finite()
+
+
+def test_transposed_payoff_checked(gpu):
+    """Uᵀ is derived on the device from U (transpose.cu); a caller's Uᵀ that
+    is not U's transpose is rejected, not silently replaced."""
+    b = bundle("leduc")
+    UT = b._c[3]
+    data = np.ctypeslib.as_array(UT.data, shape=(UT.nnz,)).copy()
+    data[0] += 1.0  # one entry off (entry 0 is always probed)
+    bad = native.Csr()
+    C.memmove(C.byref(bad), C.byref(UT), C.sizeof(native.Csr))
+    bad.data = data.ctypes.data_as(C.POINTER(C.c_double))
+    rc, _ = _raw_create(b, _cfg(), UT=bad)
+    assert rc == native.EINVAL
+    assert b"transpose" in native.lib().scfr_last_error()
+
+
+def test_device_transpose_matches_host_upload(gpu, monkeypatch):
+    """Same iterates with the device-derived Uᵀ and with the caller's Uᵀ
+    uploaded (SCFR_HOST_UT=1), on a game with duplicate payoff cells."""
+    for name, variant in (("random6", "cfr"), ("liars3", "dcfr"), ("leduc", "pcfr+")):
+        b = bundle(name)
+        out = []
+        for env in ("0", "1"):
+            monkeypatch.setenv("SCFR_HOST_UT", env)
+            s = Solver(b, SolverConfig(variant), engine="levels")
+            s.step(7)
+            out.append((s.average(1), s.average(2), s.current(1), s.current(2)))
+            s.close()
+        for a, c in zip(*out):
+            assert np.array_equal(a.view(np.uint64), c.view(np.uint64)), name
