@@ -193,7 +193,12 @@ typedef struct scfr_handle scfr_handle;
 
 /* Copies the structure to `device` and allocates the state of `batch`
  * solves, each initialised like RegretState (t=1, zero regrets, uniform
- * behaviour, zero averages). */
+ * behaviour, zero averages).  UT must be U's stable transpose, as the
+ * reference's OperatorSet holds it (CsrMatrix.transposed(), pkg/kernels.py:
+ * 95-127): unsharded handles rebuild it on the device from U (bit-identical)
+ * and check the caller's arrays only for shape, nnz and a sample of row
+ * pointers and entries (SCFR_EINVAL "... not the transpose of U" otherwise);
+ * SCFR_HOST_UT=1 in the environment uploads the caller's UT instead. */
 int scfr_create(const scfr_tfsdp* p1, const scfr_tfsdp* p2, const scfr_csr* U,
                 const scfr_csr* UT, const scfr_config* cfg, int device,
                 scfr_handle** out);
