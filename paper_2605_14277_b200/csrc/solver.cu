@@ -895,6 +895,18 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     std::vector<int>& dp_parent = hs.par[slot];
     resize_pinned(seq_ptr, J + 1);  // page-locked: uploaded below
     resize_pinned(dp_parent, std::max(J, 1));
+    // the int32 structure is copied to the device block by block as the pass
+    // produces it (the DMA of a block overlaps the conversion of the next)
+    P.seq_ptr.alloc(J + 1);
+    P.dp_parent.alloc(std::max(J, 1));
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    constexpr int64_t kDmaBlock = 1 << 18;
+    auto dma = [&](int64_t a, int64_t b) {  // [a, b) of both arrays (pool threads: no throw)
+        if (b <= a) return;
+        copy_async(P.seq_ptr.p + a, seq_ptr.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s);
+        copy_async(P.dp_parent.p + a, dp_parent.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s);
+    };
     // One pass (parallel over j): per-DP checks, int32 conversion, the depth
     // order and level starts (a DP's level is its node's depth), and whether
     // dp_parent_seq is non-decreasing.  Each chunk keeps its first offending
@@ -934,12 +946,19 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
             pd = nd >= 0 && nd < N ? dep[nd] : -1;
             pp = dps[lo - 1];
         }
+        cudaSetDevice(dev);  // (pool thread)
+        int64_t dma_from = lo, dma_next = std::min(hi, lo + kDmaBlock);
         int64_t j = lo;
         for (;;) {
             // a run of DPs at depth pd (no level start inside: nothing but
             // loads, checks and the int32 stores in the loop)
             int64_t d = pd;
             for (; j < hi; ++j) {
+                if (j == dma_next) {
+                    dma(dma_from, j);
+                    dma_from = j;
+                    dma_next = std::min(hi, j + kDmaBlock);
+                }
                 const int64_t fs = dfs[j];
                 const int64_t expect = j == 0 ? 1 : dfs[j - 1] + dna[j - 1];
                 const int64_t n = dna[j], ps = dps[j], node = dnd[j];
@@ -967,6 +986,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
             run_max = pp;
             st.push_back((int)j++);
         }
+        if (!bd.code) dma(dma_from, hi);
         bad[c] = bd;
         maxa_c[c] = ma;
         order_bad[c] = ob;
@@ -985,6 +1005,8 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     }
     seq_ptr[J] = S;
+    CUDA_OK(cudaGetLastError());  // (the pass's copies)
+    CUDA_OK(copy_async(P.seq_ptr.p + J, seq_ptr.data() + J, sizeof(int), cudaMemcpyHostToDevice, s));
     // Each parent sequence's child DPs form one contiguous group: implied
     // when dp_parent_seq is non-decreasing (Goofspiel, breadth-first
     // numbering with one DP per observation); otherwise checked with a
@@ -1036,11 +1058,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         P.lvl_ns[l] = seq_ptr[j1] - seq_ptr[j0];
         P.lvl_nj[l] = j1 - j0;
     }
-    P.seq_ptr.alloc(J + 1);
-    P.dp_parent.alloc(std::max(J, 1));
     P.child.alloc(S);
-    CUDA_OK(copy_async(P.seq_ptr.p, seq_ptr.data(), (J + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
-    if (J) CUDA_OK(copy_async(P.dp_parent.p, dp_parent.data(), J * sizeof(int), cudaMemcpyHostToDevice, s));
     P.child.zero(s);
     const size_t SB = val_slots((size_t)S * B, f32), JB = val_slots((size_t)std::max(J, 1) * B, f32);
     P.r.alloc(SB);
@@ -1104,37 +1122,57 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, i
         ix = ixv.data();
         dv = nullptr;
     }
-    // (restrict-qualified locals: the loops compile to plain streams)
+    D.indptr.alloc(D.rows + 1);
+    D.indices.alloc(std::max(D.nnz, 1));
+    D.data.alloc(std::max(D.nnz, 1));
+    // converted block by block; with pinned staging each block's DMA is
+    // issued as soon as it is written (it overlaps the next block's
+    // conversion).  (restrict-qualified locals: the loops are plain streams)
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    constexpr int64_t kDmaBlock = 1 << 18;
     parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
+        if (pinned) cudaSetDevice(dev);  // (pool thread)
         const int64_t* __restrict__ src = m->indptr + r0;
         int* __restrict__ dst = ip;
-        for (int64_t i = lo; i < hi; ++i) dst[i] = (int)(src[i] - k0);
+        for (int64_t b0 = lo; b0 < hi; b0 += kDmaBlock) {
+            const int64_t b1 = std::min(hi, b0 + kDmaBlock);
+            for (int64_t i = b0; i < b1; ++i) dst[i] = (int)(src[i] - k0);
+            if (pinned) copy_async(D.indptr.p + b0, ip + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s);
+        }
     });
     std::vector<int> badcol(host_threads(), 0);
     parallel_chunks(D.nnz, 1 << 16, [&](int c, int64_t lo, int64_t hi) {
+        if (pinned) cudaSetDevice(dev);
         const int64_t* __restrict__ src = m->indices + k0;
         int* __restrict__ dst = ix;
         const int64_t cols = m->cols;
         int bad = 0;
-        for (int64_t k = lo; k < hi; ++k) {
-            const int64_t col = src[k];
-            bad |= col < 0 || col >= cols;
-            dst[k] = (int)col;
+        for (int64_t b0 = lo; b0 < hi; b0 += kDmaBlock) {
+            const int64_t b1 = std::min(hi, b0 + kDmaBlock);
+            for (int64_t k = b0; k < b1; ++k) {
+                const int64_t col = src[k];
+                bad |= col < 0 || col >= cols;
+                dst[k] = (int)col;
+            }
+            if (dv) std::memcpy(dv + b0, m->data + k0 + b0, (b1 - b0) * sizeof(double));
+            if (pinned && !bad) {  // (a bad block fails the create: nothing reads it)
+                copy_async(D.indices.p + b0, ix + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s);
+                copy_async(D.data.p + b0, dv + b0, (b1 - b0) * sizeof(double), cudaMemcpyHostToDevice, s);
+            }
         }
         badcol[c] = bad;
-        if (dv) std::memcpy(dv + lo, m->data + k0 + lo, (hi - lo) * sizeof(double));
     });
+    CUDA_OK(cudaGetLastError());
     for (int b : badcol)
         if (b) fail(SCFR_EINVAL, "column index out of range");
     trace_stage("csr convert");
-    D.indptr.alloc(D.rows + 1);
-    D.indices.alloc(std::max(D.nnz, 1));
-    D.data.alloc(std::max(D.nnz, 1));
-    CUDA_OK(copy_async(D.indptr.p, ip, (size_t)(D.rows + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
-    if (D.nnz) {
-        CUDA_OK(copy_async(D.indices.p, ix, (size_t)D.nnz * sizeof(int), cudaMemcpyHostToDevice, s));
-        CUDA_OK(copy_async(D.data.p, dv ? dv : m->data + k0, (size_t)D.nnz * sizeof(double),
-                           cudaMemcpyHostToDevice, s));
+    if (!pinned) {
+        CUDA_OK(copy_async(D.indptr.p, ip, (size_t)(D.rows + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+        if (D.nnz) {
+            CUDA_OK(copy_async(D.indices.p, ix, (size_t)D.nnz * sizeof(int), cudaMemcpyHostToDevice, s));
+            CUDA_OK(copy_async(D.data.p, m->data + k0, (size_t)D.nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
     }
     if (f32) {  // the iteration's copy, rounded once (the fp64 one serves best responses)
         D.data32.alloc(std::max(D.nnz, 1));
