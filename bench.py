@@ -413,7 +413,7 @@ def run_ours(args):
         s.step(args.steps)
         s.synchronize()
         t2 = time.perf_counter()
-        avg = (s.average(1), s.average(2))
+        avg = s.averages()
         t3 = time.perf_counter()
         runs.append((t3 - t0, {"create_s": t1 - t0, "steps_s": t2 - t1, "readback_s": t3 - t2}))
         del avg

@@ -266,6 +266,11 @@ int scfr_snapshot(scfr_handle* h, int restore);
 int scfr_iterations(const scfr_handle* h, int64_t* out);
 /* Normalised average strategy avg_accum / avg_weight over Σ (player 1/2). */
 int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out);
+/* Both players' average strategies in one call (RunResult.average, pkg/
+ * solvers.py:129-134 for each RegretState, :436-438): the same values as two
+ * scfr_read_average calls, with player 2's device->host copy overlapping the
+ * copy out of player 1's.  host_out1 / host_out2: num_seqs of player 1 / 2. */
+int scfr_read_averages(scfr_handle* h, int solve, double* host_out1, double* host_out2);
 /* The sequence-form strategy emitted by the last iteration (x1/x2 of _step). */
 int scfr_read_current(scfr_handle* h, int player, int solve, double* host_out);
 #define SCFR_STATE_REGRETS 0  /* [num_seqs-1]  RegretState.regrets   */

@@ -374,7 +374,8 @@ struct scfr_handle {
     static constexpr int kSideLevels = 16;
     cudaEvent_t ev_side = nullptr, ev_lv[kSideLevels] = {};
     static constexpr int kReadParts = 8;
-    cudaEvent_t rd_ev[kReadParts] = {};  // chunked device->host reads (read_to_host)
+    static constexpr int kReadEvents = 2 * kReadParts;  // (two segments: scfr_read_averages)
+    cudaEvent_t rd_ev[kReadEvents] = {};  // chunked device->host reads (read_to_host_multi)
     cudaGraphExec_t exec_pro = nullptr, exec_body = nullptr, exec_epi = nullptr;
     int64_t nodes_pro = 0, nodes_body = 0, nodes_epi = 0;
     int64_t launches = 0;

@@ -2191,38 +2191,67 @@ static void preset_constant_rows(scfr_handle* h) {
 
 // Device -> caller memory for large state reads: DMA into the pinned arena,
 // then a parallel copy out (pageable DMA of a Goofspiel-5 vector is ~3 ms).
-static void read_to_host(scfr_handle* h, double* host_out, const double* dev, size_t count) {
-    if (!count) return;
-    const size_t bytes = count * sizeof(double);
+// Several vectors (segments) share one pipeline: the copy out of a chunk
+// overlaps the DMA of every chunk after it, across segments.
+struct ReadSeg {
+    double* host_out;
+    const double* dev;
+    size_t count;
+};
+static void read_to_host_multi(scfr_handle* h, const ReadSeg* seg, int nseg) {
+    size_t total = 0;
+    for (int k = 0; k < nseg; ++k) total += seg[k].count;
+    if (!total) return;
+    const size_t bytes = total * sizeof(double);
     PinnedArena& pa = pinned_arena();
     std::lock_guard<std::mutex> guard(pa.lock);
     pa.reset();
     double* stage = bytes >= (1u << 20) && pa.reserve(std::max(bytes, pa.cap)) ? static_cast<double*>(pa.take(bytes))
                                                                                : nullptr;
     if (!stage) {
-        CUDA_OK(copy_async(host_out, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+        for (int k = 0; k < nseg; ++k)
+            if (seg[k].count)
+                CUDA_OK(copy_async(seg[k].host_out, seg[k].dev, seg[k].count * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return;
     }
-    // chunked: the copy out of chunk i overlaps the DMA of the chunks after it
-    constexpr int kParts = scfr_handle::kReadParts;
-    cudaEvent_t* ev = h->rd_ev;  // (the handle's device)
+    constexpr int kParts = scfr_handle::kReadParts;  // chunks per segment
+    cudaEvent_t* ev = h->rd_ev;                      // (the handle's device)
     if (!ev[0])
-        for (int i = 0; i < kParts; ++i) CUDA_OK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-    const size_t per = (count + kParts - 1) / kParts;
-    for (int i = 0; i < kParts; ++i) {
-        const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
-        if (n) CUDA_OK(copy_async(stage + lo, dev + lo, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CUDA_OK(cudaEventRecord(ev[i], h->stream));
+        for (int i = 0; i < scfr_handle::kReadEvents; ++i)
+            CUDA_OK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    size_t base = 0;
+    for (int k = 0; k < nseg; ++k) {
+        const size_t count = seg[k].count, per = (count + kParts - 1) / kParts;
+        for (int i = 0; i < kParts; ++i) {
+            const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
+            if (n)
+                CUDA_OK(copy_async(stage + base + lo, seg[k].dev + lo, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h->stream));
+            CUDA_OK(cudaEventRecord(ev[k * kParts + i], h->stream));
+        }
+        base += count;
     }
-    for (int i = 0; i < kParts; ++i) {
-        const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
-        CUDA_OK(cudaEventSynchronize(ev[i]));
-        if (!n) continue;
-        parallel_chunks((int64_t)n, 1 << 16, [&](int, int64_t a, int64_t b) {
-            std::memcpy(host_out + lo + a, stage + lo + a, (b - a) * sizeof(double));
-        });
+    base = 0;
+    for (int k = 0; k < nseg; ++k) {
+        const size_t count = seg[k].count, per = (count + kParts - 1) / kParts;
+        double* out = seg[k].host_out;
+        for (int i = 0; i < kParts; ++i) {
+            const size_t lo = std::min(count, i * per), n = std::min(count, lo + per) - lo;
+            CUDA_OK(cudaEventSynchronize(ev[k * kParts + i]));
+            if (!n) continue;
+            const double* src = stage + base + lo;
+            parallel_chunks((int64_t)n, 1 << 16, [&](int, int64_t a, int64_t b) {
+                std::memcpy(out + lo + a, src + a, (b - a) * sizeof(double));
+            });
+        }
+        base += count;
     }
+}
+static void read_to_host(scfr_handle* h, double* host_out, const double* dev, size_t count) {
+    const ReadSeg seg{host_out, dev, count};
+    read_to_host_multi(h, &seg, 1);
 }
 
 static void check_player(const scfr_handle* h, int player, int solve) {
@@ -3071,6 +3100,27 @@ int scfr_read_average(scfr_handle* h, int player, int solve, double* host_out) {
         k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
         CUDA_OK(cudaGetLastError());
         read_to_host(h, host_out, P.xbar.p, P.S);
+    });
+}
+
+int scfr_read_averages(scfr_handle* h, int solve, double* host_out1, double* host_out2) {
+    NvtxRange nvtx("scfr_read_averages");
+    return guarded([&] {
+        check_player(h, 1, solve);
+        if (!host_out1 || !host_out2) fail(SCFR_EINVAL, "NULL argument");
+        if (h->avg_weight[solve] == 0.0) fail(SCFR_EINVAL, "no strategies accumulated yet");
+        set_device(h);
+        gather_subtrees(h);
+        ReadSeg seg[2];
+        for (int k = 0; k < 2; ++k) {  // both normalisations queued before the first DMA
+            Player& P = h->P[k];
+            expand_leaves(h, k + 1, P.avg, solve);
+            const double* avg = orig_order(h, k + 1, P.avg.p, solve);
+            k_normalize<<<grid_for(P.S), TPB, 0, h->stream>>>(avg, h->avg_weight[solve], P.xbar.p, P.S);
+            CUDA_OK(cudaGetLastError());
+            seg[k] = ReadSeg{k == 0 ? host_out1 : host_out2, P.xbar.p, (size_t)P.S};
+        }
+        read_to_host_multi(h, seg, 2);
     });
 }
 

@@ -120,6 +120,7 @@ _SIGS = {
     "scfr_snapshot": ([C.c_void_p, C.c_int], C.c_int),
     "scfr_iterations": ([C.c_void_p, i64p], C.c_int),
     "scfr_read_average": ([C.c_void_p, C.c_int, C.c_int, f64p], C.c_int),
+    "scfr_read_averages": ([C.c_void_p, C.c_int, f64p, f64p], C.c_int),
     "scfr_read_current": ([C.c_void_p, C.c_int, C.c_int, f64p], C.c_int),
     "scfr_read_state": ([C.c_void_p, C.c_int, C.c_int, C.c_int, f64p], C.c_int),
     "scfr_avg_weight": ([C.c_void_p, C.c_int, C.c_int, f64p], C.c_int),

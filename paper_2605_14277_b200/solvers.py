@@ -263,6 +263,12 @@ class Solver:
         N.check(N.lib().scfr_read_average(self._h, player, solve, N.ptr(out, C.c_double)))
         return out
 
+    def averages(self, solve: int = 0) -> tuple[np.ndarray, np.ndarray]:
+        """Both players' average strategies (one pipelined read)."""
+        o1, o2 = np.empty(self._nseq(1)), np.empty(self._nseq(2))
+        N.check(N.lib().scfr_read_averages(self._h, solve, N.ptr(o1, C.c_double), N.ptr(o2, C.c_double)))
+        return o1, o2
+
     def current(self, player: int, solve: int = 0) -> np.ndarray:
         out = np.empty(self._nseq(player))
         N.check(N.lib().scfr_read_current(self._h, player, solve, N.ptr(out, C.c_double)))
@@ -408,7 +414,7 @@ def run(game, config: SolverConfig, iterations: int | None = None,
             break
     solver.check_finite()
     result = RunResult(bundle=bundle, config=config,
-                       average=(solver.average(1), solver.average(2)),
+                       average=solver.averages(),
                        last_iterates=(solver.current(1), solver.current(2)),
                        records=records, iterations=t)
     solver.close()
