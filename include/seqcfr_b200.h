@@ -14,6 +14,7 @@
  *   scfr_create             RegretState x2 allocation     pkg/solvers.py:97-127, :404-405
  *   scfr_step               the `while True: _step(...)`  pkg/solvers.py:351-372, :424-434
  *   scfr_read_average       RegretState.average_strategy  pkg/solvers.py:129-134
+ *   scfr_read_averages      RunResult.average (both)      pkg/solvers.py:129-134, :436-438
  *   scfr_read_current       the x1, x2 returned by _step  pkg/solvers.py:372
  *   scfr_exploitability     metrics.exploitability        pkg/metrics.py:59-75
  *                           (+ oracle.scalar_best_response pkg/oracle.py:186-221)
