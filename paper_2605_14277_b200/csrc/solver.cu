@@ -902,10 +902,14 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
     int dev = 0;
     CUDA_OK(cudaGetDevice(&dev));
     constexpr int64_t kDmaBlock = 1 << 18;
-    auto dma = [&](int64_t a, int64_t b) {  // [a, b) of both arrays (pool threads: no throw)
+    std::atomic<int> dma_err{0};  // (pool threads do not throw: checked after the pass)
+    auto dma = [&](int64_t a, int64_t b) {  // [a, b) of both arrays
         if (b <= a) return;
-        copy_async(P.seq_ptr.p + a, seq_ptr.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s);
-        copy_async(P.dp_parent.p + a, dp_parent.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s);
+        if (copy_async(P.seq_ptr.p + a, seq_ptr.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s) !=
+                cudaSuccess ||
+            copy_async(P.dp_parent.p + a, dp_parent.data() + a, (b - a) * sizeof(int), cudaMemcpyHostToDevice, s) !=
+                cudaSuccess)
+            dma_err = 1;
     };
     // One pass (parallel over j): per-DP checks, int32 conversion, the depth
     // order and level starts (a DP's level is its node's depth), and whether
@@ -1005,7 +1009,7 @@ static void upload_player(const scfr_tfsdp* p, Player& P, int B, cudaStream_t s,
         if (next != S) fail(SCFR_EINVAL, "num_seqs does not match the action counts");
     }
     seq_ptr[J] = S;
-    CUDA_OK(cudaGetLastError());  // (the pass's copies)
+    if (dma_err) fail(SCFR_ECUDA, "structure upload failed");
     CUDA_OK(copy_async(P.seq_ptr.p + J, seq_ptr.data() + J, sizeof(int), cudaMemcpyHostToDevice, s));
     // Each parent sequence's child DPs form one contiguous group: implied
     // when dp_parent_seq is non-decreasing (Goofspiel, breadth-first
@@ -1131,6 +1135,7 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, i
     int dev = 0;
     CUDA_OK(cudaGetDevice(&dev));
     constexpr int64_t kDmaBlock = 1 << 18;
+    std::atomic<int> dma_err{0};  // (pool threads do not throw: checked after the pass)
     parallel_chunks(D.rows + 1, 1 << 16, [&](int, int64_t lo, int64_t hi) {
         if (pinned) cudaSetDevice(dev);  // (pool thread)
         const int64_t* __restrict__ src = m->indptr + r0;
@@ -1138,7 +1143,9 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, i
         for (int64_t b0 = lo; b0 < hi; b0 += kDmaBlock) {
             const int64_t b1 = std::min(hi, b0 + kDmaBlock);
             for (int64_t i = b0; i < b1; ++i) dst[i] = (int)(src[i] - k0);
-            if (pinned) copy_async(D.indptr.p + b0, ip + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s);
+            if (pinned && copy_async(D.indptr.p + b0, ip + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s) !=
+                              cudaSuccess)
+                dma_err = 1;
         }
     });
     std::vector<int> badcol(host_threads(), 0);
@@ -1156,16 +1163,18 @@ static void upload_csr(const scfr_csr* m, DevCsr& D, cudaStream_t s, bool f32, i
                 dst[k] = (int)col;
             }
             if (dv) std::memcpy(dv + b0, m->data + k0 + b0, (b1 - b0) * sizeof(double));
-            if (pinned && !bad) {  // (a bad block fails the create: nothing reads it)
-                copy_async(D.indices.p + b0, ix + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s);
-                copy_async(D.data.p + b0, dv + b0, (b1 - b0) * sizeof(double), cudaMemcpyHostToDevice, s);
-            }
+            if (pinned && !bad &&  // (a bad block fails the create: nothing reads it)
+                (copy_async(D.indices.p + b0, ix + b0, (b1 - b0) * sizeof(int), cudaMemcpyHostToDevice, s) !=
+                     cudaSuccess ||
+                 copy_async(D.data.p + b0, dv + b0, (b1 - b0) * sizeof(double), cudaMemcpyHostToDevice, s) !=
+                     cudaSuccess))
+                dma_err = 1;
         }
         badcol[c] = bad;
     });
-    CUDA_OK(cudaGetLastError());
     for (int b : badcol)
         if (b) fail(SCFR_EINVAL, "column index out of range");
+    if (dma_err) fail(SCFR_ECUDA, "payoff upload failed");
     trace_stage("csr convert");
     if (!pinned) {
         CUDA_OK(copy_async(D.indptr.p, ip, (size_t)(D.rows + 1) * sizeof(int), cudaMemcpyHostToDevice, s));

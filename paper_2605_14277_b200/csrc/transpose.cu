@@ -69,8 +69,8 @@ void derive_transpose(const DevCsr& U, const scfr_csr* UT, DevCsr& T, cudaStream
     const int rows = U.cols, cols = U.rows, nnz = U.nnz;
     if (!UT || UT->rows != rows || UT->cols != cols || UT->nnz != nnz)
         fail(SCFR_EINVAL, "the transposed payoff matrix does not have U's transposed shape");
-    if (!UT->indptr || UT->indptr[0] != 0 || UT->indptr[rows] != nnz)
-        fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
+    if (!UT->indptr || (nnz > 0 && (!UT->indices || !UT->data))) fail(SCFR_EINVAL, "csr has a NULL array");
+    if (UT->indptr[0] != 0 || UT->indptr[rows] != nnz) fail(SCFR_EINVAL, "indptr must start at 0 and end at nnz");
     T.full_rows = rows;
     T.row0 = 0;
     T.chunk = rows;
